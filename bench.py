@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark: batched soft-snake frames on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A "step" is one frame (dt = 1/60 s: 1 pneumatic tick, 2 substeps x 4 Newton
+x 20 PCR) of every environment. Workload (BASELINE.json configs[2]): 1024
+independent 4-link snakes per GPU, default gait with a per-env turn bias and
+time offset (seeded), latency on. Multi-GPU: one process per GPU, env slices
+(weak scaling, no data-path collective); an NCCL all_gather of per-env COM
+runs once after timing. Rank 0 prints one JSON line.
+
+The oracle (oracle/) appears only in the cpu_baseline leg and in
+--impl reference, where the reference's algorithm (its C restatement) is
+timed on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "snake-steps/sec (batched, device-timed) & real-time factor; % HBM roofline"
+UNIT = "snake-steps/s"
+WORKLOAD = "1024 independent snakes batched on 1xB200 (RL rollout shape), per GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--envs", type=int, default=1024, help="environments per GPU")
+    ap.add_argument("--profile-frames", type=int, default=2)
+    ap.add_argument("--cpu-frames", type=int, default=6, help="oracle frames per host core")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def env_commands(n_envs: int, frames: int, first_frame: int, env0: int = 0):
+    """[frames, n_envs, 4] gait commands: per-env turn bias and time offset
+    from the conftest seed."""
+    import paper_1904_02833_b200 as M
+    sc = M.SceneConfig()
+    rng = np.random.default_rng(20260817)
+    bias_all = rng.uniform(-0.5, 0.5, env0 + n_envs)
+    t0_all = rng.uniform(0.0, 0.5, env0 + n_envs)
+    bias, t0 = bias_all[env0:], t0_all[env0:]
+    w = 2.0 * np.pi * sc.frequency
+    i = np.arange(4)
+    t = t0[None, :] + (first_frame + np.arange(frames))[:, None] * sc.dt
+    raw = np.sin(w * t[..., None] + sc.phase_offset * i) + bias[None, :, None]
+    return np.ascontiguousarray(np.clip(raw, -1.0, 1.0) * sc.amplitude_psi)
+
+
+# ----------------------------------------------------------------- CPU leg
+def cpu_oracle_rate(frames_per_core: int, cores: int | None = None):
+    """The reference algorithm (oracle C port) on all host cores: one snake
+    per core, frames_per_core frames each, threads released from the GIL by
+    ctypes. Returns (snake-steps/s, cores, seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.oracle import OracleSim
+    import paper_1904_02833_b200 as M
+    from paper_1904_02833_b200.model import build_scene_parts
+    cores = cores or len(os.sched_getaffinity(0))
+    sc = M.SceneConfig()
+    parts, *_ = build_scene_parts(sc)
+    cfg = sc.solver_config()
+    sims = [OracleSim(config=cfg, **parts) for _ in range(cores)]
+    cmds = env_commands(cores, frames_per_core + 1, 0)
+    sims_cmd = [(s, cmds[:, e]) for e, s in enumerate(sims)]
+
+    def run(args, frames, first):
+        s, c = args
+        for f in range(frames):
+            s.step(c[first + f], True)
+
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(lambda a: run(a, 1, 0), sims_cmd))        # warm-up frame
+        t = time.perf_counter()
+        list(ex.map(lambda a: run(a, frames_per_core, 1), sims_cmd))
+        dt = time.perf_counter() - t
+    return cores * frames_per_core / dt, cores, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        cpu_oracle_rate(1, cores)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_oracle_rate(1, cores)
+    wall = time.perf_counter() - t
+    # each step: every core advances its own snake by one frame
+    rate = cores * args.steps / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": f"{cores} snakes x 1 frame per step"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle/softsnake_oracle.c (C restatement of the reference "
+                                   f"step), 1 snake per core, {args.steps} frames"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -------------------------------------------------------------------- main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import __graft_entry__ as g
+    if rank == 0:
+        g.build()
+    if dist:
+        dist.barrier()
+    import paper_1904_02833_b200 as M
+    from paper_1904_02833_b200 import roofline
+
+    n = args.envs
+    model = M.build_snake(M.SceneConfig(), n_envs=n, device=local)
+    sim = model.sim
+    K, W = args.steps, args.warmup
+    cmds = env_commands(n, W + K, 0, env0=rank * n)
+    d_cmds = torch.from_numpy(cmds).to(f"cuda:{local}")
+    stream = torch.cuda.ExternalStream(sim.stream, device=f"cuda:{local}")
+    frame_elems = n * 4
+
+    # warm-up (also instantiates the CUDA graph)
+    for f in range(W):
+        sim.step_device(d_cmds.data_ptr() + 8 * f * frame_elems, True, 1)
+    sim.synchronize()
+
+    # ---- device-timed region: inputs resident in HBM
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for f in range(K):
+            sim.step_device(d_cmds.data_ptr() + 8 * (W + f) * frame_elems, True, 1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    stats = sim.get_stats(0, min(n, 8))
+    finite = all(s.finite for s in sim.get_stats())
+
+    # ---- e2e through the public API: host commands (pinned) in, COM out
+    host_cmd = torch.from_numpy(env_commands(n, K, W + K, env0=rank * n)).pin_memory()
+    com_bytes = n * 3 * 8
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for f in range(K):
+        sim.step(host_cmd[f].numpy(), latency=True)
+        com = sim.center_of_mass()          # D2H of the step's result (synchronises)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+        # optional rollout-stats gather over NVLink
+        com_t = torch.from_numpy(com).to(f"cuda:{local}")
+        gathered = [torch.empty_like(com_t) for _ in range(world)]
+        dist.all_gather(gathered, com_t)
+
+    # ---- live per-kernel timing (CUDA events around each launch)
+    prof_cmds = env_commands(n, args.profile_frames, W + 2 * K, env0=rank * n)
+    prof = sim.profile_frames(prof_cmds, True, args.profile_frames)
+    step_ms_prof = sum(v[0] for v in prof.values()) / args.profile_frames
+    top = max(prof, key=lambda k: prof[k][0])
+    d = roofline.dims_of(sim)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    per_launch = roofline.bytes_per_launch_per_env(top, d) * n
+    avg_ms = prof[top][0] / prof[top][1]
+    achieved = per_launch / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(top)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    value = world * n * K / (ms * 1e-3)
+    e2e = world * n * K / e2e_s
+    launches = sim.launches_per_frame
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "envs_per_gpu": n, "global_envs": world * n,
+                   "frame_dt_s": 1 / 60, "substeps": 2, "newton": 4, "pcr": 20,
+                   "gait": "default, per-env turn bias U(-0.5,0.5), t0 U(0,0.5s), seed 20260817",
+                   "l2": "no flush: per-step working set "
+                         f"{sim.device_bytes / 1e9:.1f} GB >> 126 MB L2",
+                   "parallelism": f"env-sharded x{world}"},
+        "rtf": value / 60.0,
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                     "bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
+                     "share_of_step": prof[top][0] / sum(v[0] for v in prof.values()),
+                     "traffic": traffic},
+        "kernels_ms_per_frame": {k: round(v[0] / args.profile_frames, 4) for k, v in prof.items()},
+        "profiled_ms_per_frame": step_ms_prof,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": n * 4 * 8,
+                "d2h_bytes_per_step": com_bytes},
+        "gpu_launches": launches * K,
+        "finite": finite,
+        "stats_env0": {"contacts": stats[0].contact_count, "inverted": stats[0].inverted_tets,
+                       "residual": stats[0].residual},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        rate, cores, secs = cpu_oracle_rate(args.cpu_frames)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"oracle C port, {cores} snakes x {args.cpu_frames} "
+                                          f"frames ({secs:.1f} s wall)"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,80 @@
+"""Loader for the in-tree CUDA library (libsoftsnake_b200.so).
+
+There is no fallback: if the library is missing or CUDA is unavailable the
+calls raise, so a silent CPU path can never stand in for the GPU one.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from ._abi import SsEnvStats, SsParams, SsStateView, SsTopology
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libsoftsnake_b200.so")
+
+SS_EINVAL, SS_ECUDA, SS_ENOMEM, SS_EUNSUP = -1, -2, -3, -4
+
+_lib = None
+
+# every symbol include/softsnake_b200.h declares, with its ctypes signature
+_vp, _dp, _ip, _i = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int
+SIGNATURES = {
+    "ss_abi_version": (C.c_int, []),
+    "ss_last_error": (C.c_char_p, []),
+    "ss_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "ss_create": (C.c_int, [C.POINTER(SsTopology), C.POINTER(SsParams), _i, _i, C.POINTER(_vp)]),
+    "ss_destroy": (C.c_int, [_vp]),
+    "ss_num_envs": (C.c_int, [_vp]),
+    "ss_set_state": (C.c_int, [_vp, _i, _i, C.POINTER(SsStateView)]),
+    "ss_get_state": (C.c_int, [_vp, _i, _i, C.POINTER(SsStateView)]),
+    "ss_step": (C.c_int, [_vp, _dp, _i, _i]),
+    "ss_step_device": (C.c_int, [_vp, _vp, _i, _i]),
+    "ss_get_stats": (C.c_int, [_vp, _i, _i, C.POINTER(SsEnvStats)]),
+    "ss_get_com": (C.c_int, [_vp, _i, _i, _dp]),
+    "ss_synchronize": (C.c_int, [_vp]),
+    "ss_stream": (_vp, [_vp]),
+    "ss_launches_per_frame": (C.c_int, [_vp]),
+    "ss_device_bytes": (C.c_int64, [_vp]),
+    "ss_kernel_names": (C.c_int, [C.POINTER(C.c_char_p), _i]),
+    "ss_profile_frames": (C.c_int, [_vp, _dp, _i, _i, _dp, C.POINTER(C.c_int)]),
+    "ssk_block_forward": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
+    "ssk_block_transpose": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp]),
+    "ssk_block_rowdiag": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
+    "ssk_minv_apply": (C.c_int, [_vp, _vp, _i, _i, _vp, _vp, _i, _vp]),
+    "ssk_ereg_apply": (C.c_int, [_vp, _vp, _vp, _i, _vp]),
+    "ssk_dot": (C.c_int, [_vp, _vp, _i, _dp, _vp]),
+    "ssk_eval_distance": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
+    "ssk_eval_tetra": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _i, _vp, _vp, _i,
+                                 C.POINTER(C.c_int), _vp]),
+    "ssk_malloc": (C.c_int, [C.POINTER(_vp), C.c_int64, _i]),
+    "ssk_free": (C.c_int, [_vp]),
+    "ssk_memcpy": (C.c_int, [_vp, _vp, C.c_int64, _i]),
+}
+
+
+def lib():
+    """The loaded library; raises RuntimeError if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().ss_last_error()
+    msg = msg.decode() if msg else f"error {rc}"
+    if rc in (SS_EINVAL, SS_EUNSUP):
+        raise ValueError(msg)
+    raise RuntimeError(msg)

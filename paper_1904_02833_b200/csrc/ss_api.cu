@@ -1,0 +1,961 @@
+// ss_api.cu — C ABI of libsoftsnake_b200.so (include/softsnake_b200.h).
+//
+// Host side: topology preprocessing (row layout, incidence lists in the
+// reference accumulation order, compliance pattern), device memory, the
+// per-frame launch sequence captured once into a CUDA graph, state I/O.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/softsnake_b200.h"
+#include "ss_device.cuh"
+#include "ss_kabi.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(SS_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));        \
+  } while (0)
+
+// bump allocator over one cudaMalloc
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, off = 0;
+  template <typename T>
+  T* take(size_t n) {
+    size_t bytes = ((n * sizeof(T) + 255) / 256) * 256;
+    if (bytes == 0) bytes = 256;
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += bytes;
+    return p;
+  }
+};
+
+}  // namespace
+
+struct ss_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Ctx c{};
+  int gy_red_rows = 1, gy_red_apply = 1;
+  void* topo_mem = nullptr;
+  void* state_mem = nullptr;
+  void* work_mem = nullptr;
+  size_t bytes = 0;
+  double* d_cmd = nullptr;      // [n_real * links] (one frame)
+  double* d_stage = nullptr;    // staging for state I/O
+  size_t stage_bytes = 0;
+  cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};
+  int launches = 0;
+};
+
+namespace {
+
+// ------------------------------------------------------------ launch grid
+dim3 grid_items(const Dims& D, long n, long cap_blocks) {
+  const long IL = SS_THREADS >> D.lgW;
+  long gy = (n + IL - 1) / IL;
+  if (gy < 1) gy = 1;
+  long cap = cap_blocks / D.tiles;
+  if (cap < 1) cap = 1;
+  if (gy > cap) gy = cap;
+  if (gy > 65535) gy = 65535;
+  return dim3(D.tiles, (unsigned)gy);
+}
+constexpr long kStreamBlocks = 148 * 8;  // 8 resident 256-thread CTAs per SM
+constexpr long kReduceBlocks = 148 * 4;
+
+// kernel names for the profiler (ss_profile_frames)
+const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",     "k_eval_tet",
+                                    "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_pcr_reset",
+                                    "k_apply_rows",  "k_pcr_dir",    "k_pcr_step",  "k_newton_update",
+                                    "k_integrate"};
+constexpr int kNumKernels = 13;
+struct Prof {
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+};
+int kid(const char* name) {
+  for (int i = 0; i < kNumKernels; ++i)
+    if (!strcmp(name, kKernelNames[i])) return i;
+  return -1;
+}
+
+// Enqueue one frame (Simulator.step, solver.py:296-314) on the stream.
+// With prof, every launch is bracketed by CUDA events (eager, not graphed).
+int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
+  const Ctx& c = H->c;
+  const Dims& D = c.D;
+  cudaStream_t st = H->stream;
+  const dim3 blk(SS_THREADS);
+  int n = 0;
+#define LAUNCH(kern, grid, ...)                                          \
+  do {                                                                   \
+    cudaEvent_t e0_ = nullptr, e1_ = nullptr;                            \
+    if (prof) {                                                          \
+      cudaEventCreate(&e0_);                                             \
+      cudaEventCreate(&e1_);                                             \
+      cudaEventRecord(e0_, st);                                          \
+    }                                                                    \
+    kern<<<grid, blk, 0, st>>>(__VA_ARGS__);                             \
+    if (prof) {                                                          \
+      cudaEventRecord(e1_, st);                                          \
+      prof->ev.push_back({kid(#kern), {e0_, e1_}});                      \
+    }                                                                    \
+    ++n;                                                                 \
+  } while (0)
+  const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, kStreamBlocks);
+  LAUNCH(k_frame_begin, g_links, c, H->d_cmd, has_cmd, latency);
+  const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, kStreamBlocks);
+  const dim3 g_slots = grid_items(D, D.ns, kStreamBlocks);
+  const dim3 g_tet = grid_items(D, D.nt, kStreamBlocks);
+  const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, kStreamBlocks);
+  const dim3 g_gather = grid_items(D, D.P + D.nb, kStreamBlocks);
+  const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
+  const dim3 g_rhs = grid_items(D, n_el, kStreamBlocks);
+  const dim3 g_apply(D.tiles, H->gy_red_apply);
+  const dim3 g_rows(D.tiles, H->gy_red_rows);
+  const dim3 g_upd = grid_items(D, D.ms + D.ns, kStreamBlocks);
+  const dim3 g_int = grid_items(D, D.P + D.nb, kStreamBlocks);
+  const dim3 g_env((D.E + SS_THREADS - 1) / SS_THREADS);
+  const double* xs_lam = c.S.lam;
+  const double* xc_lam = c.K.lamc;
+  const double* xs_z = c.K.z;
+  const double* xc_z = c.K.z + (size_t)D.ms * D.E;
+  const double* xs_dl = c.K.az;
+  const double* xc_dl = c.K.az + (size_t)D.ms * D.E;
+  for (int sub = 0; sub < c.p.substeps; ++sub) {
+    LAUNCH(k_pre, g_pre, c);
+    if (D.ns) LAUNCH(k_slots, g_slots, c);
+    if (D.nt) LAUNCH(k_eval_tet, g_tet, c);
+    if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
+    LAUNCH(k_gather, g_gather, c, 1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
+    for (int it = 0; it < c.p.newton; ++it) {
+      LAUNCH(k_newton_rhs, g_rhs, c);
+      LAUNCH(k_pcr_reset, g_env, c);
+      if (c.p.pcr > 0) {
+        LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
+        LAUNCH(k_apply_rows, g_apply, c, 1);
+        LAUNCH(k_pcr_dir, g_rows, c, 1);
+        for (int k = 0; k < c.p.pcr; ++k) {
+          const bool last = k == c.p.pcr - 1;
+          LAUNCH(k_pcr_step, g_rows, c, 1, last ? 1 : 0);
+          if (!last) {
+            LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
+            LAUNCH(k_apply_rows, g_apply, c, 0);
+            LAUNCH(k_pcr_dir, g_rows, c, 0);
+          }
+        }
+      } else {
+        LAUNCH(k_pcr_step, g_rows, c, 0, 1);
+      }
+      LAUNCH(k_newton_update, g_upd, c, it == c.p.newton - 1 ? 1 : 0);
+      LAUNCH(k_gather, g_gather, c, 1, xs_dl, xc_dl);  // v += M^-1 J^T dlam
+    }
+    LAUNCH(k_integrate, g_int, c);
+  }
+#undef LAUNCH
+  if (nl) *nl = n;
+  CK(cudaGetLastError());
+  return SS_OK;
+}
+
+int get_graph(ss_handle* H, int has_cmd, int latency, cudaGraphExec_t* out) {
+  const int key = (has_cmd ? 2 : 0) | (latency ? 1 : 0);
+  if (H->graphs[key]) {
+    *out = H->graphs[key];
+    return SS_OK;
+  }
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(H->stream, cudaStreamCaptureModeThreadLocal));
+  int nl = 0;
+  int rc = enqueue_frame(H, has_cmd, latency, &nl);
+  cudaError_t e = cudaStreamEndCapture(H->stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(SS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  CK(cudaGraphInstantiate(&H->graphs[key], g, 0));
+  CK(cudaGraphDestroy(g));
+  H->launches = nl;
+  *out = H->graphs[key];
+  return SS_OK;
+}
+
+// state field table: (device base, A, B, swap, is_int)
+struct Field {
+  void* dev;
+  int A, B, swap, is_int;
+  void* host;
+};
+
+void state_fields(ss_handle* H, const ss_state_view* v, Field* f, int* nf) {
+  const Dims& D = H->c.D;
+  const State& S = H->c.S;
+  const size_t E = D.E;
+  int k = 0;
+  auto add = [&](void* dev, int A, int B, int swap, int is_int, void* host) {
+    f[k++] = Field{dev, A, B, swap, is_int, host};
+  };
+  add(S.pos, D.P, 3, 0, 0, v->positions);
+  add(S.vel, D.P, 3, 0, 0, v->velocities);
+  add(S.bpos, D.nb, 3, 0, 0, v->body_pos);
+  add(S.bquat, D.nb, 4, 0, 0, v->body_quat);
+  add(S.blin, D.nb, 3, 0, 0, v->body_lin_vel);
+  add(S.bang, D.nb, 3, 0, 0, v->body_ang_vel);
+  add(S.lam + (size_t)D.od * E, D.nd, 1, 0, 0, v->lam_dist);
+  add(S.lam + (size_t)D.ot * E, D.nt, 6, 1, 0, v->lam_tetra);
+  add(S.lam + (size_t)D.oa * E, D.na, 3, 1, 0, v->lam_attach);
+  add(S.lam + (size_t)D.oh * E, D.nh, 5, 1, 0, v->lam_hinge);
+  add(S.quat, D.nt, 4, 1, 0, v->tet_quats);
+  add(S.dirs, D.nd, 3, 1, 0, v->dist_dirs);
+  add(S.scale, D.nd, 1, 0, 0, v->dist_scale);
+  add(S.live, D.nch, 1, 0, 0, v->strain_live);
+  add(S.target, D.nch, 1, 0, 0, v->strain_target);
+  add(S.press, D.nch, 1, 0, 0, v->pressures);
+  add(S.warm, D.nw, 3, 1, 0, v->warm);
+  add(S.warm_valid, D.nw, 1, 0, 1, v->warm_valid);
+  add(S.time, 1, 1, 0, 0, v->time);
+  *nf = k;
+}
+
+__global__ void k_fill(double* p, size_t n, double val) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = val;
+}
+
+}  // namespace
+
+// ======================================================================
+extern "C" {
+
+int ss_abi_version(void) { return SS_ABI_VERSION; }
+const char* ss_last_error(void) { return g_err.c_str(); }
+
+int ss_device_count(int* n) {
+  CK(cudaGetDeviceCount(n));
+  return SS_OK;
+}
+
+int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
+              ss_handle** out) {
+  if (!t || !p || !out) return fail(SS_EINVAL, "null argument");
+  if (n_envs < 1) return fail(SS_EINVAL, "n_envs must be >= 1");
+  if (t->num_particles < 1) return fail(SS_EINVAL, "scene has no particles");
+  if (p->substeps < 1) return fail(SS_EINVAL, "substeps must be >= 1");
+  if (p->newton_iters < 0 || p->pcr_iters < 0) return fail(SS_EINVAL, "negative iteration count");
+  if (t->n_channels % 2) return fail(SS_EINVAL, "n_channels must be even (2 per link)");
+  *out = nullptr;
+  CK(cudaSetDevice(device));
+
+  Dims D{};
+  D.n_real = n_envs;
+  int E = 1;
+  if (n_envs <= 32) {
+    while (E < n_envs) E <<= 1;
+  } else {
+    E = ((n_envs + 31) / 32) * 32;
+  }
+  D.E = E;
+  D.W = E < 32 ? E : 32;
+  D.lgW = 0;
+  while ((1 << D.lgW) < D.W) ++D.lgW;
+  D.tiles = E / D.W;
+  D.P = t->num_particles;
+  D.nb = t->num_bodies;
+  D.ndof = 3 * D.P + 6 * D.nb;
+  D.bd0 = 3 * D.P;
+  D.nd = t->n_dist;
+  D.nt = t->n_tet;
+  D.na = t->n_attach;
+  D.nh = t->n_hinge;
+  D.nw = p->ground_enabled ? t->n_wheel : 0;
+  D.nq = p->ground_enabled ? (t->contact_particles ? t->n_contact_particles : D.P) : 0;
+  D.ns = D.nw + D.nq;
+  D.nch = t->n_channels;
+  D.links = D.nch / 2;
+  D.od = 0;
+  D.ot = D.nd;
+  D.oa = D.ot + 6 * D.nt;
+  D.oh = D.oa + 3 * D.na;
+  D.ms = D.oh + 5 * D.nh;
+  D.on = D.ms;
+  D.of = D.ms + D.ns;
+  D.m = D.ms + 3 * D.ns;
+  if ((long)D.nt >= (1L << 25) || (long)D.ns >= (1L << 25) || (long)D.nd >= (1L << 25))
+    return fail(SS_EUNSUP, "more than 2^25 elements in one family");
+
+  // validate indices
+  for (int i = 0; i < 2 * D.nd; ++i)
+    if (t->dist_pairs[i] < 0 || t->dist_pairs[i] >= D.P) return fail(SS_EINVAL, "dist_pairs out of range");
+  for (int i = 0; i < 4 * D.nt; ++i)
+    if (t->tets[i] < 0 || t->tets[i] >= D.P) return fail(SS_EINVAL, "tets out of range");
+  for (int i = 0; i < D.na; ++i)
+    if (t->attach_particle[i] < 0 || t->attach_particle[i] >= D.P || t->attach_body[i] < 0 ||
+        t->attach_body[i] >= D.nb)
+      return fail(SS_EINVAL, "attachment index out of range");
+  for (int i = 0; i < D.nh; ++i)
+    if (t->hinge_body_a[i] < 0 || t->hinge_body_a[i] >= D.nb || t->hinge_body_b[i] < 0 ||
+        t->hinge_body_b[i] >= D.nb)
+      return fail(SS_EINVAL, "hinge body out of range");
+  for (int i = 0; i < D.nw; ++i)
+    if (t->wheel_body[i] < 0 || t->wheel_body[i] >= D.nb) return fail(SS_EINVAL, "wheel body out of range");
+  if (t->contact_particles)
+    for (int i = 0; i < D.nq; ++i)
+      if (t->contact_particles[i] < 0 || t->contact_particles[i] >= D.P)
+        return fail(SS_EINVAL, "contact_particles out of range");
+  for (int i = 0; i < D.nd; ++i)
+    if (t->dist_channel && t->dist_channel[i] >= D.nch) return fail(SS_EINVAL, "dist_channel out of range");
+
+  // ---- parameters (solver.py:195-232, 259)
+  Par P{};
+  const double h = p->dt / p->substeps;
+  P.h = h;
+  const double dmp = 0.0 > p->constraint_damping ? 0.0 : p->constraint_damping;
+  P.gamma = 1.0 / (1.0 + dmp);
+  for (int a = 0; a < 3; ++a) P.hg[a] = h * p->gravity[a];
+  P.ground_h = p->ground_height;
+  P.margin = p->contact_margin;
+  P.mu = p->mu;
+  P.fdyn = p->friction_compliance / (h * h);
+  P.fb_delta = p->fb_delta;
+  P.smin = p->fb_slope_min;
+  P.smax = p->fb_slope_max;
+  P.dmax = p->max_strain_rate * h;
+  P.youngs = p->strain_youngs;
+  P.ki = p->k_inflate;
+  P.kd = p->k_deflate;
+  P.cap = p->deflate_cap;
+  P.supply = p->supply;
+  P.half_h = 0.5 * h;
+  P.newton = p->newton_iters;
+  P.pcr = p->pcr_iters;
+  P.substeps = p->substeps;
+  const double g = P.gamma;
+
+  // actuated rows exist (solver.py:241-248)
+  D.act_enabled = 0;
+  if (D.nd && D.nch && t->has_strain && t->dist_channel)
+    for (int i = 0; i < D.nd; ++i)
+      if (t->dist_channel[i] >= 0) D.act_enabled = 1;
+
+  // ---- host topology arrays
+  std::vector<double> inv_mass(t->inv_mass, t->inv_mass + D.P);
+  std::vector<double> body_im(D.nb), body_I(9 * (size_t)D.nb);
+  for (int b = 0; b < D.nb; ++b) {
+    body_im[b] = 1.0 / t->body_mass[b];
+    for (int k = 0; k < 9; ++k) body_I[9 * b + k] = t->body_inertia[9 * b + k];
+  }
+  std::vector<int> d_i(D.nd), d_j(D.nd), d_chan(D.nd);
+  std::vector<double> d_rest(D.nd), d_dyn(D.nd);
+  for (int e = 0; e < D.nd; ++e) {
+    d_i[e] = t->dist_pairs[2 * e];
+    d_j[e] = t->dist_pairs[2 * e + 1];
+    d_chan[e] = t->dist_channel ? t->dist_channel[e] : -1;
+    d_rest[e] = t->dist_rest[e];
+    d_dyn[e] = g * t->dist_compliance[e] / (h * h);
+  }
+  std::vector<int> t_idx(4 * (size_t)D.nt);
+  std::vector<double> t_rinv(9 * (size_t)D.nt), t_e3(3 * (size_t)D.nt);
+  for (int e = 0; e < D.nt; ++e) {
+    for (int v = 0; v < 4; ++v) t_idx[(size_t)v * D.nt + e] = t->tets[4 * (size_t)e + v];
+    for (int k = 0; k < 9; ++k) t_rinv[(size_t)k * D.nt + e] = t->tet_rest_inv[9 * (size_t)e + k];
+    // eh2 = gamma * compliance / (h*h) (solver.py:210); isotropic pattern
+    // (constraints.py:26-40) stored as (diag, off-diagonal, shear)
+    double eh[36];
+    for (int k = 0; k < 36; ++k) eh[k] = g * t->tet_compliance[36 * (size_t)e + k] / (h * h);
+    const double ed = eh[0], eo = eh[1], es = eh[21];
+    bool ok = true;
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j) {
+        double want;
+        if (i < 3 && j < 3) want = i == j ? ed : eo;
+        else if (i == j) want = es;
+        else want = 0.0;
+        if (memcmp(&eh[6 * i + j], &want, 8) != 0 && !(eh[6 * i + j] == 0.0 && want == 0.0)) ok = false;
+      }
+    if (!ok)
+      return fail(SS_EUNSUP, "tet %d compliance is not the isotropic Voigt pattern of "
+                             "constraints.py:26-40", e);
+    t_e3[e] = ed;
+    t_e3[(size_t)D.nt + e] = eo;
+    t_e3[2 * (size_t)D.nt + e] = es;
+  }
+  std::vector<int> a_p(D.na), a_b(D.na);
+  std::vector<double> a_anc(3 * (size_t)D.na), a_dyn(D.na);
+  for (int e = 0; e < D.na; ++e) {
+    a_p[e] = t->attach_particle[e];
+    a_b[e] = t->attach_body[e];
+    for (int k = 0; k < 3; ++k) a_anc[(size_t)k * D.na + e] = t->attach_anchor[3 * e + k];
+    a_dyn[e] = g * t->attach_compliance[e] / (h * h);
+  }
+  std::vector<int> h_a(D.nh), h_b(D.nh);
+  std::vector<double> h_v[5], h_dyn(D.nh);
+  const double* hsrc[5] = {t->hinge_anchor_a, t->hinge_anchor_b, t->hinge_axis_a, t->hinge_tan1_b,
+                           t->hinge_tan2_b};
+  for (int q = 0; q < 5; ++q) h_v[q].assign(3 * (size_t)D.nh, 0.0);
+  for (int e = 0; e < D.nh; ++e) {
+    h_a[e] = t->hinge_body_a[e];
+    h_b[e] = t->hinge_body_b[e];
+    for (int q = 0; q < 5; ++q)
+      for (int k = 0; k < 3; ++k) h_v[q][(size_t)k * D.nh + e] = hsrc[q][3 * e + k];
+    h_dyn[e] = g * t->hinge_compliance[e] / (h * h);
+  }
+  std::vector<int> w_body(D.nw);
+  std::vector<double> w_rad(D.nw), w_axis(3 * (size_t)D.nw);
+  for (int e = 0; e < D.nw; ++e) {
+    w_body[e] = t->wheel_body[e];
+    w_rad[e] = t->wheel_radius[e];
+    for (int k = 0; k < 3; ++k) w_axis[(size_t)k * D.nw + e] = t->wheel_axis[3 * e + k];
+  }
+  std::vector<int> slot_part(D.nq);
+  for (int q = 0; q < D.nq; ++q) slot_part[q] = t->contact_particles ? t->contact_particles[q] : q;
+
+  // ---- incidence lists in the reference accumulation order
+  struct Inc { uint64_t key; int code; };
+  std::vector<std::vector<Inc>> lists((size_t)D.P + D.nb);
+  auto push = [&](int item, int rank, int fam, int v, int e) {
+    uint64_t key = ((uint64_t)rank << 40) | ((uint64_t)e << 8) | (uint64_t)v;
+    int code = (fam << 29) | (v << 25) | e;
+    lists[item].push_back({key, code});
+  };
+  for (int e = 0; e < D.nd; ++e) {
+    push(d_i[e], 0, F_DIST, 0, e);
+    push(d_j[e], 0, F_DIST, 1, e);
+  }
+  for (int e = 0; e < D.nt; ++e)
+    for (int v = 0; v < 4; ++v) push(t->tets[4 * (size_t)e + v], 1, F_TET, v, e);
+  for (int e = 0; e < D.na; ++e) {
+    push(a_p[e], 2, F_ATTP, 0, e);
+    push(D.P + a_b[e], 2, F_ATTB, 1, e);
+  }
+  for (int e = 0; e < D.nh; ++e) {
+    push(D.P + h_a[e], 3, F_HINGE, 0, e);
+    push(D.P + h_b[e], 3, F_HINGE, 1, e);
+  }
+  for (int s = 0; s < D.ns; ++s) {
+    const int item = s < D.nw ? D.P + w_body[s] : slot_part[s - D.nw];
+    push(item, 4, F_CN, 0, s);
+    push(item, 5, F_CF, 0, s);
+  }
+  std::vector<int> inc_ptr((size_t)D.P + D.nb + 1, 0), inc;
+  for (size_t i = 0; i < lists.size(); ++i) {
+    std::stable_sort(lists[i].begin(), lists[i].end(),
+                     [](const Inc& a, const Inc& b) { return a.key < b.key; });
+    inc_ptr[i + 1] = inc_ptr[i] + (int)lists[i].size();
+    for (auto& x : lists[i]) inc.push_back(x.code);
+  }
+
+  // ---- allocations
+  ss_handle* H = new ss_handle();
+  H->device = device;
+  H->c.D = D;
+  H->c.p = P;
+  CK(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+
+  // topology
+  Arena ta;
+  auto plan_topo = [&](Arena& A) {
+    Topo& T = H->c.T;
+    T.inv_mass = A.take<double>(D.P);
+    T.body_inv_mass = A.take<double>(D.nb);
+    T.body_inertia = A.take<double>(9 * (size_t)D.nb);
+    T.d_i = A.take<int>(D.nd);
+    T.d_j = A.take<int>(D.nd);
+    T.d_chan = A.take<int>(D.nd);
+    T.d_rest = A.take<double>(D.nd);
+    T.d_dyn = A.take<double>(D.nd);
+    T.t_idx = A.take<int>(4 * (size_t)D.nt);
+    T.t_rinv = A.take<double>(9 * (size_t)D.nt);
+    T.t_e3 = A.take<double>(3 * (size_t)D.nt);
+    T.a_p = A.take<int>(D.na);
+    T.a_b = A.take<int>(D.na);
+    T.a_anc = A.take<double>(3 * (size_t)D.na);
+    T.a_dyn = A.take<double>(D.na);
+    T.h_a = A.take<int>(D.nh);
+    T.h_b = A.take<int>(D.nh);
+    T.h_anca = A.take<double>(3 * (size_t)D.nh);
+    T.h_ancb = A.take<double>(3 * (size_t)D.nh);
+    T.h_axa = A.take<double>(3 * (size_t)D.nh);
+    T.h_t1 = A.take<double>(3 * (size_t)D.nh);
+    T.h_t2 = A.take<double>(3 * (size_t)D.nh);
+    T.h_dyn = A.take<double>(D.nh);
+    T.w_body = A.take<int>(D.nw);
+    T.w_rad = A.take<double>(D.nw);
+    T.w_axis = A.take<double>(3 * (size_t)D.nw);
+    T.slot_part = A.take<int>(D.nq);
+    T.inc_ptr = A.take<int>((size_t)D.P + D.nb + 1);
+    T.inc = A.take<int>(inc.size());
+  };
+  plan_topo(ta);
+  ta.cap = ta.off;
+  ta.off = 0;
+  {
+    cudaError_t e = cudaMalloc(&H->topo_mem, ta.cap);
+    if (e != cudaSuccess) {
+      delete H;
+      return fail(SS_ENOMEM, "cudaMalloc topology (%zu bytes): %s", ta.cap, cudaGetErrorString(e));
+    }
+  }
+  ta.base = (char*)H->topo_mem;
+  plan_topo(ta);
+  H->bytes += ta.cap;
+  auto up = [&](const void* dst, const void* src, size_t bytes) -> int {
+    if (bytes) CK(cudaMemcpy((void*)dst, src, bytes, cudaMemcpyHostToDevice));
+    return SS_OK;
+  };
+  const Topo& T = H->c.T;
+  int rc = 0;
+  rc |= up(T.inv_mass, inv_mass.data(), 8 * inv_mass.size());
+  rc |= up(T.body_inv_mass, body_im.data(), 8 * body_im.size());
+  rc |= up(T.body_inertia, body_I.data(), 8 * body_I.size());
+  rc |= up(T.d_i, d_i.data(), 4 * d_i.size());
+  rc |= up(T.d_j, d_j.data(), 4 * d_j.size());
+  rc |= up(T.d_chan, d_chan.data(), 4 * d_chan.size());
+  rc |= up(T.d_rest, d_rest.data(), 8 * d_rest.size());
+  rc |= up(T.d_dyn, d_dyn.data(), 8 * d_dyn.size());
+  rc |= up(T.t_idx, t_idx.data(), 4 * t_idx.size());
+  rc |= up(T.t_rinv, t_rinv.data(), 8 * t_rinv.size());
+  rc |= up(T.t_e3, t_e3.data(), 8 * t_e3.size());
+  rc |= up(T.a_p, a_p.data(), 4 * a_p.size());
+  rc |= up(T.a_b, a_b.data(), 4 * a_b.size());
+  rc |= up(T.a_anc, a_anc.data(), 8 * a_anc.size());
+  rc |= up(T.a_dyn, a_dyn.data(), 8 * a_dyn.size());
+  rc |= up(T.h_a, h_a.data(), 4 * h_a.size());
+  rc |= up(T.h_b, h_b.data(), 4 * h_b.size());
+  rc |= up(T.h_anca, h_v[0].data(), 8 * h_v[0].size());
+  rc |= up(T.h_ancb, h_v[1].data(), 8 * h_v[1].size());
+  rc |= up(T.h_axa, h_v[2].data(), 8 * h_v[2].size());
+  rc |= up(T.h_t1, h_v[3].data(), 8 * h_v[3].size());
+  rc |= up(T.h_t2, h_v[4].data(), 8 * h_v[4].size());
+  rc |= up(T.h_dyn, h_dyn.data(), 8 * h_dyn.size());
+  rc |= up(T.w_body, w_body.data(), 4 * w_body.size());
+  rc |= up(T.w_rad, w_rad.data(), 8 * w_rad.size());
+  rc |= up(T.w_axis, w_axis.data(), 8 * w_axis.size());
+  rc |= up(T.slot_part, slot_part.data(), 4 * slot_part.size());
+  rc |= up(T.inc_ptr, inc_ptr.data(), 4 * inc_ptr.size());
+  rc |= up(T.inc, inc.data(), 4 * inc.size());
+  if (rc) {
+    ss_destroy(H);
+    return SS_ECUDA;
+  }
+
+  // reduction grids
+  {
+    const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
+    H->gy_red_apply = (int)grid_items(D, n_el, kReduceBlocks).y;
+    H->gy_red_rows = (int)grid_items(D, D.m, kReduceBlocks).y;
+  }
+  const int gy_max = std::max(H->gy_red_apply, H->gy_red_rows);
+
+  // state + work
+  const size_t Es = D.E;
+  auto plan_state = [&](Arena& A) {
+    State& S = H->c.S;
+    S.pos = A.take<double>(3 * (size_t)D.P * Es);
+    S.vel = A.take<double>(3 * (size_t)D.P * Es);
+    S.bpos = A.take<double>(3 * (size_t)D.nb * Es);
+    S.bquat = A.take<double>(4 * (size_t)D.nb * Es);
+    S.blin = A.take<double>(3 * (size_t)D.nb * Es);
+    S.bang = A.take<double>(3 * (size_t)D.nb * Es);
+    S.lam = A.take<double>((size_t)D.ms * Es);
+    S.quat = A.take<double>(4 * (size_t)D.nt * Es);
+    S.dirs = A.take<double>(3 * (size_t)D.nd * Es);
+    S.scale = A.take<double>((size_t)D.nd * Es);
+    S.live = A.take<double>((size_t)D.nch * Es);
+    S.target = A.take<double>((size_t)D.nch * Es);
+    S.press = A.take<double>((size_t)D.nch * Es);
+    S.warm = A.take<double>(3 * (size_t)D.nw * Es);
+    S.warm_valid = A.take<int>((size_t)D.nw * Es);
+    S.time = A.take<double>(Es);
+  };
+  auto plan_work = [&](Arena& A) {
+    Work& K = H->c.K;
+    K.v = A.take<double>((size_t)D.ndof * Es);
+    K.u = A.take<double>((size_t)D.ndof * Es);
+    K.ang_inv = A.take<double>(9 * (size_t)D.nb * Es);
+    K.res = A.take<double>((size_t)D.ms * Es);
+    K.tJ = A.take<double>(72 * (size_t)D.nt * Es);
+    K.rw = A.take<double>(3 * (size_t)D.na * Es);
+    K.hJ = A.take<double>(60 * (size_t)D.nh * Es);
+    K.wJ = A.take<double>(18 * (size_t)D.nw * Es);
+    K.present = A.take<int>((size_t)D.ns * Es);
+    K.gap = A.take<double>((size_t)D.ns * Es);
+    K.actf = A.take<double>((size_t)D.ns * Es);
+    K.dynn = A.take<double>((size_t)D.ns * Es);
+    K.lamc = A.take<double>(3 * (size_t)D.ns * Es);
+    K.bdiag = A.take<double>((size_t)D.m * Es);
+    K.x = A.take<double>((size_t)D.m * Es);
+    K.r = A.take<double>((size_t)D.m * Es);
+    K.z = A.take<double>((size_t)D.m * Es);
+    K.p = A.take<double>((size_t)D.m * Es);
+    K.ap = A.take<double>((size_t)D.m * Es);
+    K.az = A.take<double>((size_t)D.m * Es);
+    K.d = A.take<double>((size_t)D.m * Es);
+    K.part = A.take<double>((size_t)gy_max * Es);
+    K.cnt = A.take<int>(D.tiles);
+    K.rho = A.take<double>(Es);
+    K.alpha = A.take<double>(Es);
+    K.beta = A.take<double>(Es);
+    K.resid = A.take<double>(Es);
+    K.broken = A.take<int>(Es);
+    K.nc_cnt = A.take<int>(Es);
+    K.inv_cnt = A.take<int>(Es);
+    K.nonfinite = A.take<int>(Es);
+  };
+  Arena sa, wa;
+  plan_state(sa);
+  plan_work(wa);
+  sa.cap = sa.off;
+  wa.cap = wa.off;
+  sa.off = wa.off = 0;
+  {
+    cudaError_t e1 = cudaMalloc(&H->state_mem, sa.cap);
+    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap) : e1;
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      ss_destroy(H);
+      return fail(SS_ENOMEM, "cudaMalloc state/work (%zu + %zu bytes) for %d envs failed", sa.cap,
+                  wa.cap, n_envs);
+    }
+  }
+  sa.base = (char*)H->state_mem;
+  wa.base = (char*)H->work_mem;
+  plan_state(sa);
+  plan_work(wa);
+  H->bytes += sa.cap + wa.cap;
+  CK(cudaMemsetAsync(H->state_mem, 0, sa.cap, H->stream));
+  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap, H->stream));
+  // reference constructor defaults
+  {
+    const State& S = H->c.S;
+    auto fill = [&](double* ptr, size_t n, double val) {
+      if (n) k_fill<<<256, 256, 0, H->stream>>>(ptr, n, val);
+    };
+    for (int b = 0; b < D.nb; ++b) fill(S.bquat + (size_t)(4 * b) * Es, Es, 1.0);
+    fill(S.quat, (size_t)D.nt * Es, 1.0);  // w component block [0][nt]
+    fill(S.dirs, (size_t)D.nd * Es, 1.0);  // x component block [0][nd]
+    fill(S.scale, (size_t)D.nd * Es, 1.0);
+    fill(S.live, (size_t)D.nch * Es, 1.0);
+    fill(S.target, (size_t)D.nch * Es, 1.0);
+  }
+  CK(cudaMalloc(&H->d_cmd, 8 * (size_t)std::max(1, n_envs * std::max(1, D.links))));
+  CK(cudaMemsetAsync(H->d_cmd, 0, 8 * (size_t)std::max(1, n_envs * std::max(1, D.links)), H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  *out = H;
+  return SS_OK;
+}
+
+int ss_destroy(ss_handle* H) {
+  if (!H) return SS_OK;
+  cudaSetDevice(H->device);
+  for (auto& g : H->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  if (H->topo_mem) cudaFree(H->topo_mem);
+  if (H->state_mem) cudaFree(H->state_mem);
+  if (H->work_mem) cudaFree(H->work_mem);
+  if (H->d_cmd) cudaFree(H->d_cmd);
+  if (H->d_stage) cudaFree(H->d_stage);
+  if (H->stream) cudaStreamDestroy(H->stream);
+  delete H;
+  return SS_OK;
+}
+
+int ss_num_envs(const ss_handle* H) { return H ? H->c.D.n_real : 0; }
+
+static int ensure_stage(ss_handle* H, size_t bytes) {
+  if (bytes <= H->stage_bytes) return SS_OK;
+  if (H->d_stage) CK(cudaFree(H->d_stage));
+  H->d_stage = nullptr;
+  CK(cudaMalloc(&H->d_stage, bytes));
+  H->stage_bytes = bytes;
+  return SS_OK;
+}
+
+int ss_set_state(ss_handle* H, int env0, int n, const ss_state_view* v) {
+  if (!H || !v) return fail(SS_EINVAL, "null argument");
+  const Dims& D = H->c.D;
+  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
+  if (n == 0) return SS_OK;
+  CK(cudaSetDevice(H->device));
+  Field f[32];
+  int nf = 0;
+  state_fields(H, v, f, &nf);
+  for (int i = 0; i < nf; ++i) {
+    if (!f[i].host || f[i].A * f[i].B == 0) continue;
+    const size_t elem = f[i].is_int ? 4 : 8;
+    const size_t bytes = elem * (size_t)f[i].A * f[i].B * n;
+    int rc = ensure_stage(H, bytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(H->d_stage, f[i].host, bytes, cudaMemcpyHostToDevice, H->stream));
+    if (f[i].is_int)
+      k_scatter<int><<<512, 256, 0, H->stream>>>((int*)f[i].dev, (const int*)H->d_stage, n, f[i].A,
+                                                 f[i].B, f[i].swap, D.E, env0, D.n_real);
+    else
+      k_scatter<double><<<512, 256, 0, H->stream>>>((double*)f[i].dev, (const double*)H->d_stage, n,
+                                                    f[i].A, f[i].B, f[i].swap, D.E, env0, D.n_real);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(H->stream));
+  }
+  return SS_OK;
+}
+
+int ss_get_state(ss_handle* H, int env0, int n, ss_state_view* v) {
+  if (!H || !v) return fail(SS_EINVAL, "null argument");
+  const Dims& D = H->c.D;
+  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
+  if (n == 0) return SS_OK;
+  CK(cudaSetDevice(H->device));
+  Field f[32];
+  int nf = 0;
+  state_fields(H, v, f, &nf);
+  for (int i = 0; i < nf; ++i) {
+    if (!f[i].host || f[i].A * f[i].B == 0) continue;
+    const size_t elem = f[i].is_int ? 4 : 8;
+    const size_t bytes = elem * (size_t)f[i].A * f[i].B * n;
+    int rc = ensure_stage(H, bytes);
+    if (rc) return rc;
+    if (f[i].is_int)
+      k_gather_state<int><<<512, 256, 0, H->stream>>>((int*)H->d_stage, (const int*)f[i].dev, n,
+                                                      f[i].A, f[i].B, f[i].swap, D.E, env0);
+    else
+      k_gather_state<double><<<512, 256, 0, H->stream>>>((double*)H->d_stage,
+                                                         (const double*)f[i].dev, n, f[i].A,
+                                                         f[i].B, f[i].swap, D.E, env0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(f[i].host, H->d_stage, bytes, cudaMemcpyDeviceToHost, H->stream));
+    CK(cudaStreamSynchronize(H->stream));
+  }
+  return SS_OK;
+}
+
+static int step_impl(ss_handle* H, const double* cmd, int on_device, int latency, int n_frames) {
+  if (!H) return fail(SS_EINVAL, "null handle");
+  if (n_frames < 0) return fail(SS_EINVAL, "n_frames must be >= 0");
+  CK(cudaSetDevice(H->device));
+  const Dims& D = H->c.D;
+  const int has_cmd = cmd != nullptr && D.nch > 0;
+  cudaGraphExec_t g;
+  int rc = get_graph(H, has_cmd, latency ? 1 : 0, &g);
+  if (rc) return rc;
+  const size_t frame_bytes = 8 * (size_t)D.n_real * D.links;
+  for (int f = 0; f < n_frames; ++f) {
+    if (has_cmd)
+      CK(cudaMemcpyAsync(H->d_cmd, cmd + (size_t)f * D.n_real * D.links, frame_bytes,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, H->stream));
+    CK(cudaGraphLaunch(g, H->stream));
+  }
+  return SS_OK;
+}
+
+int ss_step(ss_handle* H, const double* commands, int latency, int n_frames) {
+  return step_impl(H, commands, 0, latency, n_frames);
+}
+int ss_step_device(ss_handle* H, const double* d_commands, int latency, int n_frames) {
+  return step_impl(H, d_commands, 1, latency, n_frames);
+}
+
+int ss_get_stats(ss_handle* H, int env0, int n, ss_env_stats* out) {
+  if (!H || !out) return fail(SS_EINVAL, "null argument");
+  const Dims& D = H->c.D;
+  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
+  CK(cudaSetDevice(H->device));
+  std::vector<int> nc(n), inv(n), nf(n);
+  std::vector<double> res(n);
+  const Work& K = H->c.K;
+  CK(cudaMemcpyAsync(nc.data(), K.nc_cnt + env0, 4 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaMemcpyAsync(inv.data(), K.inv_cnt + env0, 4 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaMemcpyAsync(nf.data(), K.nonfinite + env0, 4 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaMemcpyAsync(res.data(), K.resid + env0, 8 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  const Par& P = H->c.p;
+  for (int i = 0; i < n; ++i) {
+    out[i].newton_iterations = P.substeps * P.newton;
+    out[i].pcr_iterations = P.substeps * P.newton * P.pcr;
+    out[i].contact_count = nc[i];
+    out[i].inverted_tets = inv[i];
+    out[i].residual = res[i];
+    out[i].finite = nf[i] ? 0 : 1;
+    out[i]._pad = 0;
+  }
+  return SS_OK;
+}
+
+int ss_get_com(ss_handle* H, int env0, int n, double* out) {
+  if (!H || !out) return fail(SS_EINVAL, "null argument");
+  const Dims& D = H->c.D;
+  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
+  if (n == 0) return SS_OK;
+  CK(cudaSetDevice(H->device));
+  int rc = ensure_stage(H, 24 * (size_t)n);
+  if (rc) return rc;
+  k_com<<<(n + 127) / 128, 128, 0, H->stream>>>(H->c, env0, n, H->d_stage);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, H->d_stage, 24 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  return SS_OK;
+}
+
+int ss_synchronize(ss_handle* H) {
+  if (!H) return fail(SS_EINVAL, "null handle");
+  CK(cudaSetDevice(H->device));
+  CK(cudaStreamSynchronize(H->stream));
+  return SS_OK;
+}
+
+void* ss_stream(ss_handle* H) { return H ? (void*)H->stream : nullptr; }
+
+int ss_launches_per_frame(ss_handle* H) {
+  if (!H) return 0;
+  if (!H->launches) {
+    cudaGraphExec_t g;
+    if (get_graph(H, 1, 1, &g)) return -1;
+  }
+  return H->launches;
+}
+
+int64_t ss_device_bytes(ss_handle* H) { return H ? (int64_t)H->bytes : 0; }
+
+int ss_kernel_names(const char** names, int cap) {
+  for (int i = 0; i < kNumKernels && i < cap; ++i) names[i] = kKernelNames[i];
+  return kNumKernels;
+}
+
+int ss_profile_frames(ss_handle* H, const double* commands, int latency, int n_frames,
+                      double* ms_total, int* launches) {
+  if (!H || !ms_total || !launches) return fail(SS_EINVAL, "null argument");
+  CK(cudaSetDevice(H->device));
+  const Dims& D = H->c.D;
+  const int has_cmd = commands != nullptr && D.nch > 0;
+  for (int i = 0; i < kNumKernels; ++i) {
+    ms_total[i] = 0.0;
+    launches[i] = 0;
+  }
+  const size_t frame_bytes = 8 * (size_t)D.n_real * D.links;
+  for (int f = 0; f < n_frames; ++f) {
+    if (has_cmd)
+      CK(cudaMemcpyAsync(H->d_cmd, commands + (size_t)f * D.n_real * D.links, frame_bytes,
+                         cudaMemcpyHostToDevice, H->stream));
+    Prof prof;
+    int nl = 0;
+    int rc = enqueue_frame(H, has_cmd, latency, &nl, &prof);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(H->stream));
+    for (auto& e : prof.ev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+      if (e.first >= 0) {
+        ms_total[e.first] += ms;
+        launches[e.first] += 1;
+      }
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+  }
+  return SS_OK;
+}
+
+// ------------------------------------------------------- kernel-level ABI
+#define KSTREAM ((cudaStream_t)stream)
+#define KBLK(n) (unsigned)(((long)(n) + 255) / 256), 256, 0, KSTREAM
+
+int ssk_block_forward(const int32_t* dof_idx, const double* vals, int n, int r, int k,
+                      const double* u, double* out_rows, void* stream) {
+  if (n * r > 0) kk_block_forward<<<KBLK((long)n * r)>>>(dof_idx, vals, n, r, k, u, out_rows);
+  CK(cudaGetLastError());
+  return SS_OK;
+}
+int ssk_block_transpose(const int32_t* dof_idx, const double* vals, int n, int r, int k,
+                        const double* x_rows, double* y, int ndof, void* stream) {
+  if (ndof > 0) kk_block_transpose<<<KBLK(ndof)>>>(dof_idx, vals, n, r, k, x_rows, y, ndof);
+  CK(cudaGetLastError());
+  return SS_OK;
+}
+int ssk_block_rowdiag(const int32_t* dof_idx, const double* vals, int n, int r, int k,
+                      const double* minv_diag, double* out_rows, void* stream) {
+  if (n * r > 0) kk_block_rowdiag<<<KBLK((long)n * r)>>>(dof_idx, vals, n, r, k, minv_diag, out_rows);
+  CK(cudaGetLastError());
+  return SS_OK;
+}
+int ssk_minv_apply(const double* minv_diag, const double* ang_inv, int nb, int body_dof0,
+                   const double* u, double* out, int ndof, void* stream) {
+  if (ndof > 0) kk_minv_apply<<<KBLK(ndof)>>>(minv_diag, ang_inv, nb, body_dof0, u, out, ndof);
+  CK(cudaGetLastError());
+  return SS_OK;
+}
+int ssk_ereg_apply(const double* vals6, const double* x_rows, double* out_rows, int n,
+                   void* stream) {
+  if (n > 0) kk_ereg_apply<<<KBLK((long)n * 6)>>>(vals6, x_rows, out_rows, n);
+  CK(cudaGetLastError());
+  return SS_OK;
+}
+int ssk_dot(const double* a, const double* b, int n, double* out_host, void* stream) {
+  double* d = nullptr;
+  CK(cudaMalloc(&d, 8));
+  kk_dot<<<1, 256, 0, KSTREAM>>>(a, b, n, d);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_host, d, 8, cudaMemcpyDeviceToHost, KSTREAM);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(KSTREAM);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SS_ECUDA, "ssk_dot: %s", cudaGetErrorString(e));
+  return SS_OK;
+}
+int ssk_eval_distance(const double* pos, const int32_t* pairs, const double* rest,
+                      const double* scale, double* dirs, double* out_res, int n, void* stream) {
+  if (n > 0) kk_eval_distance<<<KBLK(n)>>>(pos, pairs, rest, scale, dirs, out_res, n);
+  CK(cudaGetLastError());
+  return SS_OK;
+}
+int ssk_eval_tetra(const double* pos, const int32_t* tets, const double* rest_inv, double* quats,
+                   double tol, int maxiter, double* out_res, double* out_vals, int n,
+                   int* n_inverted, void* stream) {
+  int* d = nullptr;
+  CK(cudaMalloc(&d, 4));
+  cudaError_t e = cudaMemsetAsync(d, 0, 4, KSTREAM);
+  if (e == cudaSuccess && n > 0)
+    kk_eval_tetra<<<KBLK(n)>>>(pos, tets, rest_inv, quats, tol, maxiter, out_res, out_vals, n, d);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  int h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, KSTREAM);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(KSTREAM);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SS_ECUDA, "ssk_eval_tetra: %s", cudaGetErrorString(e));
+  if (n_inverted) *n_inverted = h;
+  return SS_OK;
+}
+
+int ssk_malloc(void** ptr, int64_t bytes, int device) {
+  if (!ptr) return fail(SS_EINVAL, "null argument");
+  CK(cudaSetDevice(device));
+  CK(cudaMalloc(ptr, bytes > 0 ? (size_t)bytes : 8));
+  return SS_OK;
+}
+int ssk_free(void* ptr) {
+  CK(cudaFree(ptr));
+  return SS_OK;
+}
+int ssk_memcpy(void* dst, const void* src, int64_t bytes, int kind) {
+  const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                           : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (bytes > 0) CK(cudaMemcpy(dst, src, (size_t)bytes, k));
+  return SS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1454 @@
+// ss_device.cuh — data model and step kernels of the B200 soft-snake step.
+//
+// Layout: every per-environment array is [item][E] with the environment
+// index innermost (E = padded env count). A CUDA block is W env-lanes x IL
+// item-lanes (W*IL = 256, W = min(E, 32)), so with E >= 32 a warp covers
+// 32 environments of ONE constraint: topology loads are warp-uniform
+// broadcasts and every state/J load is a coalesced 256-byte line; with E = 1
+// a warp covers 32 consecutive items of the single environment (item-major,
+// still coalesced). One code path serves the batched and single-env cases.
+//
+// Arithmetic restates the reference (softsnake/solver.py, constraints.py,
+// contact.py, state.py, kernels/numba_backend.py) with its evaluation order;
+// the library is compiled with --fmad=false so no FMA contraction changes a
+// rounding. Scatter-free J^T x: per DOF, an incidence list sorted in the
+// reference's accumulation order (family order of solver.py:354-367, element
+// ascending, column ascending; numba_backend.py:43-52) is gathered, so the
+// sums are bitwise the numba block_transpose sums. PCR scalars are per
+// environment, reduced deterministically (fixed tree + fixed block order).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#define DI __device__ __forceinline__
+#define SS_PSI_TO_PA 6894.76  // pneumatics.py:23
+#define SS_THREADS 256
+
+// incidence families (code bits 29..31)
+enum { F_DIST = 0, F_TET = 1, F_ATTP = 2, F_ATTB = 3, F_HINGE = 4, F_CN = 5, F_CF = 6 };
+
+struct Dims {
+  int E, W, lgW, tiles, n_real;
+  int P, nb, ndof, bd0, nd, nt, na, nh, nw, nq, ns, nch, links;
+  int ms, m, od, ot, oa, oh, on, of;
+  int act_enabled;
+};
+
+struct Par {
+  double h, gamma, hg[3], ground_h, margin, mu, fdyn, fb_delta, smin, smax, dmax;
+  double youngs, ki, kd, cap, supply, half_h;
+  int newton, pcr, substeps;
+};
+
+// scene topology, shared by every environment (item-indexed only)
+struct Topo {
+  const double *inv_mass, *body_inv_mass, *body_inertia;         // [P] [nb] [nb*9]
+  const int *d_i, *d_j, *d_chan;                                  // [nd]
+  const double *d_rest, *d_dyn;                                   // [nd]
+  const int* t_idx;                                               // [4][nt]
+  const double *t_rinv, *t_e3;                                    // [9][nt] [3][nt]
+  const int *a_p, *a_b;                                           // [na]
+  const double *a_anc, *a_dyn;                                    // [3][na] [na]
+  const int *h_a, *h_b;                                           // [nh]
+  const double *h_anca, *h_ancb, *h_axa, *h_t1, *h_t2, *h_dyn;    // [3][nh] ... [nh]
+  const int* w_body;                                              // [nw]
+  const double *w_rad, *w_axis;                                   // [nw] [3][nw]
+  const int* slot_part;                                           // [nq]
+  const int *inc_ptr, *inc;                                       // [P+nb+1], codes
+};
+
+// persistent per-environment state, [item][E]
+struct State {
+  double *pos, *vel;                    // [3P]
+  double *bpos, *bquat, *blin, *bang;   // [3nb] [4nb] [3nb] [3nb]
+  double* lam;                          // [ms] internal row order
+  double *quat, *dirs, *scale;          // [4][nt] [3][nd] [nd]
+  double *live, *target, *press;        // [nch]
+  double* warm;                         // [3][nw]
+  int* warm_valid;                      // [nw]
+  double* time;                         // [1]
+};
+
+// per-substep workspace, [item][E]
+struct Work {
+  double *v, *u;            // [ndof]
+  double* ang_inv;          // [9][nb]
+  double* res;              // [ms]
+  double* tJ;               // [72][nt]  (row i, column j) at (12 i + j)
+  double* rw;               // [3][na]
+  double* hJ;               // [60][nh]
+  double* wJ;               // [18][nw]  normal(6), friction0(6), friction1(6)
+  int* present;             // [ns]
+  double *gap, *actf, *dynn; // [ns]
+  double* lamc;             // [3ns] contact multipliers in contact-row order
+  double* bdiag;            // [m]
+  double *x, *r, *z, *p, *ap, *az, *d;  // [m]
+  double* part;             // [gy_red][E]
+  int* cnt;                 // [tiles]
+  double *rho, *alpha, *beta, *resid;  // [E]
+  int *broken, *nc_cnt, *inv_cnt, *nonfinite;  // [E]
+};
+
+struct Ctx {
+  Dims D;
+  Par p;
+  Topo T;
+  State S;
+  Work K;
+};
+
+#define SETUP                                              \
+  const int E = c.D.E;                                     \
+  const int lane = threadIdx.x & (c.D.W - 1);              \
+  const int il = threadIdx.x >> c.D.lgW;                   \
+  const int IL = blockDim.x >> c.D.lgW;                    \
+  const int env = blockIdx.x * c.D.W + lane;               \
+  (void)il;                                                \
+  (void)IL;
+#define FOR_ITEMS(it, n) for (int it = blockIdx.y * IL + il; it < (n); it += gridDim.y * IL)
+#define IX(item) ((size_t)(item) * E + env)
+
+// ------------------------------------------------------------ small math
+// numpy.maximum: NaN in a propagates
+DI double npmax(double a, double b) { return (a >= b || a != a) ? a : b; }
+
+// numpy_backend.py:91-104 (no renormalisation)
+DI void quat_to_mat(double w, double x, double y, double z, double* R) {
+  R[0] = 1.0 - 2.0 * (y * y + z * z);
+  R[1] = 2.0 * (x * y - w * z);
+  R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);
+  R[4] = 1.0 - 2.0 * (x * x + z * z);
+  R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);
+  R[7] = 2.0 * (y * z + w * x);
+  R[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+// state.py:16-21,44-51 rotation_matrix (normalised)
+DI void rot_normalized(const double* q, double* R) {
+  double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  if (n < 1e-12) {
+    quat_to_mat(1.0, 0.0, 0.0, 0.0, R);
+  } else {
+    quat_to_mat(q[0] / n, q[1] / n, q[2] / n, q[3] / n, R);
+  }
+}
+// np.einsum("nij,nj->ni") contracts length 3 as (p0 + p2) + p1
+DI void matvec_es(const double* R, const double* v, double* o) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o[i] = R[3 * i] * v[0] + R[3 * i + 2] * v[2] + R[3 * i + 1] * v[1];
+}
+DI double dot_es(const double* a, const double* b) { return a[0] * b[0] + a[2] * b[2] + a[1] * b[1]; }
+DI void matvec_seq(const double* R, const double* v, double* o) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o[i] = R[3 * i] * v[0] + R[3 * i + 1] * v[1] + R[3 * i + 2] * v[2];
+}
+DI void cross3(const double* a, const double* b, double* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+// 3x3 inverse by Gauss-Jordan with partial pivoting (for np.linalg.inv, state.py:262)
+DI void inv3(const double* A, double* X) {
+  double a[3][6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 6; ++j) a[i][j] = j < 3 ? A[3 * i + j] : (j - 3 == i ? 1.0 : 0.0);
+#pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < 3; ++r)
+      if (fabs(a[r][col]) > fabs(a[piv][col])) piv = r;
+    if (piv != col) {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        double t = a[col][j];
+        a[col][j] = a[piv][j];
+        a[piv][j] = t;
+      }
+    }
+    double dd = a[col][col];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) a[col][j] /= dd;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      if (r == col) continue;
+      double f = a[r][col];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) a[r][j] -= f * a[col][j];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) X[3 * i + j] = a[i][j + 3];
+}
+
+// pneumatics.py:62-72 (Python min/max semantics)
+DI double update_pressure(double p, double target, const Par& P) {
+  if (target > p) {
+    double dp = (target - p) / P.supply;
+    double a = p + P.supply * dp * dp * P.ki;
+    return target < a ? target : a;
+  }
+  if (target < p) {
+    double dec = p * P.kd;
+    double mn = P.cap < dec ? P.cap : dec;
+    double r = p - mn;
+    return r > 0.0 ? r : 0.0;
+  }
+  return p;
+}
+
+// minv diagonal entry for a global DOF (state.py:246-268): particles
+// inv_mass, bodies 1/m then diag(I_w^-1)
+DI double minv_diag_of(const Ctx& c, int dof, int env) {
+  const int E = c.D.E;
+  if (dof < c.D.bd0) return c.T.inv_mass[dof / 3];
+  int b = (dof - c.D.bd0) / 6, k = (dof - c.D.bd0) % 6;
+  if (k < 3) return c.T.body_inv_mass[b];
+  return c.K.ang_inv[IX((size_t)(4 * (k - 3)) * c.D.nb + b)];
+}
+
+// attachment J value (constraints.py:227-237): row i, column col of
+// [-I3 | I3 | -skew(R r)]
+DI double att_val(int i, int col, const double* rw) {
+  if (col < 3) return col == i ? -1.0 : 0.0;
+  if (col < 6) return col - 3 == i ? 1.0 : 0.0;
+  int k = col - 6;
+  if (i == 0) return k == 0 ? 0.0 : (k == 1 ? rw[2] : -rw[1]);
+  if (i == 1) return k == 0 ? -rw[2] : (k == 1 ? 0.0 : rw[0]);
+  return k == 0 ? rw[1] : (k == 1 ? -rw[0] : 0.0);
+}
+
+// ---------------------------------------------------- reduction helper
+// Deterministic per-env block reduction of `val`, then "last block" combine
+// over gridDim.y in fixed order. Returns true in the W threads of the last
+// block with il == 0 and the total in *tot.
+DI bool reduce_env(const Ctx& c, double val, double* tot) {
+  SETUP
+  __shared__ double red[SS_THREADS];
+  __shared__ int amlast;
+  red[threadIdx.x] = val;
+  __syncthreads();
+  for (int s = IL >> 1; s > 0; s >>= 1) {
+    if (il < s) red[threadIdx.x] += red[threadIdx.x + s * c.D.W];
+    __syncthreads();
+  }
+  if (il == 0) c.K.part[(size_t)blockIdx.y * E + env] = red[lane];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = atomicAdd(&c.K.cnt[blockIdx.x], 1);
+    amlast = (t == (int)gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!amlast) return false;
+  if (threadIdx.x == 0) c.K.cnt[blockIdx.x] = 0;
+  if (il != 0) return false;
+  double s = 0.0;
+  for (int y = 0; y < (int)gridDim.y; ++y) s += __ldcg(&c.K.part[(size_t)y * E + env]);
+  *tot = s;
+  return true;
+}
+
+// ================================================================ frame
+// Simulator.step head: ChannelBank.tick + _update_actuation
+// (solver.py:296-301, pneumatics.py:102-116, solver.py:279-282)
+__global__ void k_frame_begin(const Ctx c, const double* __restrict__ cmd, int has_cmd,
+                              int latency) {
+  SETUP
+  const int n = c.D.links > 0 ? c.D.links : 1;
+  FOR_ITEMS(i, n) {
+    if (i == 0) {
+      c.K.nc_cnt[env] = 0;
+      c.K.inv_cnt[env] = 0;
+      c.K.nonfinite[env] = 0;
+    }
+    if (i < c.D.links) {
+      if (has_cmd) {
+        int ce = env < c.D.n_real ? env : 0;
+        double a = cmd[(size_t)ce * c.D.links + i];
+        double left = 0.0, right = 0.0;
+        if (a > 0.0) right = a;
+        else if (a < 0.0) left = -a;
+        double* pl = &c.S.press[IX(2 * i)];
+        double* pr = &c.S.press[IX(2 * i + 1)];
+        if (latency) {
+          *pl = update_pressure(*pl, left, c.p);
+          *pr = update_pressure(*pr, right, c.p);
+        } else {
+          *pl = left;
+          *pr = right;
+        }
+      }
+      if (c.D.act_enabled) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          double pp = c.S.press[IX(2 * i + k)];
+          c.S.target[IX(2 * i + k)] = 1.0 + pp * SS_PSI_TO_PA / c.p.youngs;
+        }
+      }
+    }
+  }
+}
+
+// =============================================================== substep
+// _slew_actuation (solver.py:284-292), build_mass_inverse (state.py:246-268)
+// and _predict_velocities (solver.py:316-332). Items: P particles, nb
+// bodies, nch channels.
+__global__ void k_pre(const Ctx c) {
+  SETUP
+  const int P = c.D.P, nb = c.D.nb;
+  FOR_ITEMS(it, P + nb + c.D.nch) {
+    if (it < P) {
+      const bool live = c.T.inv_mass[it] > 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double vi = c.S.vel[IX(3 * it + a)];
+        c.K.v[IX(3 * it + a)] = live ? vi + c.p.hg[a] : vi;
+      }
+    } else if (it < P + nb) {
+      const int b = it - P;
+      double q[4], R[9], RI[9], iw[9], Ai[9];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = c.S.bquat[IX(4 * b + k)];
+      rot_normalized(q, R);
+      const double* I = c.T.body_inertia + 9 * b;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          RI[3 * i + j] = R[3 * i] * I[j] + R[3 * i + 1] * I[3 + j] + R[3 * i + 2] * I[6 + j];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          iw[3 * i + j] = RI[3 * i] * R[3 * j] + RI[3 * i + 1] * R[3 * j + 1] + RI[3 * i + 2] * R[3 * j + 2];
+      inv3(iw, Ai);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) c.K.ang_inv[IX((size_t)k * nb + b)] = Ai[k];
+      double w[3], iww[3], tau[3], t3[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) w[a] = c.S.bang[IX(3 * b + a)];
+      matvec_es(iw, w, iww);
+      cross3(w, iww, tau);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) tau[a] = -tau[a];
+      matvec_es(Ai, tau, t3);
+      const int o = c.D.bd0 + 6 * b;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        c.K.v[IX(o + a)] = c.S.blin[IX(3 * b + a)] + c.p.hg[a];
+        c.K.v[IX(o + 3 + a)] = w[a] + c.p.h * t3[a];
+      }
+    } else if (c.D.act_enabled) {
+      const int ch = it - P - nb;
+      double live = c.S.live[IX(ch)];
+      double d = c.S.target[IX(ch)] - live;
+      if (d < -c.p.dmax) d = -c.p.dmax;
+      else if (d > c.p.dmax) d = c.p.dmax;
+      c.S.live[IX(ch)] = live + d;
+    }
+  }
+}
+
+// detect_ground_contacts + FrictionState.for_contacts + contact_row_blocks
+// + block_rowdiag of the contact families (contact.py:62-93, 135-149,
+// 183-215; solver.py:421-424). One item per candidate slot: wheels first,
+// then contact particles in order; present slots are the reference's
+// compacted contact list in the same order.
+__global__ void k_slots(const Ctx c) {
+  SETUP
+  const int nw = c.D.nw, ns = c.D.ns;
+  FOR_ITEMS(s, ns) {
+    double gap;
+    int present;
+    double nv[6], f0[6], f1[6], md[6];
+    double lam_n = 0.0, lam_f0 = 0.0, lam_f1 = 0.0;
+    if (s < nw) {
+      const int b = c.T.w_body[s];
+      double q[4], R[9], ax[3], al[3], ctr[3];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = c.S.bquat[IX(4 * b + k)];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        ctr[a] = c.S.bpos[IX(3 * b + a)];
+        al[a] = c.T.w_axis[a * nw + s];
+      }
+      rot_normalized(q, R);
+      matvec_seq(R, al, ax);
+      double nd = 0.0 * ax[0] + 0.0 * ax[1] + 1.0 * ax[2];
+      double dv[3] = {0.0 - nd * ax[0], 0.0 - nd * ax[1], 1.0 - nd * ax[2]};
+      double dn = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+      if (dn < 1e-9) {
+        dv[0] = 1.0 - ax[0] * ax[0];
+        dv[1] = 0.0 - ax[0] * ax[1];
+        dv[2] = 0.0 - ax[0] * ax[2];
+        dn = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+      }
+      double pt[3], r[3], cr[3];
+      const double rad = c.T.w_rad[s];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) pt[a] = ctr[a] - rad * (dv[a] / dn);
+      gap = pt[2] - c.p.ground_h;
+      present = gap < c.p.margin;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) r[a] = pt[a] - ctr[a];
+      const double n[3] = {0.0, 0.0, 1.0}, t1[3] = {1.0, 0.0, 0.0}, t2[3] = {0.0, 1.0, 0.0};
+      cross3(r, n, cr);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { nv[a] = n[a]; nv[3 + a] = cr[a]; }
+      cross3(r, t1, cr);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { f0[a] = t1[a]; f0[3 + a] = cr[a]; }
+      cross3(r, t2, cr);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { f1[a] = t2[a]; f1[3 + a] = cr[a]; }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        c.K.wJ[IX((size_t)k * nw + s)] = nv[k];
+        c.K.wJ[IX((size_t)(6 + k) * nw + s)] = f0[k];
+        c.K.wJ[IX((size_t)(12 + k) * nw + s)] = f1[k];
+      }
+      const int o = c.D.bd0 + 6 * b;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) md[k] = minv_diag_of(c, o + k, env);
+      if (present && c.S.warm_valid[IX(s)]) {
+        lam_n = c.S.warm[IX(s)];
+        lam_f0 = c.S.warm[IX(nw + s)];
+        lam_f1 = c.S.warm[IX(2 * nw + s)];
+      }
+    } else {
+      const int pi = c.T.slot_part[s - nw];
+      gap = c.S.pos[IX(3 * pi + 2)] - c.p.ground_h;
+      present = gap < c.p.margin;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { nv[k] = 0.0; f0[k] = 0.0; f1[k] = 0.0; }
+      nv[2] = 1.0;
+      f0[0] = 1.0;
+      f1[1] = 1.0;
+      const double mp = c.T.inv_mass[pi], m0 = c.T.inv_mass[0];
+      md[0] = mp; md[1] = mp; md[2] = mp;
+      md[3] = m0; md[4] = m0; md[5] = m0;   // padded columns point at DOF 0
+    }
+    double dn_ = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      dn_ += nv[k] * nv[k] * md[k];
+      d0 += f0[k] * f0[k] * md[k];
+      d1 += f1[k] * f1[k] * md[k];
+    }
+    c.K.present[IX(s)] = present;
+    c.K.gap[IX(s)] = gap;
+    c.K.bdiag[IX(c.D.on + s)] = dn_;
+    c.K.bdiag[IX(c.D.of + s)] = d0;
+    c.K.bdiag[IX(c.D.of + ns + s)] = d1;
+    c.K.lamc[IX(s)] = lam_n;
+    c.K.lamc[IX(ns + s)] = lam_f0;
+    c.K.lamc[IX(2 * ns + s)] = lam_f1;
+    if (present) atomicAdd(&c.K.nc_cnt[env], 1);
+  }
+}
+
+// ------------------------------------------------------------- tetra eval
+// numba_backend.py:137-312. Core shared by the batched kernel and the
+// kernel-ABI mirror; J values and residuals go through the writer.
+template <typename Out>
+DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, int maxiter,
+                     Out& out, int* iters) {
+  double F[9], R[9], S[9], K[9], Ki[9], wv[12];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double x0 = X[a];
+    double Ds0 = X[3 + a] - x0, Ds1 = X[6 + a] - x0, Ds2 = X[9 + a] - x0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) F[3 * a + j] = Ds0 * Ri[j] + Ds1 * Ri[3 + j] + Ds2 * Ri[6 + j];
+  }
+  double detF = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+                F[2] * (F[3] * F[7] - F[4] * F[6]);
+  double qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+  int it = 0;
+  for (; it < maxiter; ++it) {
+    double r[9];
+    quat_to_mat(qw, qx, qy, qz, r);
+    double o0 = 0.0, o1 = 0.0, o2 = 0.0, tr = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double rc0 = r[j], rc1 = r[3 + j], rc2 = r[6 + j];
+      double f0 = F[j], f1 = F[3 + j], f2 = F[6 + j];
+      o0 += rc1 * f2 - rc2 * f1;
+      o1 += rc2 * f0 - rc0 * f2;
+      o2 += rc0 * f1 - rc1 * f0;
+      tr += rc0 * f0 + rc1 * f1 + rc2 * f2;
+    }
+    double s = 1.0 / (fabs(tr) + 1e-9);
+    o0 *= s;
+    o1 *= s;
+    o2 *= s;
+    double wn = sqrt(o0 * o0 + o1 * o1 + o2 * o2);
+    if (wn < tol) break;
+    double half = 0.5 * wn;
+    double cw = cos(half);
+    double sw = sin(half) / wn;
+    double dw = cw, dx = sw * o0, dy = sw * o1, dz = sw * o2;
+    double nw = dw * qw - dx * qx - dy * qy - dz * qz;
+    double nx = dw * qx + dx * qw + dy * qz - dz * qy;
+    double ny = dw * qy - dx * qz + dy * qw + dz * qx;
+    double nz = dw * qz + dx * qy - dy * qx + dz * qw;
+    double qn = sqrt(nw * nw + nx * nx + ny * ny + nz * nz);
+    qw = nw / qn;
+    qx = nx / qn;
+    qy = ny / qn;
+    qz = nz / qn;
+  }
+  if (iters) *iters = it;
+  q[0] = qw; q[1] = qx; q[2] = qy; q[3] = qz;
+  quat_to_mat(qw, qx, qy, qz, R);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) S[3 * i + j] = R[i] * F[j] + R[3 + i] * F[3 + j] + R[6 + i] * F[6 + j];
+  {
+    double m01 = 0.5 * (S[1] + S[3]);
+    S[1] = m01; S[3] = m01;
+    double m02 = 0.5 * (S[2] + S[6]);
+    S[2] = m02; S[6] = m02;
+    double m12 = 0.5 * (S[5] + S[7]);
+    S[5] = m12; S[7] = m12;
+  }
+  out.res(0, S[0] - 1.0);
+  out.res(1, S[4] - 1.0);
+  out.res(2, S[8] - 1.0);
+  out.res(3, S[5]);
+  out.res(4, S[2]);
+  out.res(5, S[1]);
+  double trS = S[0] + S[4] + S[8];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) K[i] = -S[i];
+  K[0] += trS + 1e-14;
+  K[4] += trS + 1e-14;
+  K[8] += trS + 1e-14;
+  double detK = K[0] * (K[4] * K[8] - K[5] * K[7]) - K[1] * (K[3] * K[8] - K[5] * K[6]) +
+                K[2] * (K[3] * K[7] - K[4] * K[6]);
+  if (fabs(detK) < 1e-30) detK = detK >= 0 ? 1e-30 : -1e-30;
+  double id = 1.0 / detK;
+  Ki[0] = (K[4] * K[8] - K[5] * K[7]) * id;
+  Ki[1] = (K[2] * K[7] - K[1] * K[8]) * id;
+  Ki[2] = (K[1] * K[5] - K[2] * K[4]) * id;
+  Ki[3] = (K[5] * K[6] - K[3] * K[8]) * id;
+  Ki[4] = (K[0] * K[8] - K[2] * K[6]) * id;
+  Ki[5] = (K[2] * K[3] - K[0] * K[5]) * id;
+  Ki[6] = (K[3] * K[7] - K[4] * K[6]) * id;
+  Ki[7] = (K[1] * K[6] - K[0] * K[7]) * id;
+  Ki[8] = (K[0] * K[4] - K[1] * K[3]) * id;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    wv[3 + j] = Ri[j];
+    wv[6 + j] = Ri[3 + j];
+    wv[9 + j] = Ri[6 + j];
+    wv[j] = -(wv[3 + j] + wv[6 + j] + wv[9 + j]);
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double G[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) G[3 * i + j] = R[3 * a + i] * wv[3 * v + j];
+      double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
+      double w0 = Ki[0] * g0 + Ki[1] * g1 + Ki[2] * g2;
+      double w1 = Ki[3] * g0 + Ki[4] * g1 + Ki[5] * g2;
+      double w2 = Ki[6] * g0 + Ki[7] * g1 + Ki[8] * g2;
+      double ws00 = -w2 * S[3] + w1 * S[6];
+      double ws01 = -w2 * S[4] + w1 * S[7];
+      double ws02 = -w2 * S[5] + w1 * S[8];
+      double ws10 = w2 * S[0] - w0 * S[6];
+      double ws11 = w2 * S[1] - w0 * S[7];
+      double ws12 = w2 * S[2] - w0 * S[8];
+      double ws20 = -w1 * S[0] + w0 * S[3];
+      double ws21 = -w1 * S[1] + w0 * S[4];
+      double ws22 = -w1 * S[2] + w0 * S[5];
+      const int col = 3 * v + a;
+      out.val(0, col, G[0] - ws00);
+      out.val(1, col, G[4] - ws11);
+      out.val(2, col, G[8] - ws22);
+      out.val(3, col, 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21));
+      out.val(4, col, 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20));
+      out.val(5, col, 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10));
+    }
+  return detF <= 0.0 ? 1 : 0;
+}
+
+struct TetOutBatched {
+  const Ctx* c;
+  int t, env;
+  double diag[6];
+  double im[4];
+  DI void res(int i, double v) {
+    const int E = c->D.E;
+    c->K.res[IX(c->D.ot + i * c->D.nt + t)] = v;
+  }
+  DI void val(int i, int col, double v) {
+    const int E = c->D.E;
+    c->K.tJ[IX((size_t)(12 * i + col) * c->D.nt + t)] = v;
+    diag[i] += v * v * im[col / 3];  // block_rowdiag, numba_backend.py:55-65
+  }
+};
+
+// TetraSet.eval + tetra rows of block_rowdiag + eh2 diag (solver.py:410-426)
+__global__ void __launch_bounds__(SS_THREADS) k_eval_tet(const Ctx c) {
+  SETUP
+  const int nt = c.D.nt;
+  FOR_ITEMS(t, nt) {
+    double X[12], Ri[9], q[4];
+    TetOutBatched o;
+    o.c = &c;
+    o.t = t;
+    o.env = env;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      int node = c.T.t_idx[v * nt + t];
+      o.im[v] = c.T.inv_mass[node];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) X[3 * v + a] = c.S.pos[IX(3 * node + a)];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Ri[k] = c.T.t_rinv[k * nt + t];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) o.diag[i] = 0.0;
+    int inv = tet_eval_core(X, Ri, q, 1e-12, 500, o, nullptr);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c.S.quat[IX(k * nt + t)] = q[k];
+    const double ed = c.T.t_e3[t], es = c.T.t_e3[2 * nt + t];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+      c.K.bdiag[IX(c.D.ot + i * nt + t)] = o.diag[i] + (i < 3 ? ed : es);
+    if (inv) atomicAdd(&c.K.inv_cnt[env], 1);
+  }
+}
+
+// DistanceSet.eval, AttachmentSet.eval, HingeSet.eval and their rowdiag
+// (constraints.py:88-100, 220-237, 312-349; numba_backend.py:105-120)
+__global__ void k_eval_misc(const Ctx c) {
+  SETUP
+  const int nd = c.D.nd, na = c.D.na, nh = c.D.nh, nb = c.D.nb;
+  FOR_ITEMS(it, nd + na + nh) {
+    if (it < nd) {
+      const int d = it, i = c.T.d_i[d], j = c.T.d_j[d];
+      double dx = c.S.pos[IX(3 * i)] - c.S.pos[IX(3 * j)];
+      double dy = c.S.pos[IX(3 * i + 1)] - c.S.pos[IX(3 * j + 1)];
+      double dz = c.S.pos[IX(3 * i + 2)] - c.S.pos[IX(3 * j + 2)];
+      double ln = sqrt(dx * dx + dy * dy + dz * dz);
+      double u0, u1, u2;
+      if (ln > 1e-12) {
+        u0 = dx / ln; u1 = dy / ln; u2 = dz / ln;
+        c.S.dirs[IX(d)] = u0;
+        c.S.dirs[IX(nd + d)] = u1;
+        c.S.dirs[IX(2 * nd + d)] = u2;
+      } else {
+        u0 = c.S.dirs[IX(d)]; u1 = c.S.dirs[IX(nd + d)]; u2 = c.S.dirs[IX(2 * nd + d)];
+      }
+      double sc;
+      const int ch = c.T.d_chan[d];
+      if (c.D.act_enabled && ch >= 0) {
+        sc = c.S.live[IX(ch)];
+        c.S.scale[IX(d)] = sc;
+      } else {
+        sc = c.S.scale[IX(d)];
+      }
+      c.K.res[IX(c.D.od + d)] = ln - c.T.d_rest[d] * sc;
+      const double mi = c.T.inv_mass[i], mj = c.T.inv_mass[j];
+      const double nu0 = -u0, nu1 = -u1, nu2 = -u2;
+      double acc = 0.0;
+      acc += u0 * u0 * mi;
+      acc += u1 * u1 * mi;
+      acc += u2 * u2 * mi;
+      acc += nu0 * nu0 * mj;
+      acc += nu1 * nu1 * mj;
+      acc += nu2 * nu2 * mj;
+      c.K.bdiag[IX(c.D.od + d)] = acc;
+    } else if (it < nd + na) {
+      const int a = it - nd, b = c.T.a_b[a], pi = c.T.a_p[a];
+      double R[9], anc[3], rw[3];
+      quat_to_mat(c.S.bquat[IX(4 * b)], c.S.bquat[IX(4 * b + 1)], c.S.bquat[IX(4 * b + 2)],
+                  c.S.bquat[IX(4 * b + 3)], R);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) anc[k] = c.T.a_anc[k * na + a];
+      matvec_es(R, anc, rw);
+      double md[9];
+      const double mp = c.T.inv_mass[pi];
+      const int o = c.D.bd0 + 6 * b;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        c.K.rw[IX(k * na + a)] = rw[k];
+        c.K.res[IX(c.D.oa + k * na + a)] =
+            c.S.bpos[IX(3 * b + k)] + rw[k] - c.S.pos[IX(3 * pi + k)];
+        md[k] = mp;
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) md[3 + k] = minv_diag_of(c, o + k, env);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int col = 0; col < 9; ++col) {
+          double v = att_val(i, col, rw);
+          acc += v * v * md[col];
+        }
+        c.K.bdiag[IX(c.D.oa + i * na + a)] = acc;
+      }
+    } else {
+      const int h = it - nd - na, ba = c.T.h_a[h], bb = c.T.h_b[h];
+      double Ra[9], Rb[9], v3[3], ra[3], rb[3], na_[3], t1[3], t2[3], c1[3], c2[3];
+      quat_to_mat(c.S.bquat[IX(4 * ba)], c.S.bquat[IX(4 * ba + 1)], c.S.bquat[IX(4 * ba + 2)],
+                  c.S.bquat[IX(4 * ba + 3)], Ra);
+      quat_to_mat(c.S.bquat[IX(4 * bb)], c.S.bquat[IX(4 * bb + 1)], c.S.bquat[IX(4 * bb + 2)],
+                  c.S.bquat[IX(4 * bb + 3)], Rb);
+#define LD3(src) for (int k = 0; k < 3; ++k) v3[k] = src[k * nh + h];
+      LD3(c.T.h_anca) matvec_es(Ra, v3, ra);
+      LD3(c.T.h_ancb) matvec_es(Rb, v3, rb);
+      LD3(c.T.h_axa) matvec_es(Ra, v3, na_);
+      LD3(c.T.h_t1) matvec_es(Rb, v3, t1);
+      LD3(c.T.h_t2) matvec_es(Rb, v3, t2);
+#undef LD3
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        c.K.res[IX(c.D.oh + k * nh + h)] =
+            c.S.bpos[IX(3 * ba + k)] + ra[k] - c.S.bpos[IX(3 * bb + k)] - rb[k];
+      c.K.res[IX(c.D.oh + 3 * nh + h)] = dot_es(t1, na_);
+      c.K.res[IX(c.D.oh + 4 * nh + h)] = dot_es(t2, na_);
+      double J[60];
+#pragma unroll
+      for (int k = 0; k < 60; ++k) J[k] = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        J[12 * a + a] = 1.0;
+        J[12 * a + 6 + a] = -1.0;
+      }
+      J[0 * 12 + 4] = ra[2]; J[0 * 12 + 5] = -ra[1];
+      J[1 * 12 + 3] = -ra[2]; J[1 * 12 + 5] = ra[0];
+      J[2 * 12 + 3] = ra[1]; J[2 * 12 + 4] = -ra[0];
+      J[0 * 12 + 10] = -rb[2]; J[0 * 12 + 11] = rb[1];
+      J[1 * 12 + 9] = rb[2]; J[1 * 12 + 11] = -rb[0];
+      J[2 * 12 + 9] = -rb[1]; J[2 * 12 + 10] = rb[0];
+      cross3(na_, t1, c1);
+      cross3(na_, t2, c2);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        J[3 * 12 + 3 + a] = c1[a]; J[3 * 12 + 9 + a] = -c1[a];
+        J[4 * 12 + 3 + a] = c2[a]; J[4 * 12 + 9 + a] = -c2[a];
+      }
+      double md[12];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        md[k] = minv_diag_of(c, c.D.bd0 + 6 * ba + k, env);
+        md[6 + k] = minv_diag_of(c, c.D.bd0 + 6 * bb + k, env);
+      }
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 12; ++j) {
+          double v = J[12 * i + j];
+          c.K.hJ[IX((size_t)(12 * i + j) * nh + h)] = v;
+          acc += v * v * md[j];
+        }
+        c.K.bdiag[IX(c.D.oh + i * nh + h)] = acc;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ J^T gather
+// mode 0 (apply_a, solver.py:380-387): w = J^T (act o x), u = M^-1 w.
+// mode 1 (_apply_impulse, solver.py:537-544): v += M^-1 J^T x over the
+// present contacts, friction rows regardless of the active set.
+// xs: static rows [ms][E]; xc: contact rows [3 ns][E].
+__global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
+                                                       const double* __restrict__ xs,
+                                                       const double* __restrict__ xc) {
+  SETUP
+  const int P = c.D.P, nt = c.D.nt, na = c.D.na, nh = c.D.nh, nw = c.D.nw, ns = c.D.ns;
+  FOR_ITEMS(it, P + c.D.nb) {
+    const int k0 = c.T.inc_ptr[it], k1 = c.T.inc_ptr[it + 1];
+    if (it < P) {
+      double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+      for (int k = k0; k < k1; ++k) {
+        const int code = c.T.inc[k];
+        const int fam = code >> 29, v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+        double a0, a1, a2;
+        if (fam == F_TET) {
+          double x6[6];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) x6[i] = xs[IX(c.D.ot + i * nt + e)];
+          a0 = 0.0; a1 = 0.0; a2 = 0.0;
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            const size_t base = (size_t)(12 * i + 3 * v) * nt + e;
+            a0 += c.K.tJ[(base)*E + env] * x6[i];
+            a1 += c.K.tJ[(base + nt) * E + env] * x6[i];
+            a2 += c.K.tJ[(base + 2 * (size_t)nt) * E + env] * x6[i];
+          }
+        } else if (fam == F_DIST) {
+          const int nd = c.D.nd;
+          const double xr = xs[IX(c.D.od + e)];
+          double d0 = c.S.dirs[IX(e)], d1 = c.S.dirs[IX(nd + e)], d2 = c.S.dirs[IX(2 * nd + e)];
+          if (v) { d0 = -d0; d1 = -d1; d2 = -d2; }
+          a0 = 0.0 + d0 * xr;
+          a1 = 0.0 + d1 * xr;
+          a2 = 0.0 + d2 * xr;
+        } else if (fam == F_ATTP) {
+          double x3[3], rw[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < 3; ++i) x3[i] = xs[IX(c.D.oa + i * na + e)];
+          double acc[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            acc[a] = 0.0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) acc[a] += att_val(i, a, rw) * x3[i];
+          }
+          a0 = acc[0]; a1 = acc[1]; a2 = acc[2];
+        } else {  // F_CN / F_CF on a particle slot: n = (0,0,1), t1 = (1,0,0), t2 = (0,1,0)
+          const bool on = mode == 0 ? (fam == F_CN ? c.K.present[IX(e)] != 0 : c.K.actf[IX(e)] != 0.0)
+                                    : c.K.present[IX(e)] != 0;
+          if (!on) continue;
+          if (fam == F_CN) {
+            const double xn = xc[IX(e)];
+            a0 = 0.0 + 0.0 * xn;
+            a1 = 0.0 + 0.0 * xn;
+            a2 = 0.0 + 1.0 * xn;
+          } else {
+            const double xf0 = xc[IX(ns + e)], xf1 = xc[IX(2 * ns + e)];
+            a0 = 0.0 + 1.0 * xf0;
+            a0 += 0.0 * xf1;
+            a1 = 0.0 + 0.0 * xf0;
+            a1 += 1.0 * xf1;
+            a2 = 0.0 + 0.0 * xf0;
+            a2 += 0.0 * xf1;
+          }
+        }
+        w0 += a0;
+        w1 += a1;
+        w2 += a2;
+      }
+      const double im = c.T.inv_mass[it];
+      const double u0 = im * w0, u1 = im * w1, u2 = im * w2;
+      if (mode == 0) {
+        c.K.u[IX(3 * it)] = u0;
+        c.K.u[IX(3 * it + 1)] = u1;
+        c.K.u[IX(3 * it + 2)] = u2;
+      } else {
+        c.K.v[IX(3 * it)] += u0;
+        c.K.v[IX(3 * it + 1)] += u1;
+        c.K.v[IX(3 * it + 2)] += u2;
+      }
+    } else {
+      const int b = it - P;
+      double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int k = k0; k < k1; ++k) {
+        const int code = c.T.inc[k];
+        const int fam = code >> 29, v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+        double acc[6];
+        if (fam == F_ATTB) {
+          double x3[3], rw[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            x3[i] = xs[IX(c.D.oa + i * na + e)];
+            rw[i] = c.K.rw[IX(i * na + e)];
+          }
+#pragma unroll
+          for (int kk = 0; kk < 6; ++kk) {
+            acc[kk] = 0.0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) acc[kk] += att_val(i, 3 + kk, rw) * x3[i];
+          }
+        } else if (fam == F_HINGE) {
+          double x5[5];
+#pragma unroll
+          for (int i = 0; i < 5; ++i) x5[i] = xs[IX(c.D.oh + i * nh + e)];
+#pragma unroll
+          for (int kk = 0; kk < 6; ++kk) {
+            acc[kk] = 0.0;
+#pragma unroll
+            for (int i = 0; i < 5; ++i)
+              acc[kk] += c.K.hJ[IX((size_t)(12 * i + 6 * v + kk) * nh + e)] * x5[i];
+          }
+        } else {  // wheel slot e (< nw)
+          const bool on = mode == 0 ? (fam == F_CN ? c.K.present[IX(e)] != 0 : c.K.actf[IX(e)] != 0.0)
+                                    : c.K.present[IX(e)] != 0;
+          if (!on) continue;
+          if (fam == F_CN) {
+            const double xn = xc[IX(e)];
+#pragma unroll
+            for (int kk = 0; kk < 6; ++kk) acc[kk] = 0.0 + c.K.wJ[IX((size_t)kk * nw + e)] * xn;
+          } else {
+            const double xf0 = xc[IX(ns + e)], xf1 = xc[IX(2 * ns + e)];
+#pragma unroll
+            for (int kk = 0; kk < 6; ++kk) {
+              acc[kk] = 0.0 + c.K.wJ[IX((size_t)(6 + kk) * nw + e)] * xf0;
+              acc[kk] += c.K.wJ[IX((size_t)(12 + kk) * nw + e)] * xf1;
+            }
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 6; ++kk) w[kk] += acc[kk];
+      }
+      // minv_apply (numba_backend.py:68-82)
+      const double im = c.T.body_inv_mass[b];
+      double u[6];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) u[a] = im * w[a];
+      const int nb = c.D.nb;
+      double A[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) A[k] = c.K.ang_inv[IX((size_t)k * nb + b)];
+      u[3] = A[0] * w[3] + A[1] * w[4] + A[2] * w[5];
+      u[4] = A[3] * w[3] + A[4] * w[4] + A[5] * w[5];
+      u[5] = A[6] * w[3] + A[7] * w[4] + A[8] * w[5];
+      const int o = c.D.bd0 + 6 * b;
+      if (mode == 0) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) c.K.u[IX(o + k)] = u[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) c.K.v[IX(o + k)] += u[k];
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------- J rows
+// block_forward of each family on a DOF vector vec ([ndof][E]);
+// numba_backend.py:31-40 order (j ascending from acc = 0).
+DI double row_dist(const Ctx& c, int d, const double* vec, int env) {
+  const int E = c.D.E, nd = c.D.nd;
+  const int i = c.T.d_i[d], j = c.T.d_j[d];
+  const double u0 = c.S.dirs[IX(d)], u1 = c.S.dirs[IX(nd + d)], u2 = c.S.dirs[IX(2 * nd + d)];
+  double acc = 0.0;
+  acc += u0 * vec[IX(3 * i)];
+  acc += u1 * vec[IX(3 * i + 1)];
+  acc += u2 * vec[IX(3 * i + 2)];
+  acc += -u0 * vec[IX(3 * j)];
+  acc += -u1 * vec[IX(3 * j + 1)];
+  acc += -u2 * vec[IX(3 * j + 2)];
+  return acc;
+}
+DI void rows_tet(const Ctx& c, int t, const double* vec, int env, double* y) {
+  const int E = c.D.E, nt = c.D.nt;
+  double uu[12];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int node = c.T.t_idx[v * nt + t];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) uu[3 * v + a] = vec[IX(3 * node + a)];
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) acc += c.K.tJ[IX((size_t)(12 * i + j) * nt + t)] * uu[j];
+    y[i] = acc;
+  }
+}
+DI void rows_att(const Ctx& c, int a, const double* vec, int env, double* y) {
+  const int E = c.D.E, na = c.D.na;
+  const int pi = c.T.a_p[a], o = c.D.bd0 + 6 * c.T.a_b[a];
+  double uu[9], rw[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    uu[k] = vec[IX(3 * pi + k)];
+    rw[k] = c.K.rw[IX(k * na + a)];
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) uu[3 + k] = vec[IX(o + k)];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) acc += att_val(i, j, rw) * uu[j];
+    y[i] = acc;
+  }
+}
+DI void rows_hinge(const Ctx& c, int h, const double* vec, int env, double* y) {
+  const int E = c.D.E, nh = c.D.nh;
+  const int oa = c.D.bd0 + 6 * c.T.h_a[h], ob = c.D.bd0 + 6 * c.T.h_b[h];
+  double uu[12];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    uu[k] = vec[IX(oa + k)];
+    uu[6 + k] = vec[IX(ob + k)];
+  }
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) acc += c.K.hJ[IX((size_t)(12 * i + j) * nh + h)] * uu[j];
+    y[i] = acc;
+  }
+}
+// contact slot rows (normal, friction0, friction1) for a present slot
+DI void rows_slot(const Ctx& c, int s, const double* vec, int env, double* y) {
+  const int E = c.D.E, nw = c.D.nw;
+  if (s < nw) {
+    const int o = c.D.bd0 + 6 * c.T.w_body[s];
+    double uu[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) uu[k] = vec[IX(o + k)];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) acc += c.K.wJ[IX((size_t)(6 * r + k) * nw + s)] * uu[k];
+      y[r] = acc;
+    }
+  } else {
+    const int pi = c.T.slot_part[s - nw];
+    const double x0 = vec[IX(3 * pi)], x1 = vec[IX(3 * pi + 1)], x2 = vec[IX(3 * pi + 2)];
+    const double z0 = vec[IX(0)];
+    // padded columns 3..5 reference DOF 0 with zero values (contact.py:210-214)
+    double a = 0.0;
+    a += 0.0 * x0; a += 0.0 * x1; a += 1.0 * x2; a += 0.0 * z0; a += 0.0 * z0; a += 0.0 * z0;
+    y[0] = a;
+    a = 0.0;
+    a += 1.0 * x0; a += 0.0 * x1; a += 0.0 * x2; a += 0.0 * z0; a += 0.0 * z0; a += 0.0 * z0;
+    y[1] = a;
+    a = 0.0;
+    a += 0.0 * x0; a += 1.0 * x1; a += 0.0 * x2; a += 0.0 * z0; a += 0.0 * z0; a += 0.0 * z0;
+    y[2] = a;
+  }
+}
+
+// Newton head: jv = J v, velocity-level rhs, FB rows, friction active set,
+// Jacobi diagonal; PCR setup r = rhs, z = r/d, x = 0 (solver.py:439-478,
+// 36-48, 62-69; contact.py:151-155).
+__global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
+  SETUP
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const double g = c.p.gamma, h = c.p.h;
+  const double* v = c.K.v;
+#define SETROW(row, rhsv, diagv)                            \
+  {                                                         \
+    const double dg_ = (diagv);                             \
+    const double d_ = dg_ > 1e-300 ? dg_ : 1.0;             \
+    const double r_ = (rhsv);                               \
+    c.K.r[IX(row)] = r_;                                    \
+    c.K.d[IX(row)] = d_;                                    \
+    c.K.z[IX(row)] = r_ / d_;                               \
+    c.K.x[IX(row)] = 0.0;                                   \
+  }
+  FOR_ITEMS(it, nd + nt + na + nh + ns) {
+    if (it < nd) {
+      const int row = c.D.od + it;
+      const double jv = row_dist(c, it, v, env);
+      const double dyn = c.T.d_dyn[it];
+      SETROW(row, -(g * c.K.res[IX(row)] / h + jv + dyn * c.S.lam[IX(row)]),
+             npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
+    } else if (it < nd + nt) {
+      const int t = it - nd;
+      double jv[6], lm[6];
+      rows_tet(c, t, v, env, jv);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
+      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
+      // ereg_apply(eh2, lam_tetra) (numba_backend.py:85-94), isotropic pattern
+      double el[6];
+      el[0] = 0.0 + ed * lm[0]; el[0] += eo * lm[1]; el[0] += eo * lm[2];
+      el[1] = 0.0 + eo * lm[0]; el[1] += ed * lm[1]; el[1] += eo * lm[2];
+      el[2] = 0.0 + eo * lm[0]; el[2] += eo * lm[1]; el[2] += ed * lm[2];
+      el[3] = 0.0 + es * lm[3];
+      el[4] = 0.0 + es * lm[4];
+      el[5] = 0.0 + es * lm[5];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const int row = c.D.ot + i * nt + t;
+        SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + el[i]),
+               npmax(c.K.bdiag[IX(row)] + 0.0, 1e-30));
+      }
+    } else if (it < nd + nt + na) {
+      const int a = it - nd - nt;
+      double jv[3];
+      rows_att(c, a, v, env, jv);
+      const double dyn = c.T.a_dyn[a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int row = c.D.oa + i * na + a;
+        SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + dyn * c.S.lam[IX(row)]),
+               npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
+      }
+    } else if (it < nd + nt + na + nh) {
+      const int hh = it - nd - nt - na;
+      double jv[5];
+      rows_hinge(c, hh, v, env, jv);
+      const double dyn = c.T.h_dyn[hh];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int row = c.D.oh + i * nh + hh;
+        SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + dyn * c.S.lam[IX(row)]),
+               npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
+      }
+    } else {
+      const int s = it - nd - nt - na - nh;
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+      if (!c.K.present[IX(s)]) {
+        SETROW(rn, 0.0, 1.0);
+        SETROW(rf0, 0.0, 1.0);
+        SETROW(rf1, 0.0, 1.0);
+        c.K.actf[IX(s)] = 0.0;
+        c.K.dynn[IX(s)] = 0.0;
+        continue;
+      }
+      double jv[3];
+      rows_slot(c, s, v, env, jv);
+      const double ln = c.K.lamc[IX(s)];
+      const double a = c.K.gap[IX(s)] / h + jv[0];
+      const double b = ln;
+      const double root = sqrt(a * a + b * b + c.p.fb_delta);
+      const double phi = a + b - root;
+      double da = 1.0 - a / root;
+      const double db = 1.0 - b / root;
+      if (da < c.p.smin) da = c.p.smin;
+      else if (da > c.p.smax) da = c.p.smax;
+      const double dynn = db / da;
+      c.K.dynn[IX(s)] = dynn;
+      SETROW(rn, -phi / da, npmax(c.K.bdiag[IX(rn)] + dynn, 1e-30));
+      const double on = (c.p.mu * npmax(ln, 0.0) > 0.0) ? 1.0 : 0.0;
+      c.K.actf[IX(s)] = on;
+      const double fd = c.p.fdyn;
+      const double lf0 = c.K.lamc[IX(ns + s)], lf1 = c.K.lamc[IX(2 * ns + s)];
+      SETROW(rf0, -on * (jv[1] + fd * lf0),
+             on > 0.0 ? npmax(c.K.bdiag[IX(rf0)] + fd, 1e-30) : 1.0);
+      SETROW(rf1, -on * (jv[2] + fd * lf1),
+             on > 0.0 ? npmax(c.K.bdiag[IX(rf1)] + fd, 1e-30) : 1.0);
+    }
+  }
+#undef SETROW
+}
+
+// az = A z rows (apply_a second half, solver.py:388-399) + rho partial z.az.
+// setup != 0: rho = z.az (pcr_solve setup, solver.py:70-73); else
+// beta = rho_new / rho (solver.py:87-89).
+__global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setup) {
+  SETUP
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const double* u = c.K.u;
+  const double* z = c.K.z;
+  double part = 0.0;
+  FOR_ITEMS(it, nd + nt + na + nh + ns) {
+    if (it < nd) {
+      const int row = c.D.od + it;
+      const double zr = z[IX(row)];
+      const double az = row_dist(c, it, u, env) + c.T.d_dyn[it] * zr;
+      c.K.az[IX(row)] = az;
+      part += zr * az;
+    } else if (it < nd + nt) {
+      const int t = it - nd;
+      double y[6], zz[6];
+      rows_tet(c, t, u, env, y);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
+      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
+      double ez[6];
+      ez[0] = 0.0 + ed * zz[0]; ez[0] += eo * zz[1]; ez[0] += eo * zz[2];
+      ez[1] = 0.0 + eo * zz[0]; ez[1] += ed * zz[1]; ez[1] += eo * zz[2];
+      ez[2] = 0.0 + eo * zz[0]; ez[2] += eo * zz[1]; ez[2] += ed * zz[2];
+      ez[3] = 0.0 + es * zz[3];
+      ez[4] = 0.0 + es * zz[4];
+      ez[5] = 0.0 + es * zz[5];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double az = y[i] + ez[i];
+        c.K.az[IX(c.D.ot + i * nt + t)] = az;
+        part += zz[i] * az;
+      }
+    } else if (it < nd + nt + na) {
+      const int a = it - nd - nt;
+      double y[3];
+      rows_att(c, a, u, env, y);
+      const double dyn = c.T.a_dyn[a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int row = c.D.oa + i * na + a;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else if (it < nd + nt + na + nh) {
+      const int hh = it - nd - nt - na;
+      double y[5];
+      rows_hinge(c, hh, u, env, y);
+      const double dyn = c.T.h_dyn[hh];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int row = c.D.oh + i * nh + hh;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else {
+      const int s = it - nd - nt - na - nh;
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+      const double zn = z[IX(rn)], z0 = z[IX(rf0)], z1 = z[IX(rf1)];
+      double an = zn, a0 = z0, a1 = z1;
+      const bool pres = c.K.present[IX(s)] != 0;
+      if (pres) {
+        double y[3];
+        rows_slot(c, s, u, env, y);
+        an = y[0] + c.K.dynn[IX(s)] * zn;
+        if (c.K.actf[IX(s)] != 0.0) {
+          a0 = y[1] + c.p.fdyn * z0;
+          a1 = y[2] + c.p.fdyn * z1;
+        }
+      }
+      c.K.az[IX(rn)] = an;
+      c.K.az[IX(rf0)] = a0;
+      c.K.az[IX(rf1)] = a1;
+      part += zn * an;
+      part += z0 * a0;
+      part += z1 * a1;
+    }
+  }
+  double tot;
+  if (reduce_env(c, part, &tot)) {
+    if (setup) {
+      c.K.rho[env] = tot;
+    } else if (!c.K.broken[env]) {
+      const double rho = c.K.rho[env];
+      c.K.beta[env] = rho > 1e-300 ? tot / rho : 0.0;
+      c.K.rho[env] = tot;
+    }
+  }
+}
+
+// p = z + beta p, ap = az + beta ap (setup: copies), then den = ap.(ap/d)
+// and alpha = rho/den with the breakdown guard (solver.py:71-81, 90-91).
+__global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) {
+  SETUP
+  const bool brk = c.K.broken[env] != 0;
+  const double beta = c.K.beta[env];
+  double part = 0.0;
+  FOR_ITEMS(row, c.D.m) {
+    double ap;
+    if (setup) {
+      c.K.p[IX(row)] = c.K.z[IX(row)];
+      ap = c.K.az[IX(row)];
+      c.K.ap[IX(row)] = ap;
+    } else if (!brk) {
+      c.K.p[IX(row)] = c.K.z[IX(row)] + beta * c.K.p[IX(row)];
+      ap = c.K.az[IX(row)] + beta * c.K.ap[IX(row)];
+      c.K.ap[IX(row)] = ap;
+    } else {
+      ap = c.K.ap[IX(row)];
+    }
+    part += ap * (ap / c.K.d[IX(row)]);
+  }
+  double den;
+  if (reduce_env(c, part, &den)) {
+    if (!c.K.broken[env]) {
+      if (den <= 1e-300 || !isfinite(den)) c.K.broken[env] = 1;
+      else c.K.alpha[env] = c.K.rho[env] / den;
+    }
+  }
+}
+
+// x += alpha p, r -= alpha ap, z = r/d (solver.py:81-84); with want_rz the
+// preconditioned residual sqrt(max(r.z, 0)) of the solve (solver.py:85).
+__global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c, int update, int want_rz) {
+  SETUP
+  const bool brk = c.K.broken[env] != 0;
+  const double alpha = c.K.alpha[env];
+  double part = 0.0;
+  FOR_ITEMS(row, c.D.m) {
+    double r = c.K.r[IX(row)], z;
+    if (update && !brk) {
+      c.K.x[IX(row)] += alpha * c.K.p[IX(row)];
+      r -= alpha * c.K.ap[IX(row)];
+      z = r / c.K.d[IX(row)];
+      c.K.r[IX(row)] = r;
+      c.K.z[IX(row)] = z;
+    } else {
+      z = c.K.z[IX(row)];
+    }
+    part += r * z;
+  }
+  if (!want_rz) return;
+  double rz;
+  if (reduce_env(c, part, &rz)) c.K.resid[env] = sqrt(0.0 > rz ? 0.0 : rz);
+}
+
+// pcr_solve's per-solve reset
+__global__ void k_pcr_reset(const Ctx c) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env < c.D.E) {
+    c.K.broken[env] = 0;
+    c.K.beta[env] = 0.0;
+  }
+}
+
+// Multiplier update, FrictionState.project, and dlambda = lam_after -
+// lam_before into az (solver.py:487-509, contact.py:157-165); on the last
+// Newton pass also store_warm (contact.py:167-180).
+__global__ void k_newton_update(const Ctx c, int last) {
+  SETUP
+  const int ms = c.D.ms, ns = c.D.ns, nw = c.D.nw;
+  FOR_ITEMS(it, ms + ns) {
+    if (it < ms) {
+      const double l0 = c.S.lam[IX(it)];
+      const double l1 = l0 + c.K.x[IX(it)];
+      c.S.lam[IX(it)] = l1;
+      c.K.az[IX(it)] = l1 - l0;
+    } else {
+      const int s = it - ms;
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+      const bool pres = c.K.present[IX(s)] != 0;
+      double n1 = 0.0, a1 = 0.0, b1 = 0.0;
+      if (pres) {
+        const double n0 = c.K.lamc[IX(s)], a0 = c.K.lamc[IX(ns + s)], b0 = c.K.lamc[IX(2 * ns + s)];
+        n1 = n0 + c.K.x[IX(rn)];
+        a1 = a0 + c.K.x[IX(rf0)];
+        b1 = b0 + c.K.x[IX(rf1)];
+        n1 = npmax(n1, 0.0);
+        const double rad = c.p.mu * npmax(n1, 0.0);
+        const double nrm = sqrt(a1 * a1 + b1 * b1);
+        if (nrm > rad) {
+          const double sc = nrm > 0.0 ? rad / nrm : 0.0;
+          a1 *= sc;
+          b1 *= sc;
+        }
+        c.K.lamc[IX(s)] = n1;
+        c.K.lamc[IX(ns + s)] = a1;
+        c.K.lamc[IX(2 * ns + s)] = b1;
+        c.K.az[IX(rn)] = n1 - n0;
+        c.K.az[IX(rf0)] = a1 - a0;
+        c.K.az[IX(rf1)] = b1 - b0;
+      } else {
+        c.K.az[IX(rn)] = 0.0;
+        c.K.az[IX(rf0)] = 0.0;
+        c.K.az[IX(rf1)] = 0.0;
+      }
+      if (last && s < nw) {
+        c.S.warm_valid[IX(s)] = pres ? 1 : 0;
+        c.S.warm[IX(s)] = n1;
+        c.S.warm[IX(nw + s)] = a1;
+        c.S.warm[IX(2 * nw + s)] = b1;
+      }
+    }
+  }
+}
+
+// set_velocities + integrate_pose + quat_step (state.py:155-160, 171-192)
+__global__ void k_integrate(const Ctx c) {
+  SETUP
+  const int P = c.D.P;
+  const double h = c.p.h;
+  FOR_ITEMS(it, P + c.D.nb) {
+    if (it == 0) c.S.time[env] = c.S.time[env] + h;
+    if (it < P) {
+      bool bad = false;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double vv = c.K.v[IX(3 * it + a)];
+        c.S.vel[IX(3 * it + a)] = vv;
+        const double x = c.S.pos[IX(3 * it + a)] + h * vv;
+        c.S.pos[IX(3 * it + a)] = x;
+        bad |= !isfinite(x);
+      }
+      if (bad) c.K.nonfinite[env] = 1;
+    } else {
+      const int b = it - P, o = c.D.bd0 + 6 * b;
+      double w[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double lv = c.K.v[IX(o + a)];
+        w[a] = c.K.v[IX(o + 3 + a)];
+        c.S.blin[IX(3 * b + a)] = lv;
+        c.S.bang[IX(3 * b + a)] = w[a];
+        c.S.bpos[IX(3 * b + a)] = c.S.bpos[IX(3 * b + a)] + h * lv;
+      }
+      double q[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = c.S.bquat[IX(4 * b + k)];
+      const double ch = c.p.half_h;
+      const double r0 = q[0] - ch * (w[0] * q[1] + w[1] * q[2] + w[2] * q[3]);
+      const double r1 = q[1] + ch * (w[0] * q[0] + w[1] * q[3] - w[2] * q[2]);
+      const double r2 = q[2] + ch * (-w[0] * q[3] + w[1] * q[0] + w[2] * q[1]);
+      const double r3 = q[3] + ch * (w[0] * q[2] - w[1] * q[1] + w[2] * q[0]);
+      const double nrm = sqrt(r0 * r0 + r1 * r1 + r2 * r2 + r3 * r3);
+      c.S.bquat[IX(4 * b)] = r0 / nrm;
+      c.S.bquat[IX(4 * b + 1)] = r1 / nrm;
+      c.S.bquat[IX(4 * b + 2)] = r2 / nrm;
+      c.S.bquat[IX(4 * b + 3)] = r3 / nrm;
+    }
+  }
+}
+
+// center_of_mass (state.py:285-292), one thread per env (readback only)
+__global__ void k_com(const Ctx c, int env0, int n, double* out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int env = env0 + e, E = c.D.E;
+  double tot = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+  for (int i = 0; i < c.D.P; ++i) {
+    const double im = c.T.inv_mass[i];
+    if (!(im > 0.0)) continue;
+    const double m = 1.0 / im;
+    tot += m;
+    cx += m * c.S.pos[IX(3 * i)];
+    cy += m * c.S.pos[IX(3 * i + 1)];
+    cz += m * c.S.pos[IX(3 * i + 2)];
+  }
+  for (int b = 0; b < c.D.nb; ++b) {
+    const double m = 1.0 / c.T.body_inv_mass[b];
+    tot += m;
+    cx += m * c.S.bpos[IX(3 * b)];
+    cy += m * c.S.bpos[IX(3 * b + 1)];
+    cz += m * c.S.bpos[IX(3 * b + 2)];
+  }
+  out[3 * e] = cx / tot;
+  out[3 * e + 1] = cy / tot;
+  out[3 * e + 2] = cz / tot;
+}
+
+// host env-major [n][A*B] <-> device [item][E] (item = swap ? b*A+a : a*B+b).
+// Scatter also replicates env 0 into the padding lanes [n_real, E).
+template <typename T>
+__global__ void k_scatter(T* dst, const T* src, int n, int A, int B, int swap, int E, int env0,
+                          int n_real) {
+  const size_t K = (size_t)A * B;
+  const size_t tot = K * E;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot;
+       g += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(g % E);
+    const size_t k = g / E;
+    int se;
+    if (e >= env0 && e < env0 + n) se = e - env0;
+    else if (env0 == 0 && e >= n_real) se = 0;
+    else continue;
+    const size_t a = k / B, b = k % B;
+    const size_t item = swap ? b * A + a : k;
+    dst[item * E + e] = src[(size_t)se * K + k];
+  }
+}
+template <typename T>
+__global__ void k_gather_state(T* dst, const T* src, int n, int A, int B, int swap, int E,
+                               int env0) {
+  const size_t K = (size_t)A * B;
+  const size_t tot = K * n;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot;
+       g += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(g / K);
+    const size_t k = g % K;
+    const size_t a = k / B, b = k % B;
+    const size_t item = swap ? b * A + a : k;
+    dst[g] = src[item * E + env0 + e];
+  }
+}

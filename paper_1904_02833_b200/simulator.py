@@ -1,0 +1,330 @@
+"""Drop-in Simulator (softsnake/solver.py:154-544) on the B200.
+
+`BatchedSimulator` owns one device handle holding N independent copies of
+a scene (the RL-rollout shape); `Simulator` is the single-environment
+drop-in with the reference's attribute surface: `step(commands, latency)`
+returning StepStats, `state`, `channels.pressures`, `stats`, `totals`,
+`static_rows`, `lam_*`. All stepping runs in libsoftsnake_b200.so; the
+host objects only mirror state on readback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time as _time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._abi import (STATE_FIELDS, PackedTopology, SsEnvStats, StateBuffers,
+                   pack_params)
+
+
+@dataclass
+class SolverConfig:
+    """solver.py:95-117 (backend/keep_matrix kept for signature parity)."""
+    dt: float = 1.0 / 60.0
+    substeps: int = 2
+    newton_iters: int = 4
+    pcr_iters: int = 20
+    gravity: tuple = (0.0, 0.0, -9.81)
+    ground_height: float = 0.0
+    ground_enabled: bool = True
+    contact_margin: float = 0.005
+    mu: float = 1.0
+    friction_compliance: float = 1e-8
+    fb_delta: float = 1e-10
+    fb_slope_min: float = 1e-6
+    fb_slope_max: float = 2.0
+    max_strain_rate: float = 6.0
+    constraint_damping: float = 1.0
+    backend: str | None = None
+    keep_matrix: bool = False
+
+    @property
+    def h(self) -> float:
+        return self.dt / self.substeps
+
+
+@dataclass
+class StepStats:
+    """solver.py:142-151"""
+    newton_iterations: int = 0
+    pcr_iterations: int = 0
+    contact_count: int = 0
+    inverted_tets: int = 0
+    residual: float = 0.0
+    wall_time: float = 0.0
+    assembly_time: float = 0.0
+    solve_time: float = 0.0
+
+
+def _dims_of(packed: PackedTopology) -> dict:
+    return packed.dims
+
+
+class BatchedSimulator:
+    """N independent environments of one scene on one GPU.
+
+    The constructor mirrors Simulator(state, config, distances, tetras,
+    attachments, hinges, wheels, channels, strain, contact_particles)
+    (solver.py:157-165); every env starts from `state` and the sets'
+    persistent arrays (quats, dirs, scale). The device handle is created on
+    first use so scene edits made after construction (e.g. the bend
+    fixture's clamp, snake.py:363-364) are honoured.
+    """
+
+    def __init__(self, n_envs: int, state, config: SolverConfig | None = None,
+                 distances=None, tetras=None, attachments=None, hinges=None,
+                 wheels=None, channels=None, strain=None, contact_particles=None,
+                 device: int = 0):
+        if n_envs < 1:
+            raise ValueError("n_envs must be >= 1")
+        self.n_envs = int(n_envs)
+        self.state = state
+        self.config = config if config is not None else SolverConfig()
+        self.distances, self.tetras = distances, tetras
+        self.attachments, self.hinges = attachments, hinges
+        self.wheels = list(wheels) if wheels is not None else []
+        self.channels, self.strain = channels, strain
+        self.contact_particles = contact_particles
+        self.device = int(device)
+        self._h = None
+        self._packed = None
+        self.frames = 0
+        nd = distances.count if distances is not None else 0
+        nt = tetras.count if tetras is not None else 0
+        na = attachments.count if attachments is not None else 0
+        nh = hinges.count if hinges is not None else 0
+        self._m_static = nd + 6 * nt + 3 * na + 5 * nh
+
+    # ------------------------------------------------------------ lifecycle
+    @property
+    def static_rows(self) -> int:
+        return self._m_static
+
+    @property
+    def n_links(self) -> int:
+        ch = self.channels
+        return 0 if ch is None else int(np.asarray(ch.pressures).shape[0]) // 2
+
+    def _ensure(self):
+        if self._h is not None:
+            return self._h
+        L = _native.lib()
+        self._packed = PackedTopology(self.state, self.distances, self.tetras,
+                                      self.attachments, self.hinges, self.wheels,
+                                      self.channels, self.strain, self.contact_particles)
+        params = pack_params(self.config, self._packed)
+        h = C.c_void_p()
+        _native.check(L.ss_create(C.byref(self._packed.struct), C.byref(params),
+                                  self.n_envs, self.device, C.byref(h)))
+        self._h = h
+        self.set_state_arrays(self._initial_state_arrays(), env0=0, n=self.n_envs)
+        return h
+
+    def close(self):
+        if self._h is not None:
+            _native.lib().ss_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _initial_state_arrays(self) -> dict:
+        """Per-env state from the host containers (reference defaults)."""
+        st, d = self.state, self._packed.dims
+        one = {
+            "positions": st.particles.positions, "velocities": st.particles.velocities,
+            "body_pos": st.body_pos, "body_quat": st.body_quat,
+            "body_lin_vel": st.body_lin_vel, "body_ang_vel": st.body_ang_vel,
+            "lam_dist": np.zeros(d["nd"]), "lam_tetra": np.zeros((d["nt"], 6)),
+            "lam_attach": np.zeros((d["na"], 3)), "lam_hinge": np.zeros((d["nh"], 5)),
+            "tet_quats": self.tetras.quats if d["nt"] else np.zeros((0, 4)),
+            "dist_dirs": self.distances.dirs if d["nd"] else np.zeros((0, 3)),
+            "dist_scale": self.distances.scale if d["nd"] else np.zeros(0),
+            "strain_live": np.ones(d["nch"]), "strain_target": np.ones(d["nch"]),
+            "pressures": np.asarray(self.channels.pressures) if d["nch"] else np.zeros(0),
+            "warm": np.zeros((d["nw"], 3)), "warm_valid": np.zeros(d["nw"], np.int32),
+            "time": np.float64(st.time),
+        }
+        return one
+
+    # ---------------------------------------------------------------- state
+    def set_state_arrays(self, arrays: dict, env0: int = 0, n: int | None = None) -> None:
+        """Write state fields (reference shapes, optionally with a leading
+        env axis) into envs [env0, env0+n). Missing fields are untouched."""
+        h = self._ensure()
+        n = self.n_envs - env0 if n is None else n
+        buf = StateBuffers(self._packed.dims, n)
+        names = []
+        for name, shape_fn, dt in STATE_FIELDS:
+            if name not in arrays:
+                continue
+            a = np.asarray(arrays[name], dtype=dt)
+            buf.arrays[name][...] = np.broadcast_to(a, buf.arrays[name].shape)
+            names.append(name)
+        v = buf.view(names)
+        _native.check(_native.lib().ss_set_state(h, env0, n, C.byref(v)))
+
+    def get_state_arrays(self, env0: int = 0, n: int | None = None, names=None) -> dict:
+        h = self._ensure()
+        n = self.n_envs - env0 if n is None else n
+        buf = StateBuffers(self._packed.dims, n)
+        v = buf.view(names)
+        _native.check(_native.lib().ss_get_state(h, env0, n, C.byref(v)))
+        return {k: a for k, a in buf.arrays.items() if names is None or k in names}
+
+    def get_stats(self, env0: int = 0, n: int | None = None) -> list[SsEnvStats]:
+        h = self._ensure()
+        n = self.n_envs - env0 if n is None else n
+        arr = (SsEnvStats * n)()
+        _native.check(_native.lib().ss_get_stats(h, env0, n, arr))
+        return list(arr)
+
+    def center_of_mass(self, env0: int = 0, n: int | None = None) -> np.ndarray:
+        h = self._ensure()
+        n = self.n_envs - env0 if n is None else n
+        out = np.zeros((n, 3))
+        _native.check(_native.lib().ss_get_com(h, env0, n, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    # ----------------------------------------------------------------- step
+    def step(self, commands=None, latency: bool = True, n_frames: int = 1) -> None:
+        """Advance all envs n_frames frames (asynchronous on the device).
+        commands: [n_envs, links] or [n_frames, n_envs, links] psi, or None."""
+        h = self._ensure()
+        ptr = None
+        if commands is not None:
+            cmd = np.ascontiguousarray(np.asarray(commands, np.float64))
+            need = n_frames * self.n_envs * self.n_links
+            if cmd.size == self.n_links and self.n_envs > 1:
+                cmd = np.ascontiguousarray(np.broadcast_to(cmd, (n_frames, self.n_envs, self.n_links)))
+            if cmd.size != need:
+                raise ValueError(f"commands must hold {need} values, got {cmd.size}")
+            self._cmd_keep = cmd
+            ptr = cmd.ctypes.data_as(C.POINTER(C.c_double))
+        _native.check(_native.lib().ss_step(h, ptr, 1 if latency else 0, int(n_frames)))
+        self.frames += n_frames
+
+    def step_device(self, d_commands_ptr: int, latency: bool = True, n_frames: int = 1) -> None:
+        h = self._ensure()
+        _native.check(_native.lib().ss_step_device(h, C.c_void_p(d_commands_ptr),
+                                                   1 if latency else 0, int(n_frames)))
+        self.frames += n_frames
+
+    def synchronize(self) -> None:
+        _native.check(_native.lib().ss_synchronize(self._ensure()))
+
+    def profile_frames(self, commands=None, latency: bool = True, n_frames: int = 1) -> dict:
+        """Run frames un-graphed with CUDA events around every launch;
+        returns {kernel: (total_ms, launches)}."""
+        h = self._ensure()
+        L = _native.lib()
+        names = (C.c_char_p * 32)()
+        nk = L.ss_kernel_names(names, 32)
+        ms = (C.c_double * nk)()
+        cnt = (C.c_int * nk)()
+        ptr = None
+        if commands is not None:
+            cmd = np.ascontiguousarray(np.asarray(commands, np.float64))
+            if cmd.size != n_frames * self.n_envs * self.n_links:
+                raise ValueError("commands must be [n_frames, n_envs, links]")
+            ptr = cmd.ctypes.data_as(C.POINTER(C.c_double))
+        _native.check(L.ss_profile_frames(h, ptr, 1 if latency else 0, int(n_frames), ms, cnt))
+        return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(nk)}
+
+    @property
+    def stream(self) -> int:
+        return int(_native.lib().ss_stream(self._ensure()) or 0)
+
+    @property
+    def launches_per_frame(self) -> int:
+        return int(_native.lib().ss_launches_per_frame(self._ensure()))
+
+    @property
+    def device_bytes(self) -> int:
+        return int(_native.lib().ss_device_bytes(self._ensure()))
+
+
+class Simulator(BatchedSimulator):
+    """Single-environment drop-in for softsnake.solver.Simulator."""
+
+    def __init__(self, state, config: SolverConfig | None = None, distances=None,
+                 tetras=None, attachments=None, hinges=None, wheels=None, channels=None,
+                 strain=None, contact_particles=None, device: int = 0):
+        super().__init__(1, state, config, distances, tetras, attachments, hinges, wheels,
+                         channels, strain, contact_particles, device)
+        self.kern = None  # the reference's backend slot; kernels live in the .so
+        self.stats = StepStats()
+        self.totals = {"steps": 0, "newton_iterations": 0, "pcr_iterations": 0,
+                       "contact_count": 0, "inverted_tets": 0, "assembly_time": 0.0,
+                       "solve_time": 0.0, "wall_time": 0.0}
+        self._cache = None
+
+    # reference surface ------------------------------------------------
+    def set_channel_targets(self, commands, latency: bool = True) -> None:
+        """Tick the channels without stepping is not separable on the device;
+        the reference only calls this from step()."""
+        raise NotImplementedError("use step(commands, latency)")
+
+    def step(self, commands=None, latency: bool = True) -> StepStats:  # noqa: D401
+        t0 = _time.perf_counter()
+        super().step(None if commands is None else np.asarray(commands, np.float64).reshape(1, -1),
+                     latency, 1)
+        s = self.get_stats(0, 1)[0]
+        self._cache = None
+        self.stats = StepStats(s.newton_iterations, s.pcr_iterations, s.contact_count,
+                               s.inverted_tets, float(s.residual))
+        self.stats.wall_time = _time.perf_counter() - t0
+        self.stats.solve_time = self.stats.wall_time
+        tot = self.totals
+        tot["steps"] += 1
+        for k in ("newton_iterations", "pcr_iterations", "contact_count", "inverted_tets"):
+            tot[k] += getattr(self.stats, k)
+        tot["wall_time"] += self.stats.wall_time
+        tot["solve_time"] += self.stats.solve_time
+        self._refresh_host()
+        return self.stats
+
+    def _refresh_host(self):
+        """Mirror device state into the host containers in place."""
+        a = self.get_state_arrays(0, 1)
+        self._cache = a
+        st = self.state
+        st.particles.positions[...] = a["positions"][0]
+        st.particles.velocities[...] = a["velocities"][0]
+        st.body_pos[...] = a["body_pos"][0]
+        st.body_quat[...] = a["body_quat"][0]
+        st.body_lin_vel[...] = a["body_lin_vel"][0]
+        st.body_ang_vel[...] = a["body_ang_vel"][0]
+        st.time = float(a["time"][0])
+        if self.channels is not None:
+            self.channels.pressures[...] = a["pressures"][0]
+        if self.tetras is not None:
+            self.tetras.quats[...] = a["tet_quats"][0]
+        if self.distances is not None:
+            self.distances.dirs[...] = a["dist_dirs"][0]
+            self.distances.scale[...] = a["dist_scale"][0]
+
+    def push_state(self) -> None:
+        """Upload edits made to the host containers (state, quats, dirs...)."""
+        self._ensure()
+        arr = self._initial_state_arrays()
+        for k in ("lam_dist", "lam_tetra", "lam_attach", "lam_hinge", "strain_live",
+                  "strain_target", "warm", "warm_valid"):
+            arr.pop(k)
+        self.set_state_arrays(arr, 0, 1)
+
+    def _lam(self, name):
+        if self._cache is None:
+            self._cache = self.get_state_arrays(0, 1)
+        return self._cache[name][0]
+
+    lam_dist = property(lambda self: self._lam("lam_dist"))
+    lam_tetra = property(lambda self: self._lam("lam_tetra"))
+    lam_attach = property(lambda self: self._lam("lam_attach"))
+    lam_hinge = property(lambda self: self._lam("lam_hinge"))
