@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
       double w0 = 0.0, w1 = 0.0, w2 = 0.0;
       for (int k = k0; k < k1; ++k) {
         const int code = c.T.inc[k];
-        const int fam = code >> 29, v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+        const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
         double a0, a1, a2;
         if (fam == F_TET) {
           double x6[6];
@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
       double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       for (int k = k0; k < k1; ++k) {
         const int code = c.T.inc[k];
-        const int fam = code >> 29, v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+        const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
         double acc[6];
         if (fam == F_ATTB) {
           double x3[3], rw[3];
