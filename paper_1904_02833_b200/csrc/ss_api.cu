@@ -57,7 +57,7 @@ struct ss_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
   Ctx c{};
-  int gy_red_rows = 1, gy_red_apply = 1;
+  int gy_red = 1;
   void* topo_mem = nullptr;
   void* state_mem = nullptr;
   void* work_mem = nullptr;
@@ -83,14 +83,13 @@ dim3 grid_items(const Dims& D, long n, long cap_blocks) {
   return dim3(D.tiles, (unsigned)gy);
 }
 constexpr long kStreamBlocks = 148 * 8;  // 8 resident 256-thread CTAs per SM
-constexpr long kReduceBlocks = 148 * 4;
+constexpr long kReduceBlocks = 148 * 8;
 
 // kernel names for the profiler (ss_profile_frames)
-const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",     "k_eval_tet",
-                                    "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_pcr_reset",
-                                    "k_apply_rows",  "k_pcr_dir",    "k_pcr_step",  "k_newton_update",
-                                    "k_integrate"};
-constexpr int kNumKernels = 13;
+const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
+                                    "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_apply_rows",
+                                    "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate"};
+constexpr int kNumKernels = 12;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -125,18 +124,15 @@ int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = 
   } while (0)
   const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, kStreamBlocks);
   LAUNCH(k_frame_begin, g_links, c, H->d_cmd, has_cmd, latency);
+  const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
   const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, kStreamBlocks);
   const dim3 g_slots = grid_items(D, D.ns, kStreamBlocks);
   const dim3 g_tet = grid_items(D, D.nt, kStreamBlocks);
   const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, kStreamBlocks);
   const dim3 g_gather = grid_items(D, D.P + D.nb, kStreamBlocks);
-  const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
-  const dim3 g_rhs = grid_items(D, n_el, kStreamBlocks);
-  const dim3 g_apply(D.tiles, H->gy_red_apply);
-  const dim3 g_rows(D.tiles, H->gy_red_rows);
-  const dim3 g_upd = grid_items(D, D.ms + D.ns, kStreamBlocks);
+  const dim3 g_el = grid_items(D, n_el, kStreamBlocks);
+  const dim3 g_red(D.tiles, H->gy_red);
   const dim3 g_int = grid_items(D, D.P + D.nb, kStreamBlocks);
-  const dim3 g_env((D.E + SS_THREADS - 1) / SS_THREADS);
   const double* xs_lam = c.S.lam;
   const double* xc_lam = c.K.lamc;
   const double* xs_z = c.K.z;
@@ -146,29 +142,23 @@ int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = 
   for (int sub = 0; sub < c.p.substeps; ++sub) {
     LAUNCH(k_pre, g_pre, c);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
-    if (D.nt) LAUNCH(k_eval_tet, g_tet, c);
+    if (D.nt) LAUNCH(k_eval_tet, g_tet, c);  // + tet J^T lam
     if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
     LAUNCH(k_gather, g_gather, c, 1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
     for (int it = 0; it < c.p.newton; ++it) {
-      LAUNCH(k_newton_rhs, g_rhs, c);
-      LAUNCH(k_pcr_reset, g_env, c);
+      LAUNCH(k_newton_rhs, g_el, c);  // + tet J^T z0
       if (c.p.pcr > 0) {
         LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
-        LAUNCH(k_apply_rows, g_apply, c, 1);
-        LAUNCH(k_pcr_dir, g_rows, c, 1);
-        for (int k = 0; k < c.p.pcr; ++k) {
-          const bool last = k == c.p.pcr - 1;
-          LAUNCH(k_pcr_step, g_rows, c, 1, last ? 1 : 0);
-          if (!last) {
-            LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
-            LAUNCH(k_apply_rows, g_apply, c, 0);
-            LAUNCH(k_pcr_dir, g_rows, c, 0);
-          }
+        LAUNCH(k_apply_rows, g_red, c, 1);
+        LAUNCH(k_pcr_dir, g_red, c, 1);
+        for (int k = 0; k + 1 < c.p.pcr; ++k) {
+          LAUNCH(k_pcr_step, g_el, c);  // + tet J^T z
+          LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
+          LAUNCH(k_apply_rows, g_red, c, 0);
+          LAUNCH(k_pcr_dir, g_red, c, 0);
         }
-      } else {
-        LAUNCH(k_pcr_step, g_rows, c, 0, 1);
       }
-      LAUNCH(k_newton_update, g_upd, c, it == c.p.newton - 1 ? 1 : 0);
+      LAUNCH(k_newton_final, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0);
       LAUNCH(k_gather, g_gather, c, 1, xs_dl, xc_dl);  // v += M^-1 J^T dlam
     }
     LAUNCH(k_integrate, g_int, c);
@@ -558,13 +548,12 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     return SS_ECUDA;
   }
 
-  // reduction grids
+  // reduction grid (fixed: the partial-sum count per env)
   {
     const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
-    H->gy_red_apply = (int)grid_items(D, n_el, kReduceBlocks).y;
-    H->gy_red_rows = (int)grid_items(D, D.m, kReduceBlocks).y;
+    H->gy_red = (int)grid_items(D, n_el, kReduceBlocks).y;
   }
-  const int gy_max = std::max(H->gy_red_apply, H->gy_red_rows);
+  const int gy_max = H->gy_red;
 
   // state + work
   const size_t Es = D.E;
@@ -593,7 +582,10 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.u = A.take<double>((size_t)D.ndof * Es);
     K.ang_inv = A.take<double>(9 * (size_t)D.nb * Es);
     K.res = A.take<double>((size_t)D.ms * Es);
-    K.tJ = A.take<double>(72 * (size_t)D.nt * Es);
+    K.tR = A.take<double>(9 * (size_t)D.nt * Es);
+    K.tS = A.take<double>(6 * (size_t)D.nt * Es);
+    K.tK = A.take<double>(6 * (size_t)D.nt * Es);
+    K.tC = A.take<double>(12 * (size_t)D.nt * Es);
     K.rw = A.take<double>(3 * (size_t)D.na * Es);
     K.hJ = A.take<double>(60 * (size_t)D.nh * Es);
     K.wJ = A.take<double>(18 * (size_t)D.nw * Es);

@@ -74,8 +74,9 @@ struct State {
 struct Work {
   double *v, *u;            // [ndof]
   double* ang_inv;          // [9][nb]
-  double* res;              // [ms]
-  double* tJ;               // [72][nt]  (row i, column j) at (12 i + j)
+  double* res;              // [ms] (tet rows unused: derived from S)
+  double *tR, *tS, *tK;     // [9][nt] [6][nt] [6][nt] compact tet Jacobian: R, sym(R^T F), K^-1
+  double* tC;               // [12][nt] per-tet J^T x column sums (gather input)
   double* rw;               // [3][na]
   double* hJ;               // [60][nh]
   double* wJ;               // [18][nw]  normal(6), friction0(6), friction1(6)
@@ -454,21 +455,69 @@ __global__ void k_slots(const Ctx c) {
 }
 
 // ------------------------------------------------------------- tetra eval
-// numba_backend.py:137-312. Core shared by the batched kernel and the
-// kernel-ABI mirror; J values and residuals go through the writer.
-template <typename Out>
+// numba_backend.py:137-312. The Jacobian is never stored: an element keeps
+// (R, S = sym(R^T F), K^-1) — 21 doubles, S and K^-1 bitwise symmetric —
+// and tet_col() recomputes any column with the exact expressions of the
+// reference, so every use sees the same bits the eval produced.
+
+// compact tet Jacobian of one element in registers
+struct TetC {
+  double R[9], S[9], K[9];
+};
+
+// rest-inverse direction w_v (numba_backend.py:270-281)
+DI void tet_wv(const double* Ri, int v, double* w) {
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double w0 = -(Ri[j] + Ri[3 + j] + Ri[6 + j]);
+    w[j] = v == 0 ? w0 : (v == 1 ? Ri[j] : (v == 2 ? Ri[3 + j] : Ri[6 + j]));
+  }
+}
+
+// column 3v+a of the 6x12 Jacobian (numba_backend.py:283-311)
+DI void tet_col(const TetC& T, const double* wv, int a, double* o) {
+  const double* R = T.R;
+  const double* S = T.S;
+  const double* Ki = T.K;
+  double G[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) G[3 * i + j] = R[3 * a + i] * wv[j];
+  const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
+  const double w0 = Ki[0] * g0 + Ki[1] * g1 + Ki[2] * g2;
+  const double w1 = Ki[3] * g0 + Ki[4] * g1 + Ki[5] * g2;
+  const double w2 = Ki[6] * g0 + Ki[7] * g1 + Ki[8] * g2;
+  const double ws00 = -w2 * S[3] + w1 * S[6];
+  const double ws01 = -w2 * S[4] + w1 * S[7];
+  const double ws02 = -w2 * S[5] + w1 * S[8];
+  const double ws10 = w2 * S[0] - w0 * S[6];
+  const double ws11 = w2 * S[1] - w0 * S[7];
+  const double ws12 = w2 * S[2] - w0 * S[8];
+  const double ws20 = -w1 * S[0] + w0 * S[3];
+  const double ws21 = -w1 * S[1] + w0 * S[4];
+  const double ws22 = -w1 * S[2] + w0 * S[5];
+  o[0] = G[0] - ws00;
+  o[1] = G[4] - ws11;
+  o[2] = G[8] - ws22;
+  o[3] = 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21);
+  o[4] = 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20);
+  o[5] = 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10);
+}
+
+// polar decomposition + strain + K^-1; returns det(F) <= 0
 DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, int maxiter,
-                     Out& out, int* iters) {
-  double F[9], R[9], S[9], K[9], Ki[9], wv[12];
+                     TetC& T, int* iters) {
+  double F[9];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    double x0 = X[a];
-    double Ds0 = X[3 + a] - x0, Ds1 = X[6 + a] - x0, Ds2 = X[9 + a] - x0;
+    const double x0 = X[a];
+    const double Ds0 = X[3 + a] - x0, Ds1 = X[6 + a] - x0, Ds2 = X[9 + a] - x0;
 #pragma unroll
     for (int j = 0; j < 3; ++j) F[3 * a + j] = Ds0 * Ri[j] + Ds1 * Ri[3 + j] + Ds2 * Ri[6 + j];
   }
-  double detF = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
-                F[2] * (F[3] * F[7] - F[4] * F[6]);
+  const double detF = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+                      F[2] * (F[3] * F[7] - F[4] * F[6]);
   double qw = q[0], qx = q[1], qy = q[2], qz = q[3];
   int it = 0;
   for (; it < maxiter; ++it) {
@@ -477,28 +526,28 @@ DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, i
     double o0 = 0.0, o1 = 0.0, o2 = 0.0, tr = 0.0;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      double rc0 = r[j], rc1 = r[3 + j], rc2 = r[6 + j];
-      double f0 = F[j], f1 = F[3 + j], f2 = F[6 + j];
+      const double rc0 = r[j], rc1 = r[3 + j], rc2 = r[6 + j];
+      const double f0 = F[j], f1 = F[3 + j], f2 = F[6 + j];
       o0 += rc1 * f2 - rc2 * f1;
       o1 += rc2 * f0 - rc0 * f2;
       o2 += rc0 * f1 - rc1 * f0;
       tr += rc0 * f0 + rc1 * f1 + rc2 * f2;
     }
-    double s = 1.0 / (fabs(tr) + 1e-9);
+    const double s = 1.0 / (fabs(tr) + 1e-9);
     o0 *= s;
     o1 *= s;
     o2 *= s;
-    double wn = sqrt(o0 * o0 + o1 * o1 + o2 * o2);
+    const double wn = sqrt(o0 * o0 + o1 * o1 + o2 * o2);
     if (wn < tol) break;
-    double half = 0.5 * wn;
-    double cw = cos(half);
-    double sw = sin(half) / wn;
-    double dw = cw, dx = sw * o0, dy = sw * o1, dz = sw * o2;
-    double nw = dw * qw - dx * qx - dy * qy - dz * qz;
-    double nx = dw * qx + dx * qw + dy * qz - dz * qy;
-    double ny = dw * qy - dx * qz + dy * qw + dz * qx;
-    double nz = dw * qz + dx * qy - dy * qx + dz * qw;
-    double qn = sqrt(nw * nw + nx * nx + ny * ny + nz * nz);
+    const double half = 0.5 * wn;
+    const double cw = cos(half);
+    const double sw = sin(half) / wn;
+    const double dw = cw, dx = sw * o0, dy = sw * o1, dz = sw * o2;
+    const double nw = dw * qw - dx * qx - dy * qy - dz * qz;
+    const double nx = dw * qx + dx * qw + dy * qz - dz * qy;
+    const double ny = dw * qy - dx * qz + dy * qw + dz * qx;
+    const double nz = dw * qz + dx * qy - dy * qx + dz * qw;
+    const double qn = sqrt(nw * nw + nx * nx + ny * ny + nz * nz);
     qw = nw / qn;
     qx = nx / qn;
     qy = ny / qn;
@@ -506,26 +555,23 @@ DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, i
   }
   if (iters) *iters = it;
   q[0] = qw; q[1] = qx; q[2] = qy; q[3] = qz;
+  double* R = T.R;
+  double* S = T.S;
   quat_to_mat(qw, qx, qy, qz, R);
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) S[3 * i + j] = R[i] * F[j] + R[3 + i] * F[3 + j] + R[6 + i] * F[6 + j];
   {
-    double m01 = 0.5 * (S[1] + S[3]);
+    const double m01 = 0.5 * (S[1] + S[3]);
     S[1] = m01; S[3] = m01;
-    double m02 = 0.5 * (S[2] + S[6]);
+    const double m02 = 0.5 * (S[2] + S[6]);
     S[2] = m02; S[6] = m02;
-    double m12 = 0.5 * (S[5] + S[7]);
+    const double m12 = 0.5 * (S[5] + S[7]);
     S[5] = m12; S[7] = m12;
   }
-  out.res(0, S[0] - 1.0);
-  out.res(1, S[4] - 1.0);
-  out.res(2, S[8] - 1.0);
-  out.res(3, S[5]);
-  out.res(4, S[2]);
-  out.res(5, S[1]);
-  double trS = S[0] + S[4] + S[8];
+  const double trS = S[0] + S[4] + S[8];
+  double K[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) K[i] = -S[i];
   K[0] += trS + 1e-14;
@@ -534,7 +580,8 @@ DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, i
   double detK = K[0] * (K[4] * K[8] - K[5] * K[7]) - K[1] * (K[3] * K[8] - K[5] * K[6]) +
                 K[2] * (K[3] * K[7] - K[4] * K[6]);
   if (fabs(detK) < 1e-30) detK = detK >= 0 ? 1e-30 : -1e-30;
-  double id = 1.0 / detK;
+  const double id = 1.0 / detK;
+  double* Ki = T.K;
   Ki[0] = (K[4] * K[8] - K[5] * K[7]) * id;
   Ki[1] = (K[2] * K[7] - K[1] * K[8]) * id;
   Ki[2] = (K[1] * K[5] - K[2] * K[4]) * id;
@@ -544,92 +591,144 @@ DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, i
   Ki[6] = (K[3] * K[7] - K[4] * K[6]) * id;
   Ki[7] = (K[1] * K[6] - K[0] * K[7]) * id;
   Ki[8] = (K[0] * K[4] - K[1] * K[3]) * id;
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    wv[3 + j] = Ri[j];
-    wv[6 + j] = Ri[3 + j];
-    wv[9 + j] = Ri[6 + j];
-    wv[j] = -(wv[3 + j] + wv[6 + j] + wv[9 + j]);
-  }
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      double G[9];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) G[3 * i + j] = R[3 * a + i] * wv[3 * v + j];
-      double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
-      double w0 = Ki[0] * g0 + Ki[1] * g1 + Ki[2] * g2;
-      double w1 = Ki[3] * g0 + Ki[4] * g1 + Ki[5] * g2;
-      double w2 = Ki[6] * g0 + Ki[7] * g1 + Ki[8] * g2;
-      double ws00 = -w2 * S[3] + w1 * S[6];
-      double ws01 = -w2 * S[4] + w1 * S[7];
-      double ws02 = -w2 * S[5] + w1 * S[8];
-      double ws10 = w2 * S[0] - w0 * S[6];
-      double ws11 = w2 * S[1] - w0 * S[7];
-      double ws12 = w2 * S[2] - w0 * S[8];
-      double ws20 = -w1 * S[0] + w0 * S[3];
-      double ws21 = -w1 * S[1] + w0 * S[4];
-      double ws22 = -w1 * S[2] + w0 * S[5];
-      const int col = 3 * v + a;
-      out.val(0, col, G[0] - ws00);
-      out.val(1, col, G[4] - ws11);
-      out.val(2, col, G[8] - ws22);
-      out.val(3, col, 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21));
-      out.val(4, col, 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20));
-      out.val(5, col, 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10));
-    }
   return detF <= 0.0 ? 1 : 0;
 }
 
-struct TetOutBatched {
-  const Ctx* c;
-  int t, env;
-  double diag[6];
-  double im[4];
-  DI void res(int i, double v) {
-    const int E = c->D.E;
-    c->K.res[IX(c->D.ot + i * c->D.nt + t)] = v;
-  }
-  DI void val(int i, int col, double v) {
-    const int E = c->D.E;
-    c->K.tJ[IX((size_t)(12 * i + col) * c->D.nt + t)] = v;
-    diag[i] += v * v * im[col / 3];  // block_rowdiag, numba_backend.py:55-65
-  }
-};
+// strain residual in Voigt order [xx yy zz yz xz xy] (numba_backend.py:241-246)
+DI void tet_res(const TetC& T, double* r) {
+  r[0] = T.S[0] - 1.0;
+  r[1] = T.S[4] - 1.0;
+  r[2] = T.S[8] - 1.0;
+  r[3] = T.S[5];
+  r[4] = T.S[2];
+  r[5] = T.S[1];
+}
 
-// TetraSet.eval + tetra rows of block_rowdiag + eh2 diag (solver.py:410-426)
+// compact storage: R (9), S (6 unique), K^-1 (6 unique); both symmetric
+// bitwise (S symmetrised explicitly; K^-1 cofactors of a symmetric K)
+DI void tet_store(const Ctx& c, int t, int env, const TetC& T) {
+  const int E = c.D.E, nt = c.D.nt;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) c.K.tR[IX(k * nt + t)] = T.R[k];
+  const int sym[6] = {0, 4, 8, 5, 2, 1};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    c.K.tS[IX(k * nt + t)] = T.S[sym[k]];
+    c.K.tK[IX(k * nt + t)] = T.K[sym[k]];
+  }
+}
+DI void tet_load(const Ctx& c, int t, int env, TetC& T) {
+  const int E = c.D.E, nt = c.D.nt;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) T.R[k] = c.K.tR[IX(k * nt + t)];
+  double s[6], q[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    s[k] = c.K.tS[IX(k * nt + t)];
+    q[k] = c.K.tK[IX(k * nt + t)];
+  }
+  // [0 1 2; 3 4 5; 6 7 8] <- (00 11 22 12 02 01)
+  T.S[0] = s[0]; T.S[4] = s[1]; T.S[8] = s[2];
+  T.S[5] = s[3]; T.S[7] = s[3];
+  T.S[2] = s[4]; T.S[6] = s[4];
+  T.S[1] = s[5]; T.S[3] = s[5];
+  T.K[0] = q[0]; T.K[4] = q[1]; T.K[8] = q[2];
+  T.K[5] = q[3]; T.K[7] = q[3];
+  T.K[2] = q[4]; T.K[6] = q[4];
+  T.K[1] = q[5]; T.K[3] = q[5];
+}
+DI void tet_rinv(const Ctx& c, int t, double* Ri) {
+  const int nt = c.D.nt;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Ri[k] = c.T.t_rinv[k * nt + t];
+}
+
+// J^T x for one tet: the 12 column sums acc_j = sum_i J[i][j] x_i in the
+// reference's accumulation order (numba_backend.py:43-52), written to tC
+DI void tet_contrib(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
+                    const double* x6) {
+  const int E = c.D.E, nt = c.D.nt;
+#pragma unroll 1
+  for (int v = 0; v < 4; ++v) {
+    double wv[3];
+    tet_wv(Ri, v, wv);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double col[6];
+      tet_col(T, wv, a, col);
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) acc += col[i] * x6[i];
+      c.K.tC[IX((3 * v + a) * nt + t)] = acc;
+    }
+  }
+}
+
+// J y for one tet: y_i = sum_j J[i][j] vec[idx_j] (numba_backend.py:31-40)
+DI void tet_forward(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
+                    const double* vec, double* y) {
+  const int E = c.D.E, nt = c.D.nt;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) y[i] = 0.0;
+#pragma unroll 1
+  for (int v = 0; v < 4; ++v) {
+    const int node = c.T.t_idx[v * nt + t];
+    double wv[3];
+    tet_wv(Ri, v, wv);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double uj = vec[IX(3 * node + a)];
+      double col[6];
+      tet_col(T, wv, a, col);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) y[i] += col[i] * uj;
+    }
+  }
+}
+
+// TetraSet.eval + its block_rowdiag + eh2 diag (solver.py:410-426), and
+// the tet part of the initial impulse J^T lam (solver.py:428-436).
 __global__ void __launch_bounds__(SS_THREADS) k_eval_tet(const Ctx c) {
   SETUP
   const int nt = c.D.nt;
   FOR_ITEMS(t, nt) {
-    double X[12], Ri[9], q[4];
-    TetOutBatched o;
-    o.c = &c;
-    o.t = t;
-    o.env = env;
+    double X[12], Ri[9], q[4], im[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      int node = c.T.t_idx[v * nt + t];
-      o.im[v] = c.T.inv_mass[node];
+      const int node = c.T.t_idx[v * nt + t];
+      im[v] = c.T.inv_mass[node];
 #pragma unroll
       for (int a = 0; a < 3; ++a) X[3 * v + a] = c.S.pos[IX(3 * node + a)];
     }
-#pragma unroll
-    for (int k = 0; k < 9; ++k) Ri[k] = c.T.t_rinv[k * nt + t];
+    tet_rinv(c, t, Ri);
 #pragma unroll
     for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) o.diag[i] = 0.0;
-    int inv = tet_eval_core(X, Ri, q, 1e-12, 500, o, nullptr);
+    TetC T;
+    const int inv = tet_eval_core(X, Ri, q, 1e-12, 500, T, nullptr);
 #pragma unroll
     for (int k = 0; k < 4; ++k) c.S.quat[IX(k * nt + t)] = q[k];
+    tet_store(c, t, env, T);
+    // block_rowdiag (numba_backend.py:55-65): acc_i = sum_j J_ij^2 minv_j
+    double diag[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int v = 0; v < 4; ++v) {
+      double wv[3];
+      tet_wv(Ri, v, wv);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double col[6];
+        tet_col(T, wv, a, col);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) diag[i] += col[i] * col[i] * im[v];
+      }
+    }
     const double ed = c.T.t_e3[t], es = c.T.t_e3[2 * nt + t];
 #pragma unroll
-    for (int i = 0; i < 6; ++i)
-      c.K.bdiag[IX(c.D.ot + i * nt + t)] = o.diag[i] + (i < 3 ? ed : es);
+    for (int i = 0; i < 6; ++i) c.K.bdiag[IX(c.D.ot + i * nt + t)] = diag[i] + (i < 3 ? ed : es);
+    double lam6[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) lam6[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
+    tet_contrib(c, t, env, T, Ri, lam6);
     if (inv) atomicAdd(&c.K.inv_cnt[env], 1);
   }
 }
@@ -766,11 +865,13 @@ __global__ void k_eval_misc(const Ctx c) {
   }
 }
 
+
 // ------------------------------------------------------------ J^T gather
 // mode 0 (apply_a, solver.py:380-387): w = J^T (act o x), u = M^-1 w.
 // mode 1 (_apply_impulse, solver.py:537-544): v += M^-1 J^T x over the
 // present contacts, friction rows regardless of the active set.
-// xs: static rows [ms][E]; xc: contact rows [3 ns][E].
+// xs: static rows [ms][E]; xc: contact rows [3 ns][E]; tets read their
+// column sums from tC (written by the producing element kernel).
 __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
                                                        const double* __restrict__ xs,
                                                        const double* __restrict__ xc) {
@@ -785,17 +886,10 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
         const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
         double a0, a1, a2;
         if (fam == F_TET) {
-          double x6[6];
-#pragma unroll
-          for (int i = 0; i < 6; ++i) x6[i] = xs[IX(c.D.ot + i * nt + e)];
-          a0 = 0.0; a1 = 0.0; a2 = 0.0;
-#pragma unroll
-          for (int i = 0; i < 6; ++i) {
-            const size_t base = (size_t)(12 * i + 3 * v) * nt + e;
-            a0 += c.K.tJ[(base)*E + env] * x6[i];
-            a1 += c.K.tJ[(base + nt) * E + env] * x6[i];
-            a2 += c.K.tJ[(base + 2 * (size_t)nt) * E + env] * x6[i];
-          }
+          const size_t base = (size_t)(3 * v) * nt + e;
+          a0 = c.K.tC[base * E + env];
+          a1 = c.K.tC[(base + nt) * E + env];
+          a2 = c.K.tC[(base + 2 * (size_t)nt) * E + env];
         } else if (fam == F_DIST) {
           const int nd = c.D.nd;
           const double xr = xs[IX(c.D.od + e)];
@@ -805,7 +899,8 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
           a1 = 0.0 + d1 * xr;
           a2 = 0.0 + d2 * xr;
         } else if (fam == F_ATTP) {
-          double x3[3], rw[3] = {0.0, 0.0, 0.0};
+          double x3[3];
+          const double rw[3] = {0.0, 0.0, 0.0};
 #pragma unroll
           for (int i = 0; i < 3; ++i) x3[i] = xs[IX(c.D.oa + i * na + e)];
           double acc[3];
@@ -941,23 +1036,6 @@ DI double row_dist(const Ctx& c, int d, const double* vec, int env) {
   acc += -u2 * vec[IX(3 * j + 2)];
   return acc;
 }
-DI void rows_tet(const Ctx& c, int t, const double* vec, int env, double* y) {
-  const int E = c.D.E, nt = c.D.nt;
-  double uu[12];
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int node = c.T.t_idx[v * nt + t];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) uu[3 * v + a] = vec[IX(3 * node + a)];
-  }
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < 12; ++j) acc += c.K.tJ[IX((size_t)(12 * i + j) * nt + t)] * uu[j];
-    y[i] = acc;
-  }
-}
 DI void rows_att(const Ctx& c, int a, const double* vec, int env, double* y) {
   const int E = c.D.E, na = c.D.na;
   const int pi = c.T.a_p[a], o = c.D.bd0 + 6 * c.T.a_b[a];
@@ -1026,9 +1104,56 @@ DI void rows_slot(const Ctx& c, int s, const double* vec, int env, double* y) {
   }
 }
 
+// isotropic E_tet row products (ereg_apply, numba_backend.py:85-94; the
+// zero entries of the Voigt pattern contribute exact zeros)
+DI void ereg6(double ed, double eo, double es, const double* x, double* o) {
+  o[0] = 0.0 + ed * x[0]; o[0] += eo * x[1]; o[0] += eo * x[2];
+  o[1] = 0.0 + eo * x[0]; o[1] += ed * x[1]; o[1] += eo * x[2];
+  o[2] = 0.0 + eo * x[0]; o[2] += eo * x[1]; o[2] += ed * x[2];
+  o[3] = 0.0 + es * x[3];
+  o[4] = 0.0 + es * x[4];
+  o[5] = 0.0 + es * x[5];
+}
+
+// Rows owned by element item `it` (dist 1, tet 6, attach 3, hinge 5, slot 3
+// when present, else 0) for this env.
+DI int item_rows(const Ctx& c, int it, int env, int* rows) {
+  const int E = c.D.E;
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  if (it < nd) {
+    rows[0] = c.D.od + it;
+    return 1;
+  }
+  it -= nd;
+  if (it < nt) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) rows[i] = c.D.ot + i * nt + it;
+    return 6;
+  }
+  it -= nt;
+  if (it < na) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) rows[i] = c.D.oa + i * na + it;
+    return 3;
+  }
+  it -= na;
+  if (it < nh) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) rows[i] = c.D.oh + i * nh + it;
+    return 5;
+  }
+  it -= nh;
+  if (!c.K.present[IX(it)]) return 0;
+  rows[0] = c.D.on + it;
+  rows[1] = c.D.of + it;
+  rows[2] = c.D.of + ns + it;
+  return 3;
+}
+
 // Newton head: jv = J v, velocity-level rhs, FB rows, friction active set,
-// Jacobi diagonal; PCR setup r = rhs, z = r/d, x = 0 (solver.py:439-478,
-// 36-48, 62-69; contact.py:151-155).
+// Jacobi diagonal; PCR setup r = rhs, z = r/d, x = 0, and the tet column
+// sums of J^T z for the first apply (solver.py:439-478, 36-48, 62-70;
+// contact.py:151-155). Also resets the per-env PCR scalars.
 __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
   SETUP
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
@@ -1045,6 +1170,10 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
     c.K.x[IX(row)] = 0.0;                                   \
   }
   FOR_ITEMS(it, nd + nt + na + nh + ns) {
+    if (it == 0) {
+      c.K.broken[env] = 0;
+      c.K.beta[env] = 0.0;
+    }
     if (it < nd) {
       const int row = c.D.od + it;
       const double jv = row_dist(c, it, v, env);
@@ -1053,25 +1182,28 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
              npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
     } else if (it < nd + nt) {
       const int t = it - nd;
-      double jv[6], lm[6];
-      rows_tet(c, t, v, env, jv);
+      TetC T;
+      double Ri[9], jv[6], lm[6], el[6], rs[6], z6[6];
+      tet_load(c, t, env, T);
+      tet_rinv(c, t, Ri);
+      tet_forward(c, t, env, T, Ri, v, jv);
+      tet_res(T, rs);
 #pragma unroll
       for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
-      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
-      // ereg_apply(eh2, lam_tetra) (numba_backend.py:85-94), isotropic pattern
-      double el[6];
-      el[0] = 0.0 + ed * lm[0]; el[0] += eo * lm[1]; el[0] += eo * lm[2];
-      el[1] = 0.0 + eo * lm[0]; el[1] += ed * lm[1]; el[1] += eo * lm[2];
-      el[2] = 0.0 + eo * lm[0]; el[2] += eo * lm[1]; el[2] += ed * lm[2];
-      el[3] = 0.0 + es * lm[3];
-      el[4] = 0.0 + es * lm[4];
-      el[5] = 0.0 + es * lm[5];
+      ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], lm, el);
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         const int row = c.D.ot + i * nt + t;
-        SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + el[i]),
-               npmax(c.K.bdiag[IX(row)] + 0.0, 1e-30));
+        const double dg = npmax(c.K.bdiag[IX(row)] + 0.0, 1e-30);
+        const double d = dg > 1e-300 ? dg : 1.0;
+        const double r = -(g * rs[i] / h + jv[i] + el[i]);
+        z6[i] = r / d;
+        c.K.r[IX(row)] = r;
+        c.K.d[IX(row)] = d;
+        c.K.z[IX(row)] = z6[i];
+        c.K.x[IX(row)] = 0.0;
       }
+      tet_contrib(c, t, env, T, Ri, z6);
     } else if (it < nd + nt + na) {
       const int a = it - nd - nt;
       double jv[3];
@@ -1096,15 +1228,11 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
       }
     } else {
       const int s = it - nd - nt - na - nh;
-      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
       if (!c.K.present[IX(s)]) {
-        SETROW(rn, 0.0, 1.0);
-        SETROW(rf0, 0.0, 1.0);
-        SETROW(rf1, 0.0, 1.0);
         c.K.actf[IX(s)] = 0.0;
-        c.K.dynn[IX(s)] = 0.0;
         continue;
       }
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
       double jv[3];
       rows_slot(c, s, v, env, jv);
       const double ln = c.K.lamc[IX(s)];
@@ -1134,7 +1262,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
 
 // az = A z rows (apply_a second half, solver.py:388-399) + rho partial z.az.
 // setup != 0: rho = z.az (pcr_solve setup, solver.py:70-73); else
-// beta = rho_new / rho (solver.py:87-89).
+// beta = rho_new / rho (solver.py:87-89). Absent contact slots are skipped.
 __global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setup) {
   SETUP
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
@@ -1150,18 +1278,14 @@ __global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setu
       part += zr * az;
     } else if (it < nd + nt) {
       const int t = it - nd;
-      double y[6], zz[6];
-      rows_tet(c, t, u, env, y);
+      TetC T;
+      double Ri[9], y[6], zz[6], ez[6];
+      tet_load(c, t, env, T);
+      tet_rinv(c, t, Ri);
+      tet_forward(c, t, env, T, Ri, u, y);
 #pragma unroll
       for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
-      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
-      double ez[6];
-      ez[0] = 0.0 + ed * zz[0]; ez[0] += eo * zz[1]; ez[0] += eo * zz[2];
-      ez[1] = 0.0 + eo * zz[0]; ez[1] += ed * zz[1]; ez[1] += eo * zz[2];
-      ez[2] = 0.0 + eo * zz[0]; ez[2] += eo * zz[1]; ez[2] += ed * zz[2];
-      ez[3] = 0.0 + es * zz[3];
-      ez[4] = 0.0 + es * zz[4];
-      ez[5] = 0.0 + es * zz[5];
+      ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], zz, ez);
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         const double az = y[i] + ez[i];
@@ -1196,18 +1320,16 @@ __global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setu
       }
     } else {
       const int s = it - nd - nt - na - nh;
+      if (!c.K.present[IX(s)]) continue;
       const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
       const double zn = z[IX(rn)], z0 = z[IX(rf0)], z1 = z[IX(rf1)];
-      double an = zn, a0 = z0, a1 = z1;
-      const bool pres = c.K.present[IX(s)] != 0;
-      if (pres) {
-        double y[3];
-        rows_slot(c, s, u, env, y);
-        an = y[0] + c.K.dynn[IX(s)] * zn;
-        if (c.K.actf[IX(s)] != 0.0) {
-          a0 = y[1] + c.p.fdyn * z0;
-          a1 = y[2] + c.p.fdyn * z1;
-        }
+      double y[3];
+      rows_slot(c, s, u, env, y);
+      const double an = y[0] + c.K.dynn[IX(s)] * zn;
+      double a0 = z0, a1 = z1;
+      if (c.K.actf[IX(s)] != 0.0) {
+        a0 = y[1] + c.p.fdyn * z0;
+        a1 = y[2] + c.p.fdyn * z1;
       }
       c.K.az[IX(rn)] = an;
       c.K.az[IX(rf0)] = a0;
@@ -1235,21 +1357,29 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
   SETUP
   const bool brk = c.K.broken[env] != 0;
   const double beta = c.K.beta[env];
+  const int n_el = c.D.nd + c.D.nt + c.D.na + c.D.nh + c.D.ns;
   double part = 0.0;
-  FOR_ITEMS(row, c.D.m) {
-    double ap;
-    if (setup) {
-      c.K.p[IX(row)] = c.K.z[IX(row)];
-      ap = c.K.az[IX(row)];
-      c.K.ap[IX(row)] = ap;
-    } else if (!brk) {
-      c.K.p[IX(row)] = c.K.z[IX(row)] + beta * c.K.p[IX(row)];
-      ap = c.K.az[IX(row)] + beta * c.K.ap[IX(row)];
-      c.K.ap[IX(row)] = ap;
-    } else {
-      ap = c.K.ap[IX(row)];
+  FOR_ITEMS(it, n_el) {
+    int rows[6];
+    const int nr = item_rows(c, it, env, rows);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q >= nr) break;
+      const size_t o = IX(rows[q]);
+      double ap;
+      if (setup) {
+        c.K.p[o] = c.K.z[o];
+        ap = c.K.az[o];
+        c.K.ap[o] = ap;
+      } else if (!brk) {
+        c.K.p[o] = c.K.z[o] + beta * c.K.p[o];
+        ap = c.K.az[o] + beta * c.K.ap[o];
+        c.K.ap[o] = ap;
+      } else {
+        ap = c.K.ap[o];
+      }
+      part += ap * (ap / c.K.d[o]);
     }
-    part += ap * (ap / c.K.d[IX(row)]);
   }
   double den;
   if (reduce_env(c, part, &den)) {
@@ -1260,62 +1390,99 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
   }
 }
 
-// x += alpha p, r -= alpha ap, z = r/d (solver.py:81-84); with want_rz the
-// preconditioned residual sqrt(max(r.z, 0)) of the solve (solver.py:85).
-__global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c, int update, int want_rz) {
+// x += alpha p, r -= alpha ap, z = r/d (solver.py:81-84), then the tet
+// column sums of J^T z for the next apply.
+__global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
   SETUP
-  const bool brk = c.K.broken[env] != 0;
+  if (c.K.broken[env]) return;  // the reference skips the whole iteration
   const double alpha = c.K.alpha[env];
-  double part = 0.0;
-  FOR_ITEMS(row, c.D.m) {
-    double r = c.K.r[IX(row)], z;
-    if (update && !brk) {
-      c.K.x[IX(row)] += alpha * c.K.p[IX(row)];
-      r -= alpha * c.K.ap[IX(row)];
-      z = r / c.K.d[IX(row)];
-      c.K.r[IX(row)] = r;
-      c.K.z[IX(row)] = z;
-    } else {
-      z = c.K.z[IX(row)];
+  const int nd = c.D.nd, nt = c.D.nt;
+  const int n_el = nd + nt + c.D.na + c.D.nh + c.D.ns;
+  FOR_ITEMS(it, n_el) {
+    int rows[6];
+    const int nr = item_rows(c, it, env, rows);
+    double z6[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q >= nr) break;
+      const size_t o = IX(rows[q]);
+      c.K.x[o] += alpha * c.K.p[o];
+      const double r = c.K.r[o] - alpha * c.K.ap[o];
+      const double z = r / c.K.d[o];
+      c.K.r[o] = r;
+      c.K.z[o] = z;
+      z6[q] = z;
     }
-    part += r * z;
-  }
-  if (!want_rz) return;
-  double rz;
-  if (reduce_env(c, part, &rz)) c.K.resid[env] = sqrt(0.0 > rz ? 0.0 : rz);
-}
-
-// pcr_solve's per-solve reset
-__global__ void k_pcr_reset(const Ctx c) {
-  const int env = blockIdx.x * blockDim.x + threadIdx.x;
-  if (env < c.D.E) {
-    c.K.broken[env] = 0;
-    c.K.beta[env] = 0.0;
+    if (it >= nd && it < nd + nt) {
+      const int t = it - nd;
+      TetC T;
+      double Ri[9];
+      tet_load(c, t, env, T);
+      tet_rinv(c, t, Ri);
+      tet_contrib(c, t, env, T, Ri, z6);
+    }
   }
 }
 
-// Multiplier update, FrictionState.project, and dlambda = lam_after -
-// lam_before into az (solver.py:487-509, contact.py:157-165); on the last
-// Newton pass also store_warm (contact.py:167-180).
-__global__ void k_newton_update(const Ctx c, int last) {
+// Last PCR step fused with the Newton multiplier update (solver.py:81-85,
+// 487-509; contact.py:157-165): dl = x + alpha p, lam += dl, contact
+// projection, dlam = lam_after - lam_before into az (rows) and the tet
+// column sums of J^T dlam; residual sqrt(max(r.z, 0)) of the solve; on the
+// last Newton pass store_warm (contact.py:167-180). do_step = 0 when
+// pcr_iters == 0.
+__global__ void __launch_bounds__(SS_THREADS) k_newton_final(const Ctx c, int do_step, int last) {
   SETUP
-  const int ms = c.D.ms, ns = c.D.ns, nw = c.D.nw;
-  FOR_ITEMS(it, ms + ns) {
-    if (it < ms) {
-      const double l0 = c.S.lam[IX(it)];
-      const double l1 = l0 + c.K.x[IX(it)];
-      c.S.lam[IX(it)] = l1;
-      c.K.az[IX(it)] = l1 - l0;
+  const bool step = do_step && !c.K.broken[env];
+  const double alpha = c.K.alpha[env];
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns, nw = c.D.nw;
+  const int n_el = nd + nt + na + nh + ns;
+  double part = 0.0;
+  FOR_ITEMS(it, n_el) {
+    int rows[6];
+    const int nr = item_rows(c, it, env, rows);
+    double dl[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q >= nr) break;
+      const size_t o = IX(rows[q]);
+      double x = c.K.x[o], r = c.K.r[o], z = c.K.z[o];
+      if (step) {
+        x += alpha * c.K.p[o];
+        r -= alpha * c.K.ap[o];
+        z = r / c.K.d[o];
+      }
+      part += r * z;
+      dl[q] = x;
+    }
+    if (it < nd + nt + na + nh) {
+      double d6[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        if (q >= nr) break;
+        const size_t o = IX(rows[q]);
+        const double l0 = c.S.lam[o];
+        const double l1 = l0 + dl[q];
+        c.S.lam[o] = l1;
+        d6[q] = l1 - l0;
+        c.K.az[o] = d6[q];
+      }
+      if (it >= nd && it < nd + nt) {
+        const int t = it - nd;
+        TetC T;
+        double Ri[9];
+        tet_load(c, t, env, T);
+        tet_rinv(c, t, Ri);
+        tet_contrib(c, t, env, T, Ri, d6);
+      }
     } else {
-      const int s = it - ms;
-      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
-      const bool pres = c.K.present[IX(s)] != 0;
+      const int s = it - nd - nt - na - nh;
       double n1 = 0.0, a1 = 0.0, b1 = 0.0;
-      if (pres) {
+      if (nr) {
+        const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
         const double n0 = c.K.lamc[IX(s)], a0 = c.K.lamc[IX(ns + s)], b0 = c.K.lamc[IX(2 * ns + s)];
-        n1 = n0 + c.K.x[IX(rn)];
-        a1 = a0 + c.K.x[IX(rf0)];
-        b1 = b0 + c.K.x[IX(rf1)];
+        n1 = n0 + dl[0];
+        a1 = a0 + dl[1];
+        b1 = b0 + dl[2];
         n1 = npmax(n1, 0.0);
         const double rad = c.p.mu * npmax(n1, 0.0);
         const double nrm = sqrt(a1 * a1 + b1 * b1);
@@ -1330,19 +1497,17 @@ __global__ void k_newton_update(const Ctx c, int last) {
         c.K.az[IX(rn)] = n1 - n0;
         c.K.az[IX(rf0)] = a1 - a0;
         c.K.az[IX(rf1)] = b1 - b0;
-      } else {
-        c.K.az[IX(rn)] = 0.0;
-        c.K.az[IX(rf0)] = 0.0;
-        c.K.az[IX(rf1)] = 0.0;
       }
       if (last && s < nw) {
-        c.S.warm_valid[IX(s)] = pres ? 1 : 0;
+        c.S.warm_valid[IX(s)] = nr ? 1 : 0;
         c.S.warm[IX(s)] = n1;
         c.S.warm[IX(nw + s)] = a1;
         c.S.warm[IX(2 * nw + s)] = b1;
       }
     }
   }
+  double rz;
+  if (reduce_env(c, part, &rz)) c.K.resid[env] = sqrt(0.0 > rz ? 0.0 : rz);
 }
 
 // set_velocities + integrate_pose + quat_step (state.py:155-160, 171-192)

@@ -108,14 +108,8 @@ __global__ void kk_eval_distance(const double* pos, const int* pairs, const doub
   res[e] = ln - rest[e] * scale[e];
 }
 
-struct TetOutAoS {
-  double* res_base;
-  double* vals_base;
-  DI void res(int i, double v) { res_base[i] = v; }
-  DI void val(int i, int col, double v) { vals_base[12 * i + col] = v; }
-};
-
-// numba_backend.py:137-312 — one thread per element
+// numba_backend.py:137-312 — one thread per element; J written from the
+// same tet_col() the batched solver recomputes with
 __global__ void kk_eval_tetra(const double* pos, const int* tets, const double* rest_inv,
                               double* quats, double tol, int maxiter, double* out_res,
                               double* out_vals, int n, int* n_inv) {
@@ -128,10 +122,20 @@ __global__ void kk_eval_tetra(const double* pos, const int* tets, const double* 
   }
   for (int k = 0; k < 9; ++k) Ri[k] = rest_inv[9 * (long)e + k];
   for (int k = 0; k < 4; ++k) q[k] = quats[4 * (long)e + k];
-  TetOutAoS o;
-  o.res_base = out_res + 6 * (long)e;
-  o.vals_base = out_vals + 72 * (long)e;
-  const int inv = tet_eval_core(X, Ri, q, tol, maxiter, o, nullptr);
+  TetC T;
+  const int inv = tet_eval_core(X, Ri, q, tol, maxiter, T, nullptr);
   for (int k = 0; k < 4; ++k) quats[4 * (long)e + k] = q[k];
+  double r6[6];
+  tet_res(T, r6);
+  for (int i = 0; i < 6; ++i) out_res[6 * (long)e + i] = r6[i];
+  for (int v = 0; v < 4; ++v) {
+    double wv[3];
+    tet_wv(Ri, v, wv);
+    for (int a = 0; a < 3; ++a) {
+      double col[6];
+      tet_col(T, wv, a, col);
+      for (int i = 0; i < 6; ++i) out_vals[72 * (long)e + 12 * i + 3 * v + a] = col[i];
+    }
+  }
   if (inv) atomicAdd(n_inv, 1);
 }
