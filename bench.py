@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--envs", type=int, default=1024, help="environments per GPU")
+    ap.add_argument("--envs", type=int, default=1024, help="environments per GPU (weak scaling)")
+    ap.add_argument("--total-envs", type=int, default=0,
+                    help="fixed total environments split across GPUs (strong scaling)")
     ap.add_argument("--profile-frames", type=int, default=2)
     ap.add_argument("--cpu-frames", type=int, default=6, help="oracle frames per host core")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -52,10 +54,9 @@ def env_commands(n_envs: int, frames: int, first_frame: int, env0: int = 0):
     from the conftest seed."""
     import paper_1904_02833_b200 as M
     sc = M.SceneConfig()
-    rng = np.random.default_rng(20260817)
-    bias_all = rng.uniform(-0.5, 0.5, env0 + n_envs)
-    t0_all = rng.uniform(0.0, 0.5, env0 + n_envs)
-    bias, t0 = bias_all[env0:], t0_all[env0:]
+    # one (bias, t0) row per env: env e's draw does not depend on the sharding
+    draws = np.random.default_rng(20260817).uniform(size=(env0 + n_envs, 2))[env0:]
+    bias, t0 = draws[:, 0] - 0.5, 0.5 * draws[:, 1]
     w = 2.0 * np.pi * sc.frequency
     i = np.arange(4)
     t = t0[None, :] + (first_frame + np.arange(frames))[:, None] * sc.dt
@@ -197,12 +198,18 @@ def main():
         dist.barrier()
     import paper_1904_02833_b200 as M
     from paper_1904_02833_b200 import roofline
+    from paper_1904_02833_b200.distributed import env_slice, gather_env_stats, max_over_ranks
 
-    n = args.envs
+    if args.total_envs:
+        env0, n = env_slice(args.total_envs, world, rank)
+        total, scaling = args.total_envs, "strong"
+    else:
+        env0, n = rank * args.envs, args.envs
+        total, scaling = world * args.envs, "weak"
     model = M.build_snake(M.SceneConfig(), n_envs=n, device=local)
     sim = model.sim
     K, W = args.steps, args.warmup
-    cmds = env_commands(n, W + K, 0, env0=rank * n)
+    cmds = env_commands(n, W + K, 0, env0=env0)
     d_cmds = torch.from_numpy(cmds).to(f"cuda:{local}")
     stream = torch.cuda.ExternalStream(sim.stream, device=f"cuda:{local}")
     frame_elems = n * 4
@@ -223,17 +230,12 @@ def main():
             sim.step_device(d_cmds.data_ptr() + 8 * (W + f) * frame_elems, True, 1)
         e1.record(stream)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
     stats = sim.get_stats(0, min(n, 8))
     finite = all(s.finite for s in sim.get_stats())
 
     # ---- e2e through the public API: host commands (pinned) in, COM out
-    host_cmd = torch.from_numpy(env_commands(n, K, W + K, env0=rank * n)).pin_memory()
+    host_cmd = torch.from_numpy(env_commands(n, K, W + K, env0=env0)).pin_memory()
     com_bytes = n * 3 * 8
     torch.cuda.synchronize()
     if dist:
@@ -242,18 +244,12 @@ def main():
     for f in range(K):
         sim.step(host_cmd[f].numpy(), latency=True)
         com = sim.center_of_mass()          # D2H of the step's result (synchronises)
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-        # optional rollout-stats gather over NVLink
-        com_t = torch.from_numpy(com).to(f"cuda:{local}")
-        gathered = [torch.empty_like(com_t) for _ in range(world)]
-        dist.all_gather(gathered, com_t)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, device=f"cuda:{local}")
+    # optional rollout-stats gather over NVLink, off the timed path
+    all_com = gather_env_stats(com, total, device=f"cuda:{local}")
 
     # ---- live per-kernel timing (CUDA events around each launch)
-    prof_cmds = env_commands(n, args.profile_frames, W + 2 * K, env0=rank * n)
+    prof_cmds = env_commands(n, args.profile_frames, W + 2 * K, env0=env0)
     prof = sim.profile_frames(prof_cmds, True, args.profile_frames)
     step_ms_prof = sum(v[0] for v in prof.values()) / args.profile_frames
     top = max(prof, key=lambda k: prof[k][0])
@@ -261,7 +257,8 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    per_launch = roofline.bytes_per_launch_per_env(top, d) * n
+    nc_mean = float(np.mean([st.contact_count for st in sim.get_stats()])) / sim.config.substeps
+    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean) * n
     avg_ms = prof[top][0] / prof[top][1]
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
     traffic = None
@@ -274,14 +271,14 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    value = world * n * K / (ms * 1e-3)
-    e2e = world * n * K / e2e_s
+    value = total * K / (ms * 1e-3)
+    e2e = total * K / e2e_s
     launches = sim.launches_per_frame
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "envs_per_gpu": n, "global_envs": world * n,
+        "config": {"workload": WORKLOAD, "envs_per_gpu": n, "global_envs": total,
                    "frame_dt_s": 1 / 60, "substeps": 2, "newton": 4, "pcr": 20,
                    "gait": "default, per-env turn bias U(-0.5,0.5), t0 U(0,0.5s), seed 20260817",
                    "l2": "no flush: per-step working set "
@@ -292,6 +289,7 @@ def main():
                      "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
+                     "mean_contacts_per_substep": nc_mean,
                      "share_of_step": prof[top][0] / sum(v[0] for v in prof.values()),
                      "traffic": traffic},
         "kernels_ms_per_frame": {k: round(v[0] / args.profile_frames, 4) for k, v in prof.items()},
@@ -299,7 +297,7 @@ def main():
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": n * 4 * 8,
                 "d2h_bytes_per_step": com_bytes},
         "gpu_launches": launches * K,
-        "finite": finite,
+        "finite": finite and bool(np.all(np.isfinite(all_com))),
         "stats_env0": {"contacts": stats[0].contact_count, "inverted": stats[0].inverted_tets,
                        "residual": stats[0].residual},
         "clocks": clk.summary(),

@@ -105,6 +105,11 @@ typedef struct ss_params {
   double constraint_damping;
   double strain_youngs;             /* StrainLaw.youngs_modulus_pa  pneumatics.py:32-43 */
   double k_inflate, k_deflate, deflate_cap, supply;   /* pneumatics.py:88-96 */
+  /* 1: apply each tet Jacobian through its materialised 6x12 columns, so
+   * every J^T x / J u sum is bitwise numba's; 0 (default): structured
+   * chain-rule application of the same operator, ~5x fewer FP64 ops,
+   * rounding-level (1e-16) differences. */
+  int32_t exact_jacobian;
 } ss_params;
 
 /* Full per-environment state. Host pointers;

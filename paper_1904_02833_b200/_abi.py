@@ -46,6 +46,7 @@ class SsParams(C.Structure):
         ("max_strain_rate", C.c_double), ("constraint_damping", C.c_double),
         ("strain_youngs", C.c_double), ("k_inflate", C.c_double),
         ("k_deflate", C.c_double), ("deflate_cap", C.c_double), ("supply", C.c_double),
+        ("exact_jacobian", C.c_int32),
     ]
 
 
@@ -205,6 +206,7 @@ def pack_params(config, packed: PackedTopology) -> SsParams:
     p.k_deflate = float(getattr(ch, "k_deflate", 0.23))
     p.deflate_cap = float(getattr(ch, "deflate_cap", 0.68))
     p.supply = float(getattr(ch, "supply", 8.0))
+    p.exact_jacobian = 1 if getattr(config, "exact_jacobian", False) else 0
     return p
 
 

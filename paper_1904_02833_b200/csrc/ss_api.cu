@@ -94,19 +94,13 @@ struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
 int kid(const char* name) {
-  for (int i = 0; i < kNumKernels; ++i)
-    if (!strcmp(name, kKernelNames[i])) return i;
+  for (int i = 0; i < kNumKernels; ++i) {
+    const size_t n = strlen(kKernelNames[i]);
+    if (!strncmp(name, kKernelNames[i], n) && (name[n] == 0 || name[n] == '<')) return i;
+  }
   return -1;
 }
 
-// Enqueue one frame (Simulator.step, solver.py:296-314) on the stream.
-// With prof, every launch is bracketed by CUDA events (eager, not graphed).
-int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
-  const Ctx& c = H->c;
-  const Dims& D = c.D;
-  cudaStream_t st = H->stream;
-  const dim3 blk(SS_THREADS);
-  int n = 0;
 #define LAUNCH(kern, grid, ...)                                          \
   do {                                                                   \
     cudaEvent_t e0_ = nullptr, e1_ = nullptr;                            \
@@ -122,9 +116,20 @@ int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = 
     }                                                                    \
     ++n;                                                                 \
   } while (0)
-  const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, kStreamBlocks);
-  LAUNCH(k_frame_begin, g_links, c, H->d_cmd, has_cmd, latency);
+
+// Enqueue one frame (Simulator.step, solver.py:296-314) on the stream.
+// With prof, every launch is bracketed by CUDA events (eager, not graphed).
+// EX: materialised-column tet Jacobian (bitwise numba sums) instead of the
+// structured application (default).
+template <bool EX>
+int enqueue_frame_t(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof) {
+  const Ctx& c = H->c;
+  const Dims& D = c.D;
+  cudaStream_t st = H->stream;
+  const dim3 blk(SS_THREADS);
+  int n = 0;
   const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
+  const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, kStreamBlocks);
   const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, kStreamBlocks);
   const dim3 g_slots = grid_items(D, D.ns, kStreamBlocks);
   const dim3 g_tet = grid_items(D, D.nt, kStreamBlocks);
@@ -139,34 +144,40 @@ int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = 
   const double* xc_z = c.K.z + (size_t)D.ms * D.E;
   const double* xs_dl = c.K.az;
   const double* xc_dl = c.K.az + (size_t)D.ms * D.E;
+  LAUNCH(k_frame_begin, g_links, c, H->d_cmd, has_cmd, latency);
   for (int sub = 0; sub < c.p.substeps; ++sub) {
     LAUNCH(k_pre, g_pre, c);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
-    if (D.nt) LAUNCH(k_eval_tet, g_tet, c);  // + tet J^T lam
+    if (D.nt) LAUNCH(k_eval_tet<EX>, g_tet, c);  // + tet J^T lam
     if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
     LAUNCH(k_gather, g_gather, c, 1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
     for (int it = 0; it < c.p.newton; ++it) {
-      LAUNCH(k_newton_rhs, g_el, c);  // + tet J^T z0
+      LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
       if (c.p.pcr > 0) {
         LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
-        LAUNCH(k_apply_rows, g_red, c, 1);
+        LAUNCH(k_apply_rows<EX>, g_red, c, 1);
         LAUNCH(k_pcr_dir, g_red, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
-          LAUNCH(k_pcr_step, g_el, c);  // + tet J^T z
+          LAUNCH(k_pcr_step<EX>, g_el, c);  // + tet J^T z
           LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
-          LAUNCH(k_apply_rows, g_red, c, 0);
+          LAUNCH(k_apply_rows<EX>, g_red, c, 0);
           LAUNCH(k_pcr_dir, g_red, c, 0);
         }
       }
-      LAUNCH(k_newton_final, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0);
+      LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0);
       LAUNCH(k_gather, g_gather, c, 1, xs_dl, xc_dl);  // v += M^-1 J^T dlam
     }
     LAUNCH(k_integrate, g_int, c);
   }
-#undef LAUNCH
   if (nl) *nl = n;
   CK(cudaGetLastError());
   return SS_OK;
+}
+#undef LAUNCH
+
+int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
+  return H->c.p.exact_j ? enqueue_frame_t<true>(H, has_cmd, latency, nl, prof)
+                        : enqueue_frame_t<false>(H, has_cmd, latency, nl, prof);
 }
 
 int get_graph(ss_handle* H, int has_cmd, int latency, cudaGraphExec_t* out) {
@@ -339,6 +350,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   P.newton = p->newton_iters;
   P.pcr = p->pcr_iters;
   P.substeps = p->substeps;
+  P.exact_j = p->exact_jacobian ? 1 : 0;
   const double g = P.gamma;
 
   // actuated rows exist (solver.py:241-248)
@@ -447,11 +459,19 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     push(item, 5, F_CF, 0, s);
   }
   std::vector<int> inc_ptr((size_t)D.P + D.nb + 1, 0), inc;
+  std::vector<int2> inc_tet((size_t)D.P);
   for (size_t i = 0; i < lists.size(); ++i) {
     std::stable_sort(lists[i].begin(), lists[i].end(),
                      [](const Inc& a, const Inc& b) { return a.key < b.key; });
     inc_ptr[i + 1] = inc_ptr[i] + (int)lists[i].size();
-    for (auto& x : lists[i]) inc.push_back(x.code);
+    int tb = -1, te = -1;
+    for (size_t k = 0; k < lists[i].size(); ++k) {
+      const int rank = (int)(lists[i][k].key >> 40);
+      if (rank == 1 && tb < 0) tb = inc_ptr[i] + (int)k;
+      if (rank == 1) te = inc_ptr[i] + (int)k + 1;
+      inc.push_back(lists[i][k].code);
+    }
+    if (i < (size_t)D.P) inc_tet[i] = make_int2(tb, te);
   }
 
   // ---- allocations
@@ -494,6 +514,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     T.slot_part = A.take<int>(D.nq);
     T.inc_ptr = A.take<int>((size_t)D.P + D.nb + 1);
     T.inc = A.take<int>(inc.size());
+    T.inc_tet = A.take<int2>((size_t)D.P);
   };
   plan_topo(ta);
   ta.cap = ta.off;
@@ -543,6 +564,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   rc |= up(T.slot_part, slot_part.data(), 4 * slot_part.size());
   rc |= up(T.inc_ptr, inc_ptr.data(), 4 * inc_ptr.size());
   rc |= up(T.inc, inc.data(), 4 * inc.size());
+  rc |= up(T.inc_tet, inc_tet.data(), sizeof(int2) * inc_tet.size());
   if (rc) {
     ss_destroy(H);
     return SS_ECUDA;

@@ -38,7 +38,7 @@ struct Dims {
 struct Par {
   double h, gamma, hg[3], ground_h, margin, mu, fdyn, fb_delta, smin, smax, dmax;
   double youngs, ki, kd, cap, supply, half_h;
-  int newton, pcr, substeps;
+  int newton, pcr, substeps, exact_j;
 };
 
 // scene topology, shared by every environment (item-indexed only)
@@ -56,6 +56,7 @@ struct Topo {
   const double *w_rad, *w_axis;                                   // [nw] [3][nw]
   const int* slot_part;                                           // [nq]
   const int *inc_ptr, *inc;                                       // [P+nb+1], codes
+  const int2* inc_tet;                                            // [P] tet run [begin, end)
 };
 
 // persistent per-environment state, [item][E]
@@ -686,8 +687,112 @@ DI void tet_forward(const Ctx& c, int t, int env, const TetC& T, const double* R
   }
 }
 
+// ---- structured application of the same operator (default solver path)
+// The 6x12 block is never materialised: with Z the symmetric matrix of a
+// Voigt vector z (shear entries halved), N = Z S, n = K^-1 ax(N),
+//   (J^T z)_{3v+a} = R_a . (Z w_v - n x w_v),
+// and with L = sum_v u_v w_v^T, G = R^T L, w = K^-1 ax(G),
+//   J u = voigt(sym(G) - sym(skew(w) S)).
+// Algebraically identical to the columns of tet_col (numba_backend.py:283-311);
+// only the association of the sums differs (~1e-16 relative), for ~5x fewer
+// FP64 operations. ax(M) = (M21 - M12, M02 - M20, M10 - M01) as g in the ref.
+DI void tet_contrib_fast(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
+                         const double* z) {
+  const int E = c.D.E, nt = c.D.nt;
+  const double* S = T.S;
+  const double* Ki = T.K;
+  const double* R = T.R;
+  const double Z00 = z[0], Z11 = z[1], Z22 = z[2];
+  const double Z12 = 0.5 * z[3], Z02 = 0.5 * z[4], Z01 = 0.5 * z[5];
+  const double N21 = Z02 * S[1] + Z12 * S[4] + Z22 * S[7];
+  const double N12 = Z01 * S[2] + Z11 * S[5] + Z12 * S[8];
+  const double N02 = Z00 * S[2] + Z01 * S[5] + Z02 * S[8];
+  const double N20 = Z02 * S[0] + Z12 * S[3] + Z22 * S[6];
+  const double N10 = Z01 * S[0] + Z11 * S[3] + Z12 * S[6];
+  const double N01 = Z00 * S[1] + Z01 * S[4] + Z02 * S[7];
+  const double m0 = N21 - N12, m1 = N02 - N20, m2 = N10 - N01;
+  const double n0 = Ki[0] * m0 + Ki[1] * m1 + Ki[2] * m2;
+  const double n1 = Ki[3] * m0 + Ki[4] * m1 + Ki[5] * m2;
+  const double n2 = Ki[6] * m0 + Ki[7] * m1 + Ki[8] * m2;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    double wv[3];
+    tet_wv(Ri, v, wv);
+    const double q0 = (Z00 * wv[0] + Z01 * wv[1] + Z02 * wv[2]) - (n1 * wv[2] - n2 * wv[1]);
+    const double q1 = (Z01 * wv[0] + Z11 * wv[1] + Z12 * wv[2]) - (n2 * wv[0] - n0 * wv[2]);
+    const double q2 = (Z02 * wv[0] + Z12 * wv[1] + Z22 * wv[2]) - (n0 * wv[1] - n1 * wv[0]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      c.K.tC[IX((3 * v + a) * nt + t)] = R[3 * a] * q0 + R[3 * a + 1] * q1 + R[3 * a + 2] * q2;
+  }
+}
+
+DI void tet_forward_fast(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
+                         const double* vec, double* y) {
+  const int E = c.D.E, nt = c.D.nt;
+  const double* R = T.R;
+  const double* S = T.S;
+  const double* Ki = T.K;
+  double u0[3], du[9];
+  {
+    const int n0 = c.T.t_idx[t];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) u0[a] = vec[IX(3 * n0 + a)];
+  }
+#pragma unroll
+  for (int v = 1; v < 4; ++v) {
+    const int node = c.T.t_idx[v * nt + t];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) du[3 * (v - 1) + a] = vec[IX(3 * node + a)] - u0[a];
+  }
+  // L_aj = sum_{v=1..3} (u_v - u_0)_a Ri[v-1][j]   (w_0 = -(w_1 + w_2 + w_3))
+  double L[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) L[3 * a + j] = du[a] * Ri[j] + du[3 + a] * Ri[3 + j] + du[6 + a] * Ri[6 + j];
+  double G[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) G[3 * i + j] = R[i] * L[j] + R[3 + i] * L[3 + j] + R[6 + i] * L[6 + j];
+  const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
+  const double w0 = Ki[0] * g0 + Ki[1] * g1 + Ki[2] * g2;
+  const double w1 = Ki[3] * g0 + Ki[4] * g1 + Ki[5] * g2;
+  const double w2 = Ki[6] * g0 + Ki[7] * g1 + Ki[8] * g2;
+  const double ws00 = -w2 * S[3] + w1 * S[6];
+  const double ws01 = -w2 * S[4] + w1 * S[7];
+  const double ws02 = -w2 * S[5] + w1 * S[8];
+  const double ws10 = w2 * S[0] - w0 * S[6];
+  const double ws11 = w2 * S[1] - w0 * S[7];
+  const double ws12 = w2 * S[2] - w0 * S[8];
+  const double ws20 = -w1 * S[0] + w0 * S[3];
+  const double ws21 = -w1 * S[1] + w0 * S[4];
+  const double ws22 = -w1 * S[2] + w0 * S[5];
+  y[0] = G[0] - ws00;
+  y[1] = G[4] - ws11;
+  y[2] = G[8] - ws22;
+  y[3] = 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21);
+  y[4] = 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20);
+  y[5] = 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10);
+}
+
+// EXACT selects the materialised-column path (bitwise numba sums)
+template <bool EXACT>
+DI void tet_jt(const Ctx& c, int t, int env, const TetC& T, const double* Ri, const double* x6) {
+  if (EXACT) tet_contrib(c, t, env, T, Ri, x6);
+  else tet_contrib_fast(c, t, env, T, Ri, x6);
+}
+template <bool EXACT>
+DI void tet_j(const Ctx& c, int t, int env, const TetC& T, const double* Ri, const double* vec,
+              double* y) {
+  if (EXACT) tet_forward(c, t, env, T, Ri, vec, y);
+  else tet_forward_fast(c, t, env, T, Ri, vec, y);
+}
+
 // TetraSet.eval + its block_rowdiag + eh2 diag (solver.py:410-426), and
 // the tet part of the initial impulse J^T lam (solver.py:428-436).
+template <bool EXACT>
 __global__ void __launch_bounds__(SS_THREADS) k_eval_tet(const Ctx c) {
   SETUP
   const int nt = c.D.nt;
@@ -728,7 +833,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_eval_tet(const Ctx c) {
     double lam6[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) lam6[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
-    tet_contrib(c, t, env, T, Ri, lam6);
+    tet_jt<EXACT>(c, t, env, T, Ri, lam6);
     if (inv) atomicAdd(&c.K.inv_cnt[env], 1);
   }
 }
@@ -881,7 +986,40 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
     const int k0 = c.T.inc_ptr[it], k1 = c.T.inc_ptr[it + 1];
     if (it < P) {
       double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+      // the list is sorted by family: [dist][tet][attach][contact normal][friction]
+      const int2 tr = c.T.inc_tet[it];
       for (int k = k0; k < k1; ++k) {
+        if (k == tr.x) {
+          // tet run: column sums from tC, loads hoisted 4 incidences at a time
+          const double* __restrict__ tC = c.K.tC;
+          for (; k + 3 < tr.y; k += 4) {
+            double a[12];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int code = c.T.inc[k + j];
+              const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+              const size_t base = (size_t)(3 * v) * nt + e;
+              a[3 * j] = tC[base * E + env];
+              a[3 * j + 1] = tC[(base + nt) * E + env];
+              a[3 * j + 2] = tC[(base + 2 * (size_t)nt) * E + env];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              w0 += a[3 * j];
+              w1 += a[3 * j + 1];
+              w2 += a[3 * j + 2];
+            }
+          }
+          for (; k < tr.y; ++k) {
+            const int code = c.T.inc[k];
+            const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+            const size_t base = (size_t)(3 * v) * nt + e;
+            w0 += tC[base * E + env];
+            w1 += tC[(base + nt) * E + env];
+            w2 += tC[(base + 2 * (size_t)nt) * E + env];
+          }
+          if (k >= k1) break;
+        }
         const int code = c.T.inc[k];
         const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
         double a0, a1, a2;
@@ -1154,6 +1292,7 @@ DI int item_rows(const Ctx& c, int it, int env, int* rows) {
 // Jacobi diagonal; PCR setup r = rhs, z = r/d, x = 0, and the tet column
 // sums of J^T z for the first apply (solver.py:439-478, 36-48, 62-70;
 // contact.py:151-155). Also resets the per-env PCR scalars.
+template <bool EXACT>
 __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
   SETUP
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
@@ -1186,7 +1325,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
       double Ri[9], jv[6], lm[6], el[6], rs[6], z6[6];
       tet_load(c, t, env, T);
       tet_rinv(c, t, Ri);
-      tet_forward(c, t, env, T, Ri, v, jv);
+      tet_j<EXACT>(c, t, env, T, Ri, v, jv);
       tet_res(T, rs);
 #pragma unroll
       for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
@@ -1203,7 +1342,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
         c.K.z[IX(row)] = z6[i];
         c.K.x[IX(row)] = 0.0;
       }
-      tet_contrib(c, t, env, T, Ri, z6);
+      tet_jt<EXACT>(c, t, env, T, Ri, z6);
     } else if (it < nd + nt + na) {
       const int a = it - nd - nt;
       double jv[3];
@@ -1263,6 +1402,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
 // az = A z rows (apply_a second half, solver.py:388-399) + rho partial z.az.
 // setup != 0: rho = z.az (pcr_solve setup, solver.py:70-73); else
 // beta = rho_new / rho (solver.py:87-89). Absent contact slots are skipped.
+template <bool EXACT>
 __global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setup) {
   SETUP
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
@@ -1282,7 +1422,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setu
       double Ri[9], y[6], zz[6], ez[6];
       tet_load(c, t, env, T);
       tet_rinv(c, t, Ri);
-      tet_forward(c, t, env, T, Ri, u, y);
+      tet_j<EXACT>(c, t, env, T, Ri, u, y);
 #pragma unroll
       for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
       ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], zz, ez);
@@ -1359,26 +1499,47 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
   const double beta = c.K.beta[env];
   const int n_el = c.D.nd + c.D.nt + c.D.na + c.D.nh + c.D.ns;
   double part = 0.0;
+  double* __restrict__ P_ = c.K.p;
+  double* __restrict__ AP = c.K.ap;
+  const double* __restrict__ Z = c.K.z;
+  const double* __restrict__ AZ = c.K.az;
+  const double* __restrict__ Dg = c.K.d;
   FOR_ITEMS(it, n_el) {
     int rows[6];
     const int nr = item_rows(c, it, env, rows);
+    // all loads first (independent), then the updates
+    double zr[6], azr[6], pr[6], apr[6], dr[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
-      if (q >= nr) break;
-      const size_t o = IX(rows[q]);
-      double ap;
-      if (setup) {
-        c.K.p[o] = c.K.z[o];
-        ap = c.K.az[o];
-        c.K.ap[o] = ap;
-      } else if (!brk) {
-        c.K.p[o] = c.K.z[o] + beta * c.K.p[o];
-        ap = c.K.az[o] + beta * c.K.ap[o];
-        c.K.ap[o] = ap;
-      } else {
-        ap = c.K.ap[o];
+      if (q < nr) {
+        const size_t o = IX(rows[q]);
+        zr[q] = Z[o];
+        azr[q] = AZ[o];
+        dr[q] = Dg[o];
+        if (!setup) {
+          pr[q] = P_[o];
+          apr[q] = AP[o];
+        }
       }
-      part += ap * (ap / c.K.d[o]);
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q < nr) {
+        const size_t o = IX(rows[q]);
+        double ap;
+        if (setup) {
+          P_[o] = zr[q];
+          ap = azr[q];
+          AP[o] = ap;
+        } else if (!brk) {
+          P_[o] = zr[q] + beta * pr[q];
+          ap = azr[q] + beta * apr[q];
+          AP[o] = ap;
+        } else {
+          ap = apr[q];
+        }
+        part += ap * (ap / dr[q]);
+      }
     }
   }
   double den;
@@ -1392,26 +1553,45 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
 
 // x += alpha p, r -= alpha ap, z = r/d (solver.py:81-84), then the tet
 // column sums of J^T z for the next apply.
+template <bool EXACT>
 __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
   SETUP
   if (c.K.broken[env]) return;  // the reference skips the whole iteration
   const double alpha = c.K.alpha[env];
   const int nd = c.D.nd, nt = c.D.nt;
   const int n_el = nd + nt + c.D.na + c.D.nh + c.D.ns;
+  double* __restrict__ X_ = c.K.x;
+  double* __restrict__ R_ = c.K.r;
+  double* __restrict__ Z_ = c.K.z;
+  const double* __restrict__ P_ = c.K.p;
+  const double* __restrict__ AP = c.K.ap;
+  const double* __restrict__ Dg = c.K.d;
   FOR_ITEMS(it, n_el) {
     int rows[6];
     const int nr = item_rows(c, it, env, rows);
-    double z6[6];
+    double xr[6], pr[6], rr[6], apr[6], dr[6], z6[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
-      if (q >= nr) break;
-      const size_t o = IX(rows[q]);
-      c.K.x[o] += alpha * c.K.p[o];
-      const double r = c.K.r[o] - alpha * c.K.ap[o];
-      const double z = r / c.K.d[o];
-      c.K.r[o] = r;
-      c.K.z[o] = z;
-      z6[q] = z;
+      if (q < nr) {
+        const size_t o = IX(rows[q]);
+        xr[q] = X_[o];
+        pr[q] = P_[o];
+        rr[q] = R_[o];
+        apr[q] = AP[o];
+        dr[q] = Dg[o];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q < nr) {
+        const size_t o = IX(rows[q]);
+        X_[o] = xr[q] + alpha * pr[q];
+        const double r = rr[q] - alpha * apr[q];
+        const double z = r / dr[q];
+        R_[o] = r;
+        Z_[o] = z;
+        z6[q] = z;
+      }
     }
     if (it >= nd && it < nd + nt) {
       const int t = it - nd;
@@ -1419,7 +1599,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
       double Ri[9];
       tet_load(c, t, env, T);
       tet_rinv(c, t, Ri);
-      tet_contrib(c, t, env, T, Ri, z6);
+      tet_jt<EXACT>(c, t, env, T, Ri, z6);
     }
   }
 }
@@ -1430,6 +1610,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
 // column sums of J^T dlam; residual sqrt(max(r.z, 0)) of the solve; on the
 // last Newton pass store_warm (contact.py:167-180). do_step = 0 when
 // pcr_iters == 0.
+template <bool EXACT>
 __global__ void __launch_bounds__(SS_THREADS) k_newton_final(const Ctx c, int do_step, int last) {
   SETUP
   const bool step = do_step && !c.K.broken[env];
@@ -1440,19 +1621,33 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_final(const Ctx c, int do
   FOR_ITEMS(it, n_el) {
     int rows[6];
     const int nr = item_rows(c, it, env, rows);
-    double dl[6];
+    double dl[6], xr[6], rr[6], zr[6], pr[6], apr[6], dr[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
-      if (q >= nr) break;
-      const size_t o = IX(rows[q]);
-      double x = c.K.x[o], r = c.K.r[o], z = c.K.z[o];
-      if (step) {
-        x += alpha * c.K.p[o];
-        r -= alpha * c.K.ap[o];
-        z = r / c.K.d[o];
+      if (q < nr) {
+        const size_t o = IX(rows[q]);
+        xr[q] = c.K.x[o];
+        rr[q] = c.K.r[o];
+        zr[q] = c.K.z[o];
+        if (step) {
+          pr[q] = c.K.p[o];
+          apr[q] = c.K.ap[o];
+          dr[q] = c.K.d[o];
+        }
       }
-      part += r * z;
-      dl[q] = x;
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q < nr) {
+        double x = xr[q], r = rr[q], z = zr[q];
+        if (step) {
+          x += alpha * pr[q];
+          r -= alpha * apr[q];
+          z = r / dr[q];
+        }
+        part += r * z;
+        dl[q] = x;
+      }
     }
     if (it < nd + nt + na + nh) {
       double d6[6];
@@ -1472,7 +1667,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_final(const Ctx c, int do
         double Ri[9];
         tet_load(c, t, env, T);
         tet_rinv(c, t, Ri);
-        tet_contrib(c, t, env, T, Ri, d6);
+        tet_jt<EXACT>(c, t, env, T, Ri, d6);
       }
     } else {
       const int s = it - nd - nt - na - nh;

@@ -2,47 +2,57 @@
 
 Bytes are the env-private traffic one launch must move per environment if
 every operand is read once and every result written once (fp64 values,
-int32 flags), with the scene topology (index arrays, rest-shape inverses,
-incidence lists) excluded: it is shared by all environments of a batch and
-stays L2-resident. These are the figures bench.py's `roofline.achieved`
-divides by the live CUDA-event duration; DESIGN.md derives them.
+int32 flags). Scene topology shared by every environment of a batch
+(index arrays, rest-shape inverses, incidence lists, compliance) is
+excluded: it is read by all envs and stays L2-resident. Contact rows count
+only for present contacts (absent slots are skipped by every kernel); `nc`
+is the mean number of present contacts per substep. DESIGN.md §4 derives
+each line; bench.py divides by the live CUDA-event duration.
 """
 from __future__ import annotations
 
+F8 = 8
+
 
 def dims_of(sim) -> dict:
-    d = sim._packed.dims if sim._packed is not None else None
-    if d is None:
-        sim._ensure()
-        d = sim._packed.dims
+    sim._ensure()
+    d = sim._packed.dims
     P, nb, nd, nt, na, nh, nw = (d[k] for k in ("P", "nb", "nd", "nt", "na", "nh", "nw"))
     ground = bool(sim.config.ground_enabled)
     nq = (d["ncp"] if not d["cp_all"] else P) if ground else 0
     nw = nw if ground else 0
-    ns = nw + nq
     ms = nd + 6 * nt + 3 * na + 5 * nh
-    return dict(P=P, nb=nb, nd=nd, nt=nt, na=na, nh=nh, nw=nw, ns=ns, ms=ms, m=ms + 3 * ns,
+    return dict(P=P, nb=nb, nd=nd, nt=nt, na=na, nh=nh, nw=nw, ns=nw + nq, ms=ms,
                 ndof=3 * P + 6 * nb)
 
 
-def bytes_per_launch_per_env(kernel: str, d: dict) -> int:
-    f8 = 8
-    J = f8 * (72 * d["nt"] + 3 * d["nd"] + 3 * d["na"] + 60 * d["nh"] + 18 * d["nw"])
-    flags = 4 * d["ns"]
-    if kernel == "k_gather":
-        # J once, x rows once, ang_inv, contact flags; u (or v) written once
-        return J + f8 * d["m"] + f8 * 9 * d["nb"] + flags + f8 * d["ns"] + f8 * d["ndof"]
-    if kernel == "k_apply_rows":
-        # J once, u once, z once, dyn/act of contacts; az written once
-        return J + f8 * d["ndof"] + f8 * d["m"] + flags + 2 * f8 * d["ns"] + f8 * d["m"]
-    if kernel == "k_pcr_dir":
-        return f8 * 7 * d["m"]     # read z az p ap d, write p ap
+def bytes_per_launch_per_env(kernel: str, d: dict, nc: float) -> float:
+    rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches
+    jc = F8 * 21 * d["nt"]                       # compact tet J: R(9) S(6) K^-1(6)
+    tc = F8 * 12 * d["nt"]                       # tet column sums J^T x
+    small_j = F8 * (3 * d["nd"] + 3 * d["na"] + 60 * d["nh"] + 18 * d["nw"])
+    flags = 4 * d["ns"] + F8 * 2 * nc            # present flags, actf/dynn of present
     if kernel == "k_pcr_step":
-        return f8 * 8 * d["m"]     # read x p r ap d, write x r z
+        # read x p r ap d, write x r z (rows); compact J; write tC
+        return F8 * 8 * rows + jc + tc + flags
+    if kernel == "k_pcr_dir":
+        # read z az p ap d, write p ap
+        return F8 * 7 * rows + flags
+    if kernel == "k_apply_rows":
+        # compact J, small-family J, u (once), z (own rows), write az
+        return jc + small_j + F8 * d["ndof"] + F8 * 2 * rows + flags
+    if kernel == "k_gather":
+        # tC once, non-tet x rows once, small-family J, ang_inv; write u
+        return tc + F8 * (rows - 6 * d["nt"]) + small_j + F8 * 9 * d["nb"] + flags + \
+            F8 * d["ndof"]
     if kernel == "k_newton_rhs":
-        # J once, v once, res/lam/bdiag once; write r d z x
-        return J + f8 * d["ndof"] + 3 * f8 * d["m"] + 4 * f8 * d["m"] + flags
+        # compact J, v, res/lam/bdiag of rows, write r d z x, write tC
+        return jc + small_j + F8 * d["ndof"] + F8 * 3 * rows + F8 * 4 * rows + tc + flags
+    if kernel == "k_newton_final":
+        # read x r z p ap d + lam, write lam + dlam, compact J, write tC
+        return F8 * 9 * rows + jc + tc + flags
     if kernel == "k_eval_tet":
-        # positions once, quats read+write, J + res + diag written
-        return f8 * (3 * d["P"] + 8 * d["nt"] + 72 * d["nt"] + 12 * d["nt"])
-    return 0
+        # positions once, quats r/w, compact J + diag + tC written, lam read
+        return F8 * (3 * d["P"] + 8 * d["nt"] + 21 * d["nt"] + 6 * d["nt"] + 12 * d["nt"]
+                     + 6 * d["nt"])
+    return 0.0

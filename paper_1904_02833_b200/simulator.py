@@ -40,6 +40,9 @@ class SolverConfig:
     constraint_damping: float = 1.0
     backend: str | None = None
     keep_matrix: bool = False
+    # B200 extension: materialised-column tet Jacobian (bitwise numba sums)
+    # instead of the structured chain-rule application (default)
+    exact_jacobian: bool = False
 
     @property
     def h(self) -> float:

@@ -18,8 +18,9 @@ def built():
     g.build()
 
 
-def _sim(tag, n_envs=1):
+def _sim(tag, n_envs=1, exact=False):
     parts, cfg = scene_parts(tag)
+    cfg.exact_jacobian = exact
     if n_envs == 1:
         return M.Simulator(config=cfg, **parts), parts, cfg
     return M.BatchedSimulator(n_envs, config=cfg, **parts), parts, cfg
@@ -29,10 +30,11 @@ def _one(a):
     return {k: v[0] for k, v in a.items()}
 
 
+@pytest.mark.parametrize("exact", [False, True], ids=["structuredJ", "exactJ"])
 @pytest.mark.parametrize("tag", ["B", "S"])
-def test_step_vs_reference_golden(tag):
+def test_step_vs_reference_golden(tag, exact):
     g = load_golden(f"step_{tag}.npz")
-    sim, _, _ = _sim(tag)
+    sim, _, _ = _sim(tag, exact=exact)
     for f in g["frames_captured"]:
         sim.set_state_arrays(golden_frame(g, f, "before"), 0, 1)
         st = sim.step(g[f"f{f}.commands"], latency=True)
@@ -44,10 +46,11 @@ def test_step_vs_reference_golden(tag):
         assert st.residual == pytest.approx(float(g[f"f{f}.residual"]), rel=1e-8)
 
 
+@pytest.mark.parametrize("exact", [False, True], ids=["structuredJ", "exactJ"])
 @pytest.mark.parametrize("tag", ["B", "S"])
-def test_step_vs_oracle(oracle_mod, tag):
+def test_step_vs_oracle(oracle_mod, tag, exact):
     g = load_golden(f"step_{tag}.npz")
-    sim, parts, cfg = _sim(tag)
+    sim, parts, cfg = _sim(tag, exact=exact)
     for f in g["frames_captured"]:
         before = golden_frame(g, f, "before")
         o = oracle_mod.OracleSim(config=cfg, **parts)
