@@ -65,46 +65,62 @@ def env_commands(n_envs: int, frames: int, first_frame: int, env0: int = 0):
 
 
 # ----------------------------------------------------------------- CPU leg
+class CpuArm:
+    """The reference algorithm (oracle C port) on host cores: one snake per
+    core, stepped in threads (ctypes releases the GIL)."""
+
+    def __init__(self, cores: int | None = None, frames: int = 64):
+        from concurrent.futures import ThreadPoolExecutor
+        from oracle.oracle import OracleSim
+        import paper_1904_02833_b200 as M
+        from paper_1904_02833_b200.model import build_scene_parts
+        self.cores = cores or len(os.sched_getaffinity(0))
+        sc = M.SceneConfig()
+        parts, *_ = build_scene_parts(sc)
+        cfg = sc.solver_config()
+        self.sims = [OracleSim(config=cfg, **parts) for _ in range(self.cores)]
+        self.cmds = env_commands(self.cores, frames, 0)
+        self.frame = 0
+        self.ex = ThreadPoolExecutor(self.cores)
+
+    def step(self, frames: int = 1):
+        f0 = self.frame
+
+        def run(e):
+            for f in range(frames):
+                self.sims[e].step(self.cmds[(f0 + f) % len(self.cmds), e], True)
+
+        list(self.ex.map(run, range(self.cores)))
+        self.frame += frames
+
+    def close(self):
+        self.ex.shutdown()
+
+
 def cpu_oracle_rate(frames_per_core: int, cores: int | None = None):
-    """The reference algorithm (oracle C port) on all host cores: one snake
-    per core, frames_per_core frames each, threads released from the GIL by
-    ctypes. Returns (snake-steps/s, cores, seconds)."""
-    from concurrent.futures import ThreadPoolExecutor
-    from oracle.oracle import OracleSim
-    import paper_1904_02833_b200 as M
-    from paper_1904_02833_b200.model import build_scene_parts
-    cores = cores or len(os.sched_getaffinity(0))
-    sc = M.SceneConfig()
-    parts, *_ = build_scene_parts(sc)
-    cfg = sc.solver_config()
-    sims = [OracleSim(config=cfg, **parts) for _ in range(cores)]
-    cmds = env_commands(cores, frames_per_core + 1, 0)
-    sims_cmd = [(s, cmds[:, e]) for e, s in enumerate(sims)]
-
-    def run(args, frames, first):
-        s, c = args
-        for f in range(frames):
-            s.step(c[first + f], True)
-
-    with ThreadPoolExecutor(cores) as ex:
-        list(ex.map(lambda a: run(a, 1, 0), sims_cmd))        # warm-up frame
-        t = time.perf_counter()
-        list(ex.map(lambda a: run(a, frames_per_core, 1), sims_cmd))
-        dt = time.perf_counter() - t
-    return cores * frames_per_core / dt, cores, dt
+    """snake-steps/s of the oracle port on all host cores (1 warm-up frame)."""
+    arm = CpuArm(cores, frames_per_core + 1)
+    arm.step(1)
+    t = time.perf_counter()
+    arm.step(frames_per_core)
+    dt = time.perf_counter() - t
+    arm.close()
+    return arm.cores * frames_per_core / dt, arm.cores, dt
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = len(os.sched_getaffinity(0))
+    arm = CpuArm(frames=args.warmup + args.steps)
+    cores = arm.cores
     for _ in range(args.warmup):
-        cpu_oracle_rate(1, cores)
+        arm.step(1)
     t = time.perf_counter()
     for _ in range(args.steps):
-        cpu_oracle_rate(1, cores)
+        arm.step(1)
     wall = time.perf_counter() - t
+    arm.close()
     # each step: every core advances its own snake by one frame
     rate = cores * args.steps / wall
     line = {
@@ -264,7 +280,9 @@ def main():
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(top)
+        tj = json.load(open(tp))
+        if tj.get(top) is not None:
+            traffic = float(tj[top]) * n / float(tj.get("_envs", 1024))  # scaled to this env count
 
     if rank != 0:
         if dist:

@@ -88,8 +88,9 @@ constexpr long kReduceBlocks = 148 * 8;
 // kernel names for the profiler (ss_profile_frames)
 const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
                                     "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_apply_rows",
-                                    "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate"};
-constexpr int kNumKernels = 12;
+                                    "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
+                                    "k_tet_jt"};
+constexpr int kNumKernels = 13;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -158,7 +159,8 @@ int enqueue_frame_t(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof)
         LAUNCH(k_apply_rows<EX>, g_red, c, 1);
         LAUNCH(k_pcr_dir, g_red, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
-          LAUNCH(k_pcr_step<EX>, g_el, c);  // + tet J^T z
+          LAUNCH(k_pcr_step, g_el, c);
+          if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
           LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
           LAUNCH(k_apply_rows<EX>, g_red, c, 0);
           LAUNCH(k_pcr_dir, g_red, c, 0);

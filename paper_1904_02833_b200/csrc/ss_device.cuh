@@ -1491,23 +1491,34 @@ __global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setu
   }
 }
 
+// Row-wise iteration over the m rows of an env: static rows always, contact
+// rows only when their slot is present (absent slots do not exist in the
+// reference's compacted system). Returns false for an absent contact row.
+DI bool row_live(const Ctx& c, int row, int env) {
+  if (row < c.D.ms) return true;
+  const int E = c.D.E;
+  int s = row - c.D.ms;
+  s = s < c.D.ns ? s : (s < 2 * c.D.ns ? s - c.D.ns : s - 2 * c.D.ns);
+  return c.K.present[IX(s)] != 0;
+}
+
 // p = z + beta p, ap = az + beta ap (setup: copies), then den = ap.(ap/d)
 // and alpha = rho/den with the breakdown guard (solver.py:71-81, 90-91).
+// Element-owned rows, all loads of an element issued before its stores.
 __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) {
   SETUP
   const bool brk = c.K.broken[env] != 0;
   const double beta = c.K.beta[env];
   const int n_el = c.D.nd + c.D.nt + c.D.na + c.D.nh + c.D.ns;
-  double part = 0.0;
   double* __restrict__ P_ = c.K.p;
   double* __restrict__ AP = c.K.ap;
   const double* __restrict__ Z = c.K.z;
   const double* __restrict__ AZ = c.K.az;
   const double* __restrict__ Dg = c.K.d;
+  double part = 0.0;
   FOR_ITEMS(it, n_el) {
     int rows[6];
     const int nr = item_rows(c, it, env, rows);
-    // all loads first (independent), then the updates
     double zr[6], azr[6], pr[6], apr[6], dr[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
@@ -1551,15 +1562,13 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
   }
 }
 
-// x += alpha p, r -= alpha ap, z = r/d (solver.py:81-84), then the tet
-// column sums of J^T z for the next apply.
-template <bool EXACT>
+// x += alpha p, r -= alpha ap, z = r/d (solver.py:81-84); element-owned
+// rows, loads before stores.
 __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
   SETUP
   if (c.K.broken[env]) return;  // the reference skips the whole iteration
   const double alpha = c.K.alpha[env];
-  const int nd = c.D.nd, nt = c.D.nt;
-  const int n_el = nd + nt + c.D.na + c.D.nh + c.D.ns;
+  const int n_el = c.D.nd + c.D.nt + c.D.na + c.D.nh + c.D.ns;
   double* __restrict__ X_ = c.K.x;
   double* __restrict__ R_ = c.K.r;
   double* __restrict__ Z_ = c.K.z;
@@ -1569,7 +1578,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
   FOR_ITEMS(it, n_el) {
     int rows[6];
     const int nr = item_rows(c, it, env, rows);
-    double xr[6], pr[6], rr[6], apr[6], dr[6], z6[6];
+    double xr[6], pr[6], rr[6], apr[6], dr[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       if (q < nr) {
@@ -1587,20 +1596,27 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
         const size_t o = IX(rows[q]);
         X_[o] = xr[q] + alpha * pr[q];
         const double r = rr[q] - alpha * apr[q];
-        const double z = r / dr[q];
         R_[o] = r;
-        Z_[o] = z;
-        z6[q] = z;
+        Z_[o] = r / dr[q];
       }
     }
-    if (it >= nd && it < nd + nt) {
-      const int t = it - nd;
-      TetC T;
-      double Ri[9];
-      tet_load(c, t, env, T);
-      tet_rinv(c, t, Ri);
-      tet_jt<EXACT>(c, t, env, T, Ri, z6);
-    }
+  }
+}
+
+// tet column sums of J^T z for the next apply (after k_pcr_step)
+template <bool EXACT>
+__global__ void __launch_bounds__(SS_THREADS) k_tet_jt(const Ctx c) {
+  SETUP
+  if (c.K.broken[env]) return;  // z unchanged: tC from the previous pass is still valid
+  const int nt = c.D.nt;
+  FOR_ITEMS(t, nt) {
+    double z6[6], Ri[9];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) z6[i] = c.K.z[IX(c.D.ot + i * nt + t)];
+    TetC T;
+    tet_load(c, t, env, T);
+    tet_rinv(c, t, Ri);
+    tet_jt<EXACT>(c, t, env, T, Ri, z6);
   }
 }
 
