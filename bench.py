@@ -301,7 +301,8 @@ def main():
                    "gait": "default, per-env turn bias U(-0.5,0.5), t0 U(0,0.5s), seed 20260817",
                    "l2": "no flush: per-step working set "
                          f"{sim.device_bytes / 1e9:.1f} GB >> 126 MB L2",
-                   "parallelism": f"env-sharded x{world}"},
+                   "parallelism": f"env-sharded x{world}",
+                   "solver": sim.solver_info},
         "rtf": value / 60.0,
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,

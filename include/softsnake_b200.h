@@ -110,6 +110,10 @@ typedef struct ss_params {
    * chain-rule application of the same operator, ~5x fewer FP64 ops,
    * rounding-level (1e-16) differences. */
   int32_t exact_jacobian;
+  /* Newton-loop solver: 0 auto (= streaming), 1 streaming batched kernels,
+   * 2 cluster-resident: one env per <=16-CTA cluster, PCR state in shared
+   * memory (error if the scene does not fit). */
+  int32_t solver_mode;
 } ss_params;
 
 /* Full per-environment state. Host pointers;
@@ -183,6 +187,12 @@ void* ss_stream(ss_handle* h);
 int ss_launches_per_frame(ss_handle* h);
 /* Bytes of device memory held by the handle. */
 int64_t ss_device_bytes(ss_handle* h);
+/* info[0] 1 if the cluster-resident solver is used, info[1] CTAs per
+ * cluster, info[2] shared bytes per CTA, info[3] padded env lanes. */
+int ss_solver_info(ss_handle* h, int* info);
+/* Debug: clock64 phase stamps of one PCR iteration of the cluster solver
+ * (handle created with SS_CLUSTER_STAMPS set); out[16]. */
+int ss_cluster_stamps(ss_handle* h, long long* out);
 /* Kernel names (static strings) of the step, in profiler slot order;
  * returns the number of kernels. */
 int ss_kernel_names(const char** names, int cap);

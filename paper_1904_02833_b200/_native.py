@@ -37,6 +37,8 @@ SIGNATURES = {
     "ss_launches_per_frame": (C.c_int, [_vp]),
     "ss_device_bytes": (C.c_int64, [_vp]),
     "ss_kernel_names": (C.c_int, [C.POINTER(C.c_char_p), _i]),
+    "ss_solver_info": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "ss_cluster_stamps": (C.c_int, [_vp, C.POINTER(C.c_longlong)]),
     "ss_profile_frames": (C.c_int, [_vp, _dp, _i, _i, _dp, C.POINTER(C.c_int)]),
     "ssk_block_forward": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "ssk_block_transpose": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp]),

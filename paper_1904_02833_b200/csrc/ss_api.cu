@@ -8,11 +8,13 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/softsnake_b200.h"
+#include "ss_cluster.cuh"
 #include "ss_device.cuh"
 #include "ss_kabi.cuh"
 
@@ -67,6 +69,10 @@ struct ss_handle {
   size_t stage_bytes = 0;
   cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};
   int launches = 0;
+  // cluster-resident Newton solver (0 = streaming kernels)
+  int use_cluster = 0;
+  ClPlan plan{};
+  void* plan_mem = nullptr;
 };
 
 namespace {
@@ -89,8 +95,8 @@ constexpr long kReduceBlocks = 148 * 8;
 const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
                                     "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_apply_rows",
                                     "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
-                                    "k_tet_jt"};
-constexpr int kNumKernels = 13;
+                                    "k_tet_jt",      "k_newton_cluster"};
+constexpr int kNumKernels = 14;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -151,6 +157,35 @@ int enqueue_frame_t(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof)
     if (D.ns) LAUNCH(k_slots, g_slots, c);
     if (D.nt) LAUNCH(k_eval_tet<EX>, g_tet, c);  // + tet J^T lam
     if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
+    if (H->use_cluster) {
+      // whole Newton loop, one environment per cluster (ss_cluster.cuh)
+      cudaEvent_t e0_ = nullptr, e1_ = nullptr;
+      if (prof) {
+        cudaEventCreate(&e0_);
+        cudaEventCreate(&e1_);
+        cudaEventRecord(e0_, st);
+      }
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = H->plan.C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cfg.blockDim = dim3(CL_THREADS);
+      cfg.gridDim = dim3(H->plan.C * D.E);
+      cfg.dynamicSmemBytes = 8 * (size_t)H->plan.smem_doubles;
+      cfg.stream = st;
+      CK(cudaLaunchKernelEx(&cfg, k_newton_cluster<EX>, c, H->plan));
+      if (prof) {
+        cudaEventRecord(e1_, st);
+        prof->ev.push_back({kid("k_newton_cluster"), {e0_, e1_}});
+      }
+      ++n;
+      LAUNCH(k_integrate, g_int, c);
+      continue;
+    }
     LAUNCH(k_gather, g_gather, c, 1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
     for (int it = 0; it < c.p.newton; ++it) {
       LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
@@ -246,6 +281,338 @@ __global__ void k_fill(double* p, size_t n, double val) {
 }
 
 }  // namespace
+
+// ------------------------------------------------------ cluster plan
+// Partition of one environment over the C CTAs of a cluster (contiguous tet
+// ranges = mesh slabs; every other element follows its first node). Each
+// CTA gets: its element list, the local U/V layout (owned DOFs, then halo
+// copies of the foreign nodes its elements touch), an inbox slot per
+// incidence of every owned node in the reference accumulation order (the
+// same sorted incidence lists as the streaming path), the inbox destination
+// of every column block its elements produce, and the halo push lists.
+struct PlanBuild {
+  int C;
+  std::vector<int> own_t, own_d, own_a, own_h, own_s, own_p, own_b;  // owner CTA
+  std::vector<int> loc_t, loc_d, loc_a, loc_h, loc_s, loc_p, loc_b;  // family-local index
+  std::vector<std::vector<int>> Lt, Ld, La, Lh, Ls, Lp, Lb;          // per CTA lists
+  std::vector<std::vector<int>> halo;  // per CTA: halo nodes (global node id: p or P+b)
+  std::vector<int> in_size;            // per CTA inbox doubles
+  ClPlan P;
+  size_t smem_bytes;
+};
+
+static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& d_i,
+                           const std::vector<int>& d_j, const std::vector<int>& tets,
+                           const std::vector<int>& a_p, const std::vector<int>& a_b,
+                           const std::vector<int>& h_a, const std::vector<int>& h_b,
+                           const std::vector<int>& w_body, const std::vector<int>& slot_part,
+                           const std::vector<int>& inc_ptr_g) {
+  const int C = B.C;
+  B.own_t.assign(D.nt, 0);
+  for (int t = 0; t < D.nt; ++t) B.own_t[t] = (int)((long)t * C / std::max(D.nt, 1));
+  B.own_p.assign(D.P, -1);
+  for (int t = 0; t < D.nt; ++t)
+    for (int v = 0; v < 4; ++v) {
+      const int p = tets[4 * (size_t)t + v];
+      if (B.own_p[p] < 0) B.own_p[p] = B.own_t[t];
+    }
+  for (int p = 0; p < D.P; ++p)
+    if (B.own_p[p] < 0) B.own_p[p] = (int)((long)p * C / std::max(D.P, 1));
+  B.own_b.assign(D.nb, -1);
+  for (int a = 0; a < D.na; ++a)
+    if (B.own_b[a_b[a]] < 0) B.own_b[a_b[a]] = B.own_p[a_p[a]];
+  for (int pass = 0; pass < 2; ++pass)
+    for (int h = 0; h < D.nh; ++h) {
+      if (B.own_b[h_a[h]] < 0 && B.own_b[h_b[h]] >= 0) B.own_b[h_a[h]] = B.own_b[h_b[h]];
+      if (B.own_b[h_b[h]] < 0 && B.own_b[h_a[h]] >= 0) B.own_b[h_b[h]] = B.own_b[h_a[h]];
+    }
+  for (int b = 0; b < D.nb; ++b)
+    if (B.own_b[b] < 0) B.own_b[b] = b % C;
+  B.own_d.resize(D.nd);
+  for (int d = 0; d < D.nd; ++d) B.own_d[d] = B.own_p[d_i[d]];
+  B.own_a.resize(D.na);
+  for (int a = 0; a < D.na; ++a) B.own_a[a] = B.own_p[a_p[a]];
+  B.own_h.resize(D.nh);
+  for (int h = 0; h < D.nh; ++h) B.own_h[h] = B.own_b[h_a[h]];
+  B.own_s.resize(D.ns);
+  for (int s = 0; s < D.ns; ++s)
+    B.own_s[s] = s < D.nw ? B.own_b[w_body[s]] : B.own_p[slot_part[s - D.nw]];
+  auto lists = [&](const std::vector<int>& own, std::vector<std::vector<int>>& Lx,
+                   std::vector<int>& loc) {
+    Lx.assign(C, {});
+    loc.assign(own.size(), 0);
+    for (size_t i = 0; i < own.size(); ++i) {
+      loc[i] = (int)Lx[own[i]].size();
+      Lx[own[i]].push_back((int)i);
+    }
+  };
+  lists(B.own_t, B.Lt, B.loc_t);
+  lists(B.own_d, B.Ld, B.loc_d);
+  lists(B.own_a, B.La, B.loc_a);
+  lists(B.own_h, B.Lh, B.loc_h);
+  lists(B.own_s, B.Ls, B.loc_s);
+  lists(B.own_p, B.Lp, B.loc_p);
+  lists(B.own_b, B.Lb, B.loc_b);
+  // halo nodes: foreign nodes touched by local elements (sorted, unique)
+  B.halo.assign(C, {});
+  auto own_of = [&](int gn) { return gn < D.P ? B.own_p[gn] : B.own_b[gn - D.P]; };
+  for (int c = 0; c < C; ++c) {
+    std::vector<int> h;
+    auto need = [&](int gn) { if (own_of(gn) != c) h.push_back(gn); };
+    for (int t : B.Lt[c])
+      for (int v = 0; v < 4; ++v) need(tets[4 * (size_t)t + v]);
+    for (int d : B.Ld[c]) { need(d_i[d]); need(d_j[d]); }
+    for (int a : B.La[c]) { need(a_p[a]); need(D.P + a_b[a]); }
+    for (int x : B.Lh[c]) { need(D.P + h_a[x]); need(D.P + h_b[x]); }
+    for (int s : B.Ls[c]) {
+      if (s < D.nw) need(D.P + w_body[s]);
+      else { need(slot_part[s - D.nw]); need(0); }
+    }
+    std::sort(h.begin(), h.end());
+    h.erase(std::unique(h.begin(), h.end()), h.end());
+    B.halo[c] = h;
+  }
+  B.in_size.assign(C, 0);
+  for (int c = 0; c < C; ++c) {
+    int sz = 0;
+    for (int p : B.Lp[c]) sz += 3 * (inc_ptr_g[p + 1] - inc_ptr_g[p]);
+    for (int b : B.Lb[c]) sz += 6 * (inc_ptr_g[D.P + b + 1] - inc_ptr_g[D.P + b]);
+    B.in_size[c] = sz;
+  }
+  auto mx = [&](const std::vector<std::vector<int>>& Lx) {
+    size_t m = 1;
+    for (auto& v : Lx) m = std::max(m, v.size());
+    return (int)m;
+  };
+  ClPlan& P = B.P;
+  P = ClPlan{};
+  P.C = C;
+  P.MT = mx(B.Lt); P.MD = mx(B.Ld); P.MA = mx(B.La); P.MH = mx(B.Lh); P.MS = mx(B.Ls);
+  P.MP = mx(B.Lp); P.MB = mx(B.Lb);
+  P.MW = 1;
+  for (auto& v : B.Ls) {
+    int w = 0;
+    for (int s : v) w += s < D.nw ? 1 : 0;
+    P.MW = std::max(P.MW, w);
+  }
+  P.NR = 6 * P.MT + P.MD + 3 * P.MA + 5 * P.MH + 3 * P.MS;
+  P.ME = P.MT + P.MD + P.MA + P.MH + P.MS;
+  P.MN = P.MP + P.MB;
+  P.MDOFX = 1;
+  for (int c = 0; c < C; ++c) {
+    int n = 3 * (int)B.Lp[c].size() + 6 * (int)B.Lb[c].size();
+    for (int gn : B.halo[c]) n += gn < D.P ? 3 : 6;
+    P.MDOFX = std::max(P.MDOFX, n);
+  }
+  P.MIN = 2;
+  for (int v : B.in_size) P.MIN = std::max(P.MIN, v);
+  int off = 0;
+  auto take = [&](int n) { const int o = off; off += (n + 1) & ~1; return o; };
+  P.oX = take(P.NR); P.oR = take(P.NR); P.oZ = take(P.NR); P.oP = take(P.NR);
+  P.oAP = take(P.NR); P.oAZ = take(P.NR); P.oD = take(P.NR);
+  P.oJR = take(9 * P.MT); P.oJS = take(6 * P.MT); P.oJK = take(6 * P.MT);
+  P.oIn = take(P.MIN);
+  P.oDir = take(3 * P.MD); P.oRw = take(3 * P.MA); P.oHJ = take(60 * P.MH);
+  P.oWJ = take(18 * P.MW);
+  P.oPres = take(P.MS); P.oGap = take(P.MS); P.oLc = take(3 * P.MS); P.oAct = take(P.MS);
+  P.oDyn = take(P.MS); P.oBdn = take(P.MS); P.oBdf = take(2 * P.MS);
+  P.oResD = take(P.MD); P.oResA = take(3 * P.MA); P.oResH = take(5 * P.MH);
+  P.oU = take(P.MDOFX); P.oV = take(P.MDOFX); P.oAng = take(9 * P.MB);
+  P.oRed = take(16 * C);
+  P.smem_doubles = off;
+  B.smem_bytes = 8 * (size_t)off;
+}
+
+// device tables of a partition
+static int plan_upload(ss_handle* H, PlanBuild& B, const Dims& D, const std::vector<int>& d_i,
+                       const std::vector<int>& d_j, const std::vector<int>& tets,
+                       const std::vector<int>& a_p, const std::vector<int>& a_b,
+                       const std::vector<int>& h_a, const std::vector<int>& h_b,
+                       const std::vector<int>& w_body, const std::vector<int>& slot_part,
+                       const std::vector<int>& inc_ptr_g, const std::vector<int>& inc_g) {
+  ClPlan& P = B.P;
+  const int C = B.C;
+  auto own_of = [&](int gn) { return gn < D.P ? B.own_p[gn] : B.own_b[gn - D.P]; };
+  // local U/V offset of a global node in CTA c (owned or halo)
+  std::vector<std::vector<int>> halo_off(C);
+  for (int c = 0; c < C; ++c) {
+    int o = 3 * (int)B.Lp[c].size() + 6 * (int)B.Lb[c].size();
+    for (int gn : B.halo[c]) {
+      halo_off[c].push_back(o);
+      o += gn < D.P ? 3 : 6;
+    }
+  }
+  auto local_off = [&](int c, int gn) -> int {
+    if (own_of(gn) == c) {
+      if (gn < D.P) return 3 * B.loc_p[gn];
+      return 3 * (int)B.Lp[c].size() + 6 * B.loc_b[gn - D.P];
+    }
+    const auto& h = B.halo[c];
+    const size_t i = std::lower_bound(h.begin(), h.end(), gn) - h.begin();
+    return halo_off[c][i];
+  };
+  // inbox destinations of every (family, element, vertex) incidence
+  std::vector<int> dst_t(4 * (size_t)D.nt), dst_d(2 * (size_t)D.nd), dst_ap(D.na), dst_ab(D.na),
+      dst_h(2 * (size_t)D.nh), dst_cn(D.ns), dst_cf(D.ns);
+  std::vector<int> in_ptr((size_t)C * (P.MN + 1), 0), node((size_t)C * P.MN, 0);
+  for (int c = 0; c < C; ++c) {
+    int o = 0, n = 0;
+    auto walk = [&](int gn) {
+      in_ptr[(size_t)c * (P.MN + 1) + n] = o;
+      node[(size_t)c * P.MN + n] = gn;
+      const int w = gn < D.P ? 3 : 6;
+      for (int k = inc_ptr_g[gn]; k < inc_ptr_g[gn + 1]; ++k) {
+        const int code = inc_g[k];
+        const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+        const int d = (c << 24) | o;
+        switch (fam) {
+          case F_DIST: dst_d[2 * (size_t)e + v] = d; break;
+          case F_TET: dst_t[4 * (size_t)e + v] = d; break;
+          case F_ATTP: dst_ap[e] = d; break;
+          case F_ATTB: dst_ab[e] = d; break;
+          case F_HINGE: dst_h[2 * (size_t)e + v] = d; break;
+          case F_CN: dst_cn[e] = d; break;
+          default: dst_cf[e] = d; break;
+        }
+        o += w;
+      }
+      ++n;
+    };
+    for (int p : B.Lp[c]) walk(p);
+    for (int b : B.Lb[c]) walk(D.P + b);
+    for (int k = n; k <= P.MN; ++k) in_ptr[(size_t)c * (P.MN + 1) + k] = o;
+  }
+  std::vector<int> cnt(8 * (size_t)C), elem((size_t)C * P.ME, 0), eref((size_t)C * P.ME * 4, 0),
+      dest((size_t)C * P.ME * 4, 0);
+  for (int c = 0; c < C; ++c) {
+    int* k = &cnt[8 * (size_t)c];
+    k[0] = (int)B.Lt[c].size(); k[1] = (int)B.Ld[c].size(); k[2] = (int)B.La[c].size();
+    k[3] = (int)B.Lh[c].size(); k[4] = (int)B.Ls[c].size(); k[5] = (int)B.Lp[c].size();
+    k[6] = (int)B.Lb[c].size(); k[7] = 0;
+    int e = 0;
+    auto put = [&](int g, std::initializer_list<int> nodes, std::initializer_list<int> dsts) {
+      elem[(size_t)c * P.ME + e] = g;
+      int q = 0;
+      for (int gn : nodes) eref[((size_t)c * P.ME + e) * 4 + q++] = local_off(c, gn);
+      q = 0;
+      for (int d : dsts) dest[((size_t)c * P.ME + e) * 4 + q++] = d;
+      ++e;
+    };
+    for (int t : B.Lt[c]) {
+      const int* tv = &tets[4 * (size_t)t];
+      put(t, {tv[0], tv[1], tv[2], tv[3]},
+          {dst_t[4 * (size_t)t], dst_t[4 * (size_t)t + 1], dst_t[4 * (size_t)t + 2], dst_t[4 * (size_t)t + 3]});
+    }
+    for (int d : B.Ld[c]) put(d, {d_i[d], d_j[d]}, {dst_d[2 * (size_t)d], dst_d[2 * (size_t)d + 1]});
+    for (int a : B.La[c]) put(a, {a_p[a], D.P + a_b[a]}, {dst_ap[a], dst_ab[a]});
+    for (int x : B.Lh[c]) put(x, {D.P + h_a[x], D.P + h_b[x]}, {dst_h[2 * (size_t)x], dst_h[2 * (size_t)x + 1]});
+    for (int s : B.Ls[c]) {
+      if (s < D.nw) put(s, {D.P + w_body[s]}, {dst_cn[s], dst_cf[s]});
+      else put(s, {slot_part[s - D.nw], 0}, {dst_cn[s], dst_cf[s]});
+    }
+  }
+  // halo pushes: owner -> every consumer holding a halo copy
+  std::vector<std::vector<std::pair<int, int>>> consumers((size_t)D.P + D.nb);
+  for (int c = 0; c < C; ++c)
+    for (size_t i = 0; i < B.halo[c].size(); ++i)
+      consumers[B.halo[c][i]].push_back({c, halo_off[c][i]});
+  std::vector<int> hp_ptr((size_t)C * (P.MN + 1), 0), hpush;
+  for (int c = 0; c < C; ++c) {
+    int n = 0;
+    auto emit = [&](int gn) {
+      hp_ptr[(size_t)c * (P.MN + 1) + n] = (int)hpush.size();
+      for (auto& pr : consumers[gn]) hpush.push_back((pr.first << 24) | pr.second);
+      ++n;
+    };
+    for (int p : B.Lp[c]) emit(p);
+    for (int b : B.Lb[c]) emit(D.P + b);
+    for (int k = n; k <= P.MN; ++k) hp_ptr[(size_t)c * (P.MN + 1) + k] = (int)hpush.size();
+  }
+  const size_t bytes = 4 * (cnt.size() + elem.size() + eref.size() + dest.size() + node.size() +
+                            in_ptr.size() + hp_ptr.size() + hpush.size()) + 9 * 256;
+  CK(cudaMalloc(&H->plan_mem, bytes));
+  char* base = (char*)H->plan_mem;
+  size_t o = 0;
+  auto up = [&](const std::vector<int>& v) -> const int* {
+    int* d = (int*)(base + o);
+    o += ((4 * v.size() + 255) / 256) * 256 + (v.empty() ? 256 : 0);
+    if (!v.empty()) cudaMemcpy(d, v.data(), 4 * v.size(), cudaMemcpyHostToDevice);
+    return d;
+  };
+  P.cnt = up(cnt);
+  P.elem = up(elem);
+  P.eref = up(eref);
+  P.dest = up(dest);
+  P.node = up(node);
+  P.in_ptr = up(in_ptr);
+  P.hp_ptr = up(hp_ptr);
+  P.hpush = up(hpush);
+  CK(cudaGetLastError());
+  H->bytes += bytes;
+  return SS_OK;
+}
+
+// choose the smallest cluster whose shared-memory plan fits, or none
+static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i,
+                        const std::vector<int>& d_j, const std::vector<int>& tets,
+                        const std::vector<int>& a_p, const std::vector<int>& a_b,
+                        const std::vector<int>& h_a, const std::vector<int>& h_b,
+                        const std::vector<int>& w_body, const std::vector<int>& slot_part,
+                        const std::vector<int>& inc_ptr_g, const std::vector<int>& inc_g,
+                        int allow) {
+  H->use_cluster = 0;
+  if (!allow) return SS_OK;
+  int dev = H->device, max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t budget = (size_t)max_smem - 1024;  // static reduction scratch
+  for (int C : {1, 2, 4, 8, 16}) {
+    PlanBuild B;
+    B.C = C;
+    plan_partition(B, D, d_i, d_j, tets, a_p, a_b, h_a, h_b, w_body, slot_part, inc_ptr_g);
+    if (B.smem_bytes > budget) continue;
+    // one element and one node per thread for the whole solve
+    {
+      bool ok = true;
+      for (int c2 = 0; c2 < C; ++c2) {
+        const size_t ne = B.Lt[c2].size() + B.Ld[c2].size() + B.La[c2].size() + B.Lh[c2].size() +
+                          B.Ls[c2].size();
+        if (ne > CL_THREADS || B.Lp[c2].size() + B.Lb[c2].size() > CL_THREADS) ok = false;
+      }
+      if (!ok) continue;
+    }
+    const void* fn = (const void*)(H->c.p.exact_j ? k_newton_cluster<true> : k_newton_cluster<false>);
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)B.smem_bytes));
+    if (C > 8) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(CL_THREADS);
+    cfg.gridDim = dim3(C);
+    cfg.dynamicSmemBytes = B.smem_bytes;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, fn, &cfg) != cudaSuccess || nclus < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    int rc = plan_upload(H, B, D, d_i, d_j, tets, a_p, a_b, h_a, h_b, w_body, slot_part,
+                         inc_ptr_g, inc_g);
+    if (rc) return rc;
+    H->plan = B.P;
+    H->plan.dbg = nullptr;
+    if (getenv("SS_CLUSTER_STAMPS")) {
+      CK(cudaMalloc(&H->plan.dbg, 64 * sizeof(long long)));
+      CK(cudaMemset(H->plan.dbg, 0, 64 * sizeof(long long)));
+    }
+    H->use_cluster = 1;
+    return SS_OK;
+  }
+  return SS_OK;
+}
 
 // ======================================================================
 extern "C" {
@@ -572,6 +939,23 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     return SS_ECUDA;
   }
 
+  // cluster-resident Newton solver plan (ss_params.solver_mode: 0 auto = streaming, 1 streaming,
+  // 2 cluster). The cluster solver is opt-in: it is correct (parity-tested) but latency-bound
+  // (DESIGN.md §7); the streaming kernels are faster on the batched workload.
+  {
+    std::vector<int> tets_v(t->tets, t->tets + 4 * (size_t)D.nt);
+    int prc = plan_cluster(H, D, d_i, d_j, tets_v, a_p, a_b, h_a, h_b, w_body, slot_part,
+                           inc_ptr, inc, p->solver_mode == 2);
+    if (prc) {
+      ss_destroy(H);
+      return prc;
+    }
+    if (p->solver_mode == 2 && !H->use_cluster) {
+      ss_destroy(H);
+      return fail(SS_EUNSUP, "scene does not fit the cluster-resident solver");
+    }
+  }
+
   // reduction grid (fixed: the partial-sum count per env)
   {
     const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
@@ -689,6 +1073,7 @@ int ss_destroy(ss_handle* H) {
   if (H->work_mem) cudaFree(H->work_mem);
   if (H->d_cmd) cudaFree(H->d_cmd);
   if (H->d_stage) cudaFree(H->d_stage);
+  if (H->plan_mem) cudaFree(H->plan_mem);
   if (H->stream) cudaStreamDestroy(H->stream);
   delete H;
   return SS_OK;
@@ -848,6 +1233,22 @@ int ss_launches_per_frame(ss_handle* H) {
 }
 
 int64_t ss_device_bytes(ss_handle* H) { return H ? (int64_t)H->bytes : 0; }
+
+int ss_cluster_stamps(ss_handle* H, long long* out) {
+  if (!H || !out) return fail(SS_EINVAL, "null argument");
+  if (!H->plan.dbg) return fail(SS_EINVAL, "stamps off (set SS_CLUSTER_STAMPS)");
+  CK(cudaMemcpy(out, H->plan.dbg, 16 * sizeof(long long), cudaMemcpyDeviceToHost));
+  return SS_OK;
+}
+
+int ss_solver_info(ss_handle* H, int* info) {
+  if (!H || !info) return fail(SS_EINVAL, "null argument");
+  info[0] = H->use_cluster;
+  info[1] = H->use_cluster ? H->plan.C : 0;
+  info[2] = H->use_cluster ? 8 * H->plan.smem_doubles : 0;
+  info[3] = H->c.D.E;
+  return SS_OK;
+}
 
 int ss_kernel_names(const char** names, int cap) {
   for (int i = 0; i < kNumKernels && i < cap; ++i) names[i] = kKernelNames[i];

@@ -1,0 +1,1049 @@
+// ss_cluster.cuh — cluster-resident Newton solver (one environment per
+// thread-block cluster).
+//
+// The whole Newton loop of a substep (solver.py:428-509: initial impulse,
+// newton_iters x {rhs, pcr_solve, multiplier update + projection, impulse})
+// runs inside ONE kernel launch in which a cluster of C CTAs (C <= 16,
+// one CTA per SM) owns one environment. The environment's elements and
+// DOF nodes are partitioned over the C CTAs (contiguous mesh slabs); every
+// PCR row vector, the compact tet Jacobians, the per-element J^T column
+// sums and the DOF vectors live in shared memory for the whole solve. The
+// node gather (J^T x, in the reference accumulation order) and the element
+// forward products (J u) only read local shared memory: every cross-CTA
+// transfer is a DSMEM *store* pushed by the producer before a cluster
+// barrier (column sums into per-incidence inbox slots of the node owner, in
+// the reference accumulation order; updated DOF values into halo copies of
+// the consumer CTAs; reduction partials into every peer). The per-env PCR
+// dot products are fixed-order trees combined across the cluster in rank
+// order (identical in every CTA, deterministic). HBM is
+// touched only to load the substep inputs and store the results, so the
+// 160 PCR iterations of a frame run at on-chip bandwidth.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "ss_device.cuh"
+
+namespace cg = cooperative_groups;
+
+#define CL_THREADS 512
+#define CL_MAXC 16
+
+// contrib families (gather entry bits 23..25)
+enum { CF_TET = 0, CF_DIST = 1, CF_ATT = 2, CF_HINGE = 3, CF_SLOT = 4 };
+
+struct ClPlan {
+  int C;                                    // CTAs per cluster
+  int MT, MD, MA, MH, MS, MP, MB, MW;       // per-CTA maxima of each family / node kind
+                                            // (MW: wheel slots, the first local slots)
+  int NR, ME, MN, MDOFX, MIN;               // rows, elements, owned nodes, owned+halo DOFs, inbox
+  // shared-memory offsets (doubles)
+  int oX, oR, oZ, oP, oAP, oAZ, oD;         // row vectors [NR]
+  int oJR, oJS, oJK;                        // compact tet J [9][MT] [6][MT] [6][MT]
+  int oIn;                                  // inbox: per owned node, one 3/6-vector per incidence
+  int oDir, oRw, oHJ, oWJ;                  // [3][MD] [3][MA] [60][MH] [18][MW]
+  int oPres, oGap, oLc, oAct, oDyn, oBdn, oBdf;  // slots [MS] ... lamc [3][MS], bdf [2][MS]
+  int oResD, oResA, oResH;                  // [MD] [3][MA] [5][MH]
+  int oU, oV, oAng;                         // [MDOFX] (owned then halo DOFs) x2, [9][MB]
+  int oRed;                                 // reduction partials [16][C]
+  int smem_doubles;
+  long long* dbg;      // optional phase timestamps (nullptr = off)
+  const int* cnt;      // [C][8]: nT nD nA nH nS nP nB -
+  const int* elem;     // [C][ME]    family-local global index of each local element
+  const int* eref;     // [C][ME][4] local U/V offsets of the element's nodes
+  const int* dest;     // [C][ME][4] inbox destinations: owner << 24 | inbox offset
+  const int* node;     // [C][MN]    global node of each owned node: particle id, or P + body
+  const int* in_ptr;   // [C][MN+1]  inbox offset of each owned node's first incidence
+  const int* hp_ptr;   // [C][MN+1]  halo pushes of each owned node
+  const int* hpush;    // consumer << 24 | consumer U/V offset
+};
+
+struct ClSmem {
+  double* b;             // this CTA's shared memory base
+  double* const* peer;   // shared-memory table of every CTA's base (incl. self)
+};
+
+// fixed-order block sum over CL_THREADS threads (warp shuffles down, then
+// the 16 warp sums in warp order); result valid in every thread
+DI double cl_block_sum(double v, double* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (CL_THREADS >> 5) ? scratch[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) scratch[32] = s;
+  }
+  __syncthreads();
+  return scratch[32];
+}
+
+// cluster-wide deterministic sum: block sum, pushed by thread 0 into slot
+// `slot` of every CTA (DSMEM stores), cluster barrier, then the C partials
+// are added in rank order by one fixed shuffle tree (same result in every
+// CTA). Slots rotate over 16, so a slot is rewritten only 15 barriers later.
+DI double cl_cluster_sum(const ClPlan& L, const ClSmem& S, double v, int slot, double* scratch) {
+  const double bs = cl_block_sum(v, scratch);
+  const int rank = (int)cg::this_cluster().block_rank();
+  if (threadIdx.x < L.C) S.peer[threadIdx.x][L.oRed + slot * L.C + rank] = bs;
+  cg::this_cluster().sync();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < L.C ? S.b[L.oRed + slot * L.C + threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) scratch[33] = t;
+  }
+  __syncthreads();
+  return scratch[33];
+}
+
+// ------------------------------------------------------------ node gather
+// Per-thread owned-node state (a thread owns at most one node): inbox range,
+// halo push range, inverse mass, body index, local DOF base.
+struct ClMn {
+  int k0, k1, hp0, hp1, gb, base;
+  double im;
+};
+
+// For the owned node: w = sum of its inbox (the incidences' column sums,
+// stored there by the element owners in the reference accumulation order),
+// u = M^-1 w (numba_backend.py:68-82); mode 0: U = u, mode 1: V += u; then
+// the new value is pushed into every consumer CTA's halo copy.
+DI void cl_gather(const ClPlan& L, const ClSmem& S, bool has_node, const ClMn& mn, int mode) {
+  if (!has_node) return;
+  double* sb = S.b;
+  const int arr = mode == 0 ? L.oU : L.oV;
+  double out[6];
+  int nd;
+  if (mn.gb < 0) {
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+    for (int k = mn.k0; k < mn.k1; k += 3) {
+      w0 += sb[k];
+      w1 += sb[k + 1];
+      w2 += sb[k + 2];
+    }
+    out[0] = mn.im * w0;
+    out[1] = mn.im * w1;
+    out[2] = mn.im * w2;
+    nd = 3;
+  } else {
+    const int lb = mn.gb;  // local body slot (ang_inv column)
+    double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = mn.k0; k < mn.k1; k += 6) {
+#pragma unroll
+      for (int kk = 0; kk < 6; ++kk) w[kk] += sb[k + kk];
+    }
+    const double* A = sb + L.oAng;
+    const int MB = L.MB;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[a] = mn.im * w[a];
+    out[3] = A[0 * MB + lb] * w[3] + A[1 * MB + lb] * w[4] + A[2 * MB + lb] * w[5];
+    out[4] = A[3 * MB + lb] * w[3] + A[4 * MB + lb] * w[4] + A[5 * MB + lb] * w[5];
+    out[5] = A[6 * MB + lb] * w[3] + A[7 * MB + lb] * w[4] + A[8 * MB + lb] * w[5];
+    nd = 6;
+  }
+  double* dst = sb + arr + mn.base;
+  for (int k = 0; k < nd; ++k) {
+    const double val = mode == 0 ? out[k] : dst[k] + out[k];
+    dst[k] = val;
+    out[k] = val;
+  }
+  for (int q = mn.hp0; q < mn.hp1; ++q) {
+    const int hp = L.hpush[q];
+    double* rem = S.peer[(unsigned)hp >> 24] + arr + (hp & 0xFFFFFF);
+    for (int k = 0; k < nd; ++k) rem[k] = out[k];
+  }
+}
+
+// push n values to an inbox destination (owner << 24 | offset), negated if neg
+DI void cl_put(const ClSmem& S, const ClPlan& L, int dst, const double* v, int n, bool neg = false) {
+  double* p = S.peer[(unsigned)dst >> 24] + L.oIn + (dst & 0xFFFFFF);
+  for (int k = 0; k < n; ++k) p[k] = neg ? -v[k] : v[k];
+}
+
+// row index of family-local row i of local element le
+DI int cl_row_t(const ClPlan& L, int i, int le) { return i * L.MT + le; }
+DI int cl_row_d(const ClPlan& L, int le) { return 6 * L.MT + le; }
+DI int cl_row_a(const ClPlan& L, int i, int le) { return 6 * L.MT + L.MD + i * L.MA + le; }
+DI int cl_row_h(const ClPlan& L, int i, int le) { return 6 * L.MT + L.MD + 3 * L.MA + i * L.MH + le; }
+DI int cl_row_s(const ClPlan& L, int k, int le) {
+  return 6 * L.MT + L.MD + 3 * L.MA + 5 * L.MH + k * L.MS + le;
+}
+
+// node DOF values of an element (local U/V copy: owned or halo)
+DI const double* cl_dofp(const ClSmem& S, int ref, int arr) { return S.b + arr + ref; }
+
+// local tet compact J from shared memory
+DI void cl_tet_load(const ClPlan& L, const double* sb, int lt, TetC& T) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) T.R[k] = sb[L.oJR + k * L.MT + lt];
+  double s[6], q[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    s[k] = sb[L.oJS + k * L.MT + lt];
+    q[k] = sb[L.oJK + k * L.MT + lt];
+  }
+  T.S[0] = s[0]; T.S[4] = s[1]; T.S[8] = s[2];
+  T.S[5] = s[3]; T.S[7] = s[3];
+  T.S[2] = s[4]; T.S[6] = s[4];
+  T.S[1] = s[5]; T.S[3] = s[5];
+  T.K[0] = q[0]; T.K[4] = q[1]; T.K[8] = q[2];
+  T.K[5] = q[3]; T.K[7] = q[3];
+  T.K[2] = q[4]; T.K[6] = q[4];
+  T.K[1] = q[5]; T.K[3] = q[5];
+}
+
+// J^T x of one tet into its 12 column sums (structured or materialised)
+template <bool EXACT>
+DI void cl_tet_jt(const TetC& T, const double* Ri, const double* x6, double* col12) {
+  if (EXACT) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      double wv[3];
+      tet_wv(Ri, v, wv);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double col[6];
+        tet_col(T, wv, a, col);
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) acc += col[i] * x6[i];
+        col12[3 * v + a] = acc;
+      }
+    }
+  } else {
+    const double* S_ = T.S;
+    const double* Ki = T.K;
+    const double* R = T.R;
+    const double Z00 = x6[0], Z11 = x6[1], Z22 = x6[2];
+    const double Z12 = 0.5 * x6[3], Z02 = 0.5 * x6[4], Z01 = 0.5 * x6[5];
+    const double N21 = Z02 * S_[1] + Z12 * S_[4] + Z22 * S_[7];
+    const double N12 = Z01 * S_[2] + Z11 * S_[5] + Z12 * S_[8];
+    const double N02 = Z00 * S_[2] + Z01 * S_[5] + Z02 * S_[8];
+    const double N20 = Z02 * S_[0] + Z12 * S_[3] + Z22 * S_[6];
+    const double N10 = Z01 * S_[0] + Z11 * S_[3] + Z12 * S_[6];
+    const double N01 = Z00 * S_[1] + Z01 * S_[4] + Z02 * S_[7];
+    const double m0 = N21 - N12, m1 = N02 - N20, m2 = N10 - N01;
+    const double n0 = Ki[0] * m0 + Ki[1] * m1 + Ki[2] * m2;
+    const double n1 = Ki[3] * m0 + Ki[4] * m1 + Ki[5] * m2;
+    const double n2 = Ki[6] * m0 + Ki[7] * m1 + Ki[8] * m2;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      double wv[3];
+      tet_wv(Ri, v, wv);
+      const double q0 = (Z00 * wv[0] + Z01 * wv[1] + Z02 * wv[2]) - (n1 * wv[2] - n2 * wv[1]);
+      const double q1 = (Z01 * wv[0] + Z11 * wv[1] + Z12 * wv[2]) - (n2 * wv[0] - n0 * wv[2]);
+      const double q2 = (Z02 * wv[0] + Z12 * wv[1] + Z22 * wv[2]) - (n0 * wv[1] - n1 * wv[0]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) col12[3 * v + a] = R[3 * a] * q0 + R[3 * a + 1] * q1 + R[3 * a + 2] * q2;
+    }
+  }
+}
+
+// J u of one tet (u: 4 nodes x 3 gathered through the element refs)
+template <bool EXACT>
+DI void cl_tet_j(const TetC& T, const double* Ri, const double* uu, double* y) {
+  if (EXACT) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) y[i] = 0.0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      double wv[3];
+      tet_wv(Ri, v, wv);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double col[6];
+        tet_col(T, wv, a, col);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) y[i] += col[i] * uu[3 * v + a];
+      }
+    }
+    return;
+  }
+  const double* R = T.R;
+  const double* S_ = T.S;
+  const double* Ki = T.K;
+  double du[9];
+#pragma unroll
+  for (int v = 1; v < 4; ++v)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) du[3 * (v - 1) + a] = uu[3 * v + a] - uu[a];
+  double Lm[9], G[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      Lm[3 * a + j] = du[a] * Ri[j] + du[3 + a] * Ri[3 + j] + du[6 + a] * Ri[6 + j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) G[3 * i + j] = R[i] * Lm[j] + R[3 + i] * Lm[3 + j] + R[6 + i] * Lm[6 + j];
+  const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
+  const double w0 = Ki[0] * g0 + Ki[1] * g1 + Ki[2] * g2;
+  const double w1 = Ki[3] * g0 + Ki[4] * g1 + Ki[5] * g2;
+  const double w2 = Ki[6] * g0 + Ki[7] * g1 + Ki[8] * g2;
+  const double ws00 = -w2 * S_[3] + w1 * S_[6];
+  const double ws01 = -w2 * S_[4] + w1 * S_[7];
+  const double ws02 = -w2 * S_[5] + w1 * S_[8];
+  const double ws10 = w2 * S_[0] - w0 * S_[6];
+  const double ws11 = w2 * S_[1] - w0 * S_[7];
+  const double ws12 = w2 * S_[2] - w0 * S_[8];
+  const double ws20 = -w1 * S_[0] + w0 * S_[3];
+  const double ws21 = -w1 * S_[1] + w0 * S_[4];
+  const double ws22 = -w1 * S_[2] + w0 * S_[5];
+  y[0] = G[0] - ws00;
+  y[1] = G[4] - ws11;
+  y[2] = G[8] - ws22;
+  y[3] = 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21);
+  y[4] = 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20);
+  y[5] = 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10);
+}
+
+// ---------------------------------------------------------------- family
+// Element enumeration of a CTA: [tets][dist][attach][hinge][slots].
+struct ClEl {
+  int fam, le, g;  // family, family-local index, global index
+};
+// Per-thread element state, loaded once per kernel (a thread owns at most
+// one element for the whole solve): identity, node offsets, inbox
+// destinations, and the tet's rest-shape inverse and E_tet scalars.
+struct ClMe {
+  ClEl el;
+  int ref[4], dst[4];
+  double dyn;  // compliance term of distance / attachment / hinge rows
+};
+DI ClEl cl_el(const ClPlan& L, int rank, int e) {
+  const int* cnt = L.cnt + 8 * rank;
+  ClEl r;
+  r.g = L.elem[(size_t)rank * L.ME + e];
+  int b = 0;
+  if (e < (b += cnt[0])) { r.fam = CF_TET; r.le = e; return r; }
+  if (e < (b + cnt[1])) { r.fam = CF_DIST; r.le = e - b; return r; }
+  b += cnt[1];
+  if (e < (b + cnt[2])) { r.fam = CF_ATT; r.le = e - b; return r; }
+  b += cnt[2];
+  if (e < (b + cnt[3])) { r.fam = CF_HINGE; r.le = e - b; return r; }
+  b += cnt[3];
+  r.fam = CF_SLOT;
+  r.le = e - b;
+  return r;
+}
+DI int cl_nel(const ClPlan& L, int rank) {
+  const int* cnt = L.cnt + 8 * rank;
+  return cnt[0] + cnt[1] + cnt[2] + cnt[3] + cnt[4];
+}
+
+// rows of a local element (up to 6) and whether they are live (absent
+// contact slots have no rows)
+DI int cl_rows(const ClPlan& L, const double* sb, const ClEl& el, int* rows) {
+  switch (el.fam) {
+    case CF_TET:
+#pragma unroll
+      for (int i = 0; i < 6; ++i) rows[i] = cl_row_t(L, i, el.le);
+      return 6;
+    case CF_DIST:
+      rows[0] = cl_row_d(L, el.le);
+      return 1;
+    case CF_ATT:
+#pragma unroll
+      for (int i = 0; i < 3; ++i) rows[i] = cl_row_a(L, i, el.le);
+      return 3;
+    case CF_HINGE:
+#pragma unroll
+      for (int i = 0; i < 5; ++i) rows[i] = cl_row_h(L, i, el.le);
+      return 5;
+    default:
+      if (sb[L.oPres + el.le] == 0.0) return 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) rows[k] = cl_row_s(L, k, el.le);
+      return 3;
+  }
+}
+
+// Column sums J^T x of one element (per-row values xr[]) pushed to the
+// inbox slots of its nodes. mode 0: apply_a masking (inactive friction ->
+// 0); mode 1: impulse (present contacts, all rows). Absent slots push zeros.
+template <bool EXACT>
+DI void cl_contrib(const Ctx& c, const ClPlan& L, const ClSmem& S, const ClMe& me,
+                   const double* xr, int mode) {
+  const double* sb = S.b;
+  const ClEl& el = me.el;
+  const int* dst = me.dst;
+  switch (el.fam) {
+    case CF_TET: {
+      TetC T;
+      double col12[12], Ri[9];
+      cl_tet_load(L, sb, el.le, T);
+      tet_rinv(c, el.g, Ri);
+      cl_tet_jt<EXACT>(T, Ri, xr, col12);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cl_put(S, L, dst[v], col12 + 3 * v, 3);
+      break;
+    }
+    case CF_DIST: {
+      // +dir on the first particle, -dir on the second ((-d)*x == -(d*x))
+      double a[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) a[k] = 0.0 + sb[L.oDir + k * L.MD + el.le] * xr[0];
+      cl_put(S, L, dst[0], a, 3);
+      cl_put(S, L, dst[1], a, 3, true);
+      break;
+    }
+    case CF_ATT: {
+      double rw[3], col[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) rw[i] = sb[L.oRw + i * L.MA + el.le];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) acc += att_val(i, j, rw) * xr[i];
+        col[j] = acc;
+      }
+      cl_put(S, L, dst[0], col, 3);
+      cl_put(S, L, dst[1], col + 3, 6);
+      break;
+    }
+    case CF_HINGE: {
+      double col[12];
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) acc += sb[L.oHJ + (12 * i + j) * L.MH + el.le] * xr[i];
+        col[j] = acc;
+      }
+      cl_put(S, L, dst[0], col, 6);
+      cl_put(S, L, dst[1], col + 6, 6);
+      break;
+    }
+    default: {
+      const int ls = el.le;
+      const bool pres = sb[L.oPres + ls] != 0.0;
+      const bool fon = mode == 0 ? sb[L.oAct + ls] != 0.0 : true;
+      const bool wheel = el.g < c.D.nw;
+      double nv[6], f0[6], f1[6];
+      if (wheel) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          nv[k] = sb[L.oWJ + k * L.MW + ls];
+          f0[k] = sb[L.oWJ + (6 + k) * L.MW + ls];
+          f1[k] = sb[L.oWJ + (12 + k) * L.MW + ls];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) { nv[k] = 0.0; f0[k] = 0.0; f1[k] = 0.0; }
+        nv[2] = 1.0;
+        f0[0] = 1.0;
+        f1[1] = 1.0;
+      }
+      double cn[6], cf[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        cn[k] = pres ? 0.0 + nv[k] * xr[0] : 0.0;
+        cf[k] = 0.0;
+        if (pres && fon) {
+          cf[k] = 0.0 + f0[k] * xr[1];
+          cf[k] += f1[k] * xr[2];
+        }
+      }
+      const int nd = wheel ? 6 : 3;
+      cl_put(S, L, dst[0], cn, nd);
+      cl_put(S, L, dst[1], cf, nd);
+      break;
+    }
+  }
+}
+
+// J y rows of one element for a node vector at shared offset `arr` (U or V)
+template <bool EXACT>
+DI int cl_forward(const Ctx& c, const ClPlan& L, const ClSmem& S, const ClMe& me, int arr,
+                  double* y) {
+  const ClEl& el = me.el;
+  const int* ref = me.ref;
+  const double* sb = S.b;
+  switch (el.fam) {
+    case CF_TET: {
+      double uu[12];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const double* p = cl_dofp(S, ref[v], arr);
+        uu[3 * v] = p[0];
+        uu[3 * v + 1] = p[1];
+        uu[3 * v + 2] = p[2];
+      }
+      TetC T;
+      double Ri[9];
+      cl_tet_load(L, sb, el.le, T);
+      tet_rinv(c, el.g, Ri);
+      cl_tet_j<EXACT>(T, Ri, uu, y);
+      return 6;
+    }
+    case CF_DIST: {
+      const double* pi = cl_dofp(S, ref[0], arr);
+      const double* pj = cl_dofp(S, ref[1], arr);
+      const double u0 = sb[L.oDir + el.le], u1 = sb[L.oDir + L.MD + el.le],
+                   u2 = sb[L.oDir + 2 * L.MD + el.le];
+      double acc = 0.0;
+      acc += u0 * pi[0];
+      acc += u1 * pi[1];
+      acc += u2 * pi[2];
+      acc += -u0 * pj[0];
+      acc += -u1 * pj[1];
+      acc += -u2 * pj[2];
+      y[0] = acc;
+      return 1;
+    }
+    case CF_ATT: {
+      const double* pp = cl_dofp(S, ref[0], arr);
+      const double* pb = cl_dofp(S, ref[1], arr);
+      double uu[9], rw[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        uu[k] = pp[k];
+        rw[k] = sb[L.oRw + k * L.MA + el.le];
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) uu[3 + k] = pb[k];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) acc += att_val(i, j, rw) * uu[j];
+        y[i] = acc;
+      }
+      return 3;
+    }
+    case CF_HINGE: {
+      const double* pa = cl_dofp(S, ref[0], arr);
+      const double* pb = cl_dofp(S, ref[1], arr);
+      double uu[12];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        uu[k] = pa[k];
+        uu[6 + k] = pb[k];
+      }
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 12; ++j) acc += sb[L.oHJ + (12 * i + j) * L.MH + el.le] * uu[j];
+        y[i] = acc;
+      }
+      return 5;
+    }
+    default: {
+      const int ls = el.le;
+      if (sb[L.oPres + ls] == 0.0) return 0;
+      const double* p = cl_dofp(S, ref[0], arr);
+      if (el.g < c.D.nw) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) acc += sb[L.oWJ + (6 * r + k) * L.MW + ls] * p[k];
+          y[r] = acc;
+        }
+      } else {
+        // padded columns reference DOF 0 (contact.py:210-214): particle 0's x
+        const double* p0 = cl_dofp(S, ref[1], arr);
+        const double x0 = p[0], x1 = p[1], x2 = p[2], z0 = p0[0];
+        double a = 0.0;
+        a += 0.0 * x0; a += 0.0 * x1; a += 1.0 * x2; a += 0.0 * z0; a += 0.0 * z0; a += 0.0 * z0;
+        y[0] = a;
+        a = 0.0;
+        a += 1.0 * x0; a += 0.0 * x1; a += 0.0 * x2; a += 0.0 * z0; a += 0.0 * z0; a += 0.0 * z0;
+        y[1] = a;
+        a = 0.0;
+        a += 0.0 * x0; a += 1.0 * x1; a += 0.0 * x2; a += 0.0 * z0; a += 0.0 * z0; a += 0.0 * z0;
+        y[2] = a;
+      }
+      return 3;
+    }
+  }
+}
+
+// global static-row index of row i of element el (internal row layout)
+DI int cl_grow(const Ctx& c, const ClEl& el, int i) {
+  switch (el.fam) {
+    case CF_TET: return c.D.ot + i * c.D.nt + el.g;
+    case CF_DIST: return c.D.od + el.g;
+    case CF_ATT: return c.D.oa + i * c.D.na + el.g;
+    default: return c.D.oh + i * c.D.nh + el.g;
+  }
+}
+
+// ===================================================================
+// The Newton loop of one substep for one environment per cluster:
+// grid.x = C * E, cluster (C,1,1), CL_THREADS threads, dynamic smem.
+// Reads the eval/contact outputs of this substep from global memory,
+// writes back velocities, multipliers, warm starts and the residual.
+#define CL_STAMP(id)                                                                    \
+  do {                                                                                  \
+    if (L.dbg && blockIdx.x == 0 && threadIdx.x == 0 && itn == 1 && k == 3)             \
+      L.dbg[id] = clock64();                                                            \
+  } while (0)
+
+template <bool EXACT>
+__global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, const ClPlan L) {
+  extern __shared__ __align__(16) double sm_[];
+  __shared__ double scratch[40];
+  __shared__ double* peers[CL_MAXC];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int env = blockIdx.x / L.C;
+  const int E = c.D.E;
+  if (threadIdx.x < L.C) peers[threadIdx.x] = cl.map_shared_rank(sm_, (int)threadIdx.x);
+  __syncthreads();
+  ClSmem S;
+  S.b = sm_;
+  S.peer = peers;
+  double* sb = sm_;
+  const int* cnt = L.cnt + 8 * rank;
+  const int nEl = cl_nel(L, rank);
+  const int nP = cnt[5], nB = cnt[6];
+  const double g = c.p.gamma, h = c.p.h;
+  // per-thread element and node state for the whole solve
+  const bool has_el = (int)threadIdx.x < nEl;
+  ClMe me;
+  if (has_el) {
+    const int e = threadIdx.x;
+    me.el = cl_el(L, rank, e);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      me.ref[q] = L.eref[((size_t)rank * L.ME + e) * 4 + q];
+      me.dst[q] = L.dest[((size_t)rank * L.ME + e) * 4 + q];
+    }
+    me.dyn = 0.0;
+    if (me.el.fam == CF_DIST) me.dyn = c.T.d_dyn[me.el.g];
+    else if (me.el.fam == CF_ATT) me.dyn = c.T.a_dyn[me.el.g];
+    else if (me.el.fam == CF_HINGE) me.dyn = c.T.h_dyn[me.el.g];
+  }
+  const bool has_node = (int)threadIdx.x < nP + nB;
+  ClMn mn;
+  if (has_node) {
+    const int n = threadIdx.x;
+    const int* iptr = L.in_ptr + (size_t)rank * (L.MN + 1);
+    const int* hptr = L.hp_ptr + (size_t)rank * (L.MN + 1);
+    mn.k0 = L.oIn + iptr[n];
+    mn.k1 = L.oIn + iptr[n + 1];
+    mn.hp0 = hptr[n];
+    mn.hp1 = hptr[n + 1];
+    const int gn = L.node[(size_t)rank * L.MN + n];
+    if (n < nP) {
+      mn.gb = -1;
+      mn.im = c.T.inv_mass[gn];
+      mn.base = 3 * n;
+    } else {
+      mn.gb = n - nP;  // local body slot (ang_inv column)
+      mn.im = c.T.body_inv_mass[gn - c.D.P];
+      mn.base = 3 * nP + 6 * (n - nP);
+    }
+  }
+
+  // ---- load substep inputs into shared memory
+  if (has_el) {
+    const ClEl& el = me.el;
+    int rows[6];
+    switch (el.fam) {
+      case CF_TET: {
+        const int nt = c.D.nt, t = el.g;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) sb[L.oJR + k * L.MT + el.le] = c.K.tR[IX(k * nt + t)];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          sb[L.oJS + k * L.MT + el.le] = c.K.tS[IX(k * nt + t)];
+          sb[L.oJK + k * L.MT + el.le] = c.K.tK[IX(k * nt + t)];
+        }
+        break;
+      }
+      case CF_DIST:
+#pragma unroll
+        for (int a = 0; a < 3; ++a) sb[L.oDir + a * L.MD + el.le] = c.S.dirs[IX(a * c.D.nd + el.g)];
+        sb[L.oResD + el.le] = c.K.res[IX(c.D.od + el.g)];
+        break;
+      case CF_ATT:
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          sb[L.oRw + i * L.MA + el.le] = c.K.rw[IX(i * c.D.na + el.g)];
+          sb[L.oResA + i * L.MA + el.le] = c.K.res[IX(c.D.oa + i * c.D.na + el.g)];
+        }
+        break;
+      case CF_HINGE:
+        for (int k = 0; k < 60; ++k) sb[L.oHJ + k * L.MH + el.le] = c.K.hJ[IX((size_t)k * c.D.nh + el.g)];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) sb[L.oResH + i * L.MH + el.le] = c.K.res[IX(c.D.oh + i * c.D.nh + el.g)];
+        break;
+      default: {
+        const int s = el.g, ls = el.le, ns = c.D.ns;
+        sb[L.oPres + ls] = c.K.present[IX(s)] ? 1.0 : 0.0;
+        sb[L.oGap + ls] = c.K.gap[IX(s)];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) sb[L.oLc + k * L.MS + ls] = c.K.lamc[IX(k * ns + s)];
+        sb[L.oBdn + ls] = c.K.bdiag[IX(c.D.on + s)];
+        sb[L.oBdf + ls] = c.K.bdiag[IX(c.D.of + s)];
+        sb[L.oBdf + L.MS + ls] = c.K.bdiag[IX(c.D.of + ns + s)];
+        if (s < c.D.nw)
+          for (int k = 0; k < 18; ++k) sb[L.oWJ + k * L.MW + ls] = c.K.wJ[IX((size_t)k * c.D.nw + s)];
+        break;
+      }
+    }
+    (void)rows;
+  }
+  for (int n = threadIdx.x; n < nP + nB; n += blockDim.x) {
+    const int gn = L.node[(size_t)rank * L.MN + n];
+    if (n < nP) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) sb[L.oV + 3 * n + a] = c.K.v[IX(3 * gn + a)];
+    } else {
+      const int lb = n - nP, gb = gn - c.D.P, o = c.D.bd0 + 6 * gb;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sb[L.oV + 3 * nP + 6 * lb + k] = c.K.v[IX(o + k)];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) sb[L.oAng + k * L.MB + lb] = c.K.ang_inv[IX((size_t)k * c.D.nb + gb)];
+    }
+  }
+  __syncthreads();
+  // halo copies of V: the loads above wrote owned DOFs; also fill halos
+  // directly from global memory (same values the owners hold)
+  {
+    const int* hptr = L.hp_ptr + (size_t)rank * (L.MN + 1);
+    for (int n = threadIdx.x; n < nP + nB; n += blockDim.x) {
+      const int nd = n < nP ? 3 : 6, base = n < nP ? 3 * n : 3 * nP + 6 * (n - nP);
+      for (int q = hptr[n]; q < hptr[n + 1]; ++q) {
+        const int hp = L.hpush[q];
+        double* rem = S.peer[(unsigned)hp >> 24] + L.oV + (hp & 0xFFFFFF);
+        for (int k = 0; k < nd; ++k) rem[k] = sb[L.oV + base + k];
+      }
+    }
+  }
+
+  // ---- initial impulse v = vt + M^-1 J^T lam (solver.py:428-436)
+  if (has_el) {
+    const ClEl& el = me.el;
+    double xr[6];
+    if (el.fam == CF_SLOT) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) xr[k] = sb[L.oLc + k * L.MS + el.le];
+    } else {
+      const int nr = el.fam == CF_TET ? 6 : el.fam == CF_DIST ? 1 : el.fam == CF_ATT ? 3 : 5;
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+        if (i < nr) xr[i] = c.S.lam[IX(cl_grow(c, el, i))];
+    }
+    cl_contrib<EXACT>(c, L, S, me, xr, 1);
+  }
+  cl.sync();
+  cl_gather(L, S, has_node, mn, 1);
+  cl.sync();
+
+  int rslot = 0;  // rotating reduction slot (16 slots: a slot is rewritten only
+                  // after 15 further cluster barriers, long after its readers)
+  double resid = 0.0;
+  for (int itn = 0; itn < c.p.newton; ++itn) {
+    const bool lastn = itn == c.p.newton - 1;
+    // ---- rhs, FB, active set, diagonal; x = 0, r, z = r/d; J^T z
+    if (has_el) {
+      const ClEl& el = me.el;
+      int rows[6];
+      const int nr = cl_rows(L, sb, el, rows);
+      double jv[6];
+      cl_forward<EXACT>(c, L, S, me, L.oV, jv);
+      double zr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (el.fam == CF_TET) {
+        TetC T;
+        cl_tet_load(L, sb, el.le, T);
+        double rs[6], lm[6], el6[6];
+        tet_res(T, rs);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[IX(cl_grow(c, el, i))];
+        ereg6(c.T.t_e3[el.g], c.T.t_e3[c.D.nt + el.g], c.T.t_e3[2 * c.D.nt + el.g], lm, el6);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double dg = npmax(c.K.bdiag[IX(cl_grow(c, el, i))] + 0.0, 1e-30);
+          const double d = dg > 1e-300 ? dg : 1.0;
+          const double r = -(g * rs[i] / h + jv[i] + el6[i]);
+          sb[L.oR + rows[i]] = r;
+          sb[L.oD + rows[i]] = d;
+          sb[L.oX + rows[i]] = 0.0;
+          zr[i] = r / d;
+          sb[L.oZ + rows[i]] = zr[i];
+        }
+      } else if (el.fam != CF_SLOT) {
+        const double dyn = me.dyn;
+        for (int i = 0; i < nr; ++i) {
+          const int gr = cl_grow(c, el, i);
+          const double res = el.fam == CF_DIST ? sb[L.oResD + el.le]
+                           : el.fam == CF_ATT ? sb[L.oResA + i * L.MA + el.le]
+                                              : sb[L.oResH + i * L.MH + el.le];
+          const double dg = npmax(c.K.bdiag[IX(gr)] + dyn, 1e-30);
+          const double d = dg > 1e-300 ? dg : 1.0;
+          const double r = -(g * res / h + jv[i] + dyn * c.S.lam[IX(gr)]);
+          sb[L.oR + rows[i]] = r;
+          sb[L.oD + rows[i]] = d;
+          sb[L.oX + rows[i]] = 0.0;
+          zr[i] = r / d;
+          sb[L.oZ + rows[i]] = zr[i];
+        }
+      } else if (nr) {
+        const int ls = el.le;
+        const double ln = sb[L.oLc + ls];
+        const double a = sb[L.oGap + ls] / h + jv[0];
+        const double b = ln;
+        const double root = sqrt(a * a + b * b + c.p.fb_delta);
+        const double phi = a + b - root;
+        double da = 1.0 - a / root;
+        const double db = 1.0 - b / root;
+        if (da < c.p.smin) da = c.p.smin;
+        else if (da > c.p.smax) da = c.p.smax;
+        const double dynn = db / da;
+        sb[L.oDyn + ls] = dynn;
+        const double on = (c.p.mu * npmax(ln, 0.0) > 0.0) ? 1.0 : 0.0;
+        sb[L.oAct + ls] = on;
+        const double fd = c.p.fdyn;
+        double rr[3], dd[3];
+        rr[0] = -phi / da;
+        {
+          const double dg = npmax(sb[L.oBdn + ls] + dynn, 1e-30);
+          dd[0] = dg > 1e-300 ? dg : 1.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          rr[1 + k] = -on * (jv[1 + k] + fd * sb[L.oLc + (1 + k) * L.MS + ls]);
+          const double dg = on > 0.0 ? npmax(sb[L.oBdf + k * L.MS + ls] + fd, 1e-30) : 1.0;
+          dd[1 + k] = dg > 1e-300 ? dg : 1.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          sb[L.oR + rows[k]] = rr[k];
+          sb[L.oD + rows[k]] = dd[k];
+          sb[L.oX + rows[k]] = 0.0;
+          zr[k] = rr[k] / dd[k];
+          sb[L.oZ + rows[k]] = zr[k];
+        }
+      } else {
+        sb[L.oAct + el.le] = 0.0;
+      }
+      cl_contrib<EXACT>(c, L, S, me, zr, 0);
+    }
+    bool broken = false;
+    double rho = 0.0, alpha = 0.0, beta = 0.0;
+    for (int k = 0; k <= c.p.pcr; ++k) {
+      const bool setup = k == 0;
+      CL_STAMP(0);
+      if (k > 0 && c.p.pcr > 0) {
+        // x += alpha p, r -= alpha ap, z = r/d, then J^T z (k < pcr), or the
+        // Newton update (k == pcr)
+        if (k < c.p.pcr) {
+          if (!broken) {
+            if (has_el) {
+              const ClEl& el = me.el;
+              int rows[6];
+              const int nr = cl_rows(L, sb, el, rows);
+              double zr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+              for (int q = 0; q < nr; ++q) {
+                const int o = rows[q];
+                sb[L.oX + o] += alpha * sb[L.oP + o];
+                const double r = sb[L.oR + o] - alpha * sb[L.oAP + o];
+                sb[L.oR + o] = r;
+                zr[q] = r / sb[L.oD + o];
+                sb[L.oZ + o] = zr[q];
+              }
+              cl_contrib<EXACT>(c, L, S, me, zr, 0);
+            }
+          }
+        }
+      }
+      if (k == c.p.pcr) break;
+      if (!(k > 0 && broken)) {
+        CL_STAMP(1);
+        cl.sync();                               // column sums of J^T z visible
+        CL_STAMP(2);
+        cl_gather(L, S, has_node, mn, 0);        // U = M^-1 J^T z
+        CL_STAMP(3);
+        cl.sync();                               // U visible
+        CL_STAMP(4);
+      }
+      // az = J u + dyn z + E z; rho = z.az
+      double part = 0.0;
+      if (!broken) {
+        if (has_el) {
+          const ClEl& el = me.el;
+          int rows[6];
+          const int nr = cl_rows(L, sb, el, rows);
+          double y[6];
+          if (nr) cl_forward<EXACT>(c, L, S, me, L.oU, y);
+          if (!nr) {
+          } else if (el.fam == CF_TET) {
+            double zz[6], ez[6];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) zz[i] = sb[L.oZ + rows[i]];
+            ereg6(c.T.t_e3[el.g], c.T.t_e3[c.D.nt + el.g], c.T.t_e3[2 * c.D.nt + el.g], zz, ez);
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+              const double az = y[i] + ez[i];
+              sb[L.oAZ + rows[i]] = az;
+              part += zz[i] * az;
+            }
+          } else if (el.fam == CF_SLOT) {
+            const int ls = el.le;
+            const double zn = sb[L.oZ + rows[0]], z0 = sb[L.oZ + rows[1]], z1 = sb[L.oZ + rows[2]];
+            const double an = y[0] + sb[L.oDyn + ls] * zn;
+            double a0 = z0, a1 = z1;
+            if (sb[L.oAct + ls] != 0.0) {
+              a0 = y[1] + c.p.fdyn * z0;
+              a1 = y[2] + c.p.fdyn * z1;
+            }
+            sb[L.oAZ + rows[0]] = an;
+            sb[L.oAZ + rows[1]] = a0;
+            sb[L.oAZ + rows[2]] = a1;
+            part += zn * an;
+            part += z0 * a0;
+            part += z1 * a1;
+          } else {
+            const double dyn = me.dyn;
+            for (int i = 0; i < nr; ++i) {
+              const double zr = sb[L.oZ + rows[i]];
+              const double az = y[i] + dyn * zr;
+              sb[L.oAZ + rows[i]] = az;
+              part += zr * az;
+            }
+          }
+        }
+      }
+      CL_STAMP(5);
+      const double rho_new = cl_cluster_sum(L, S, part, rslot, scratch);
+      CL_STAMP(6);
+      rslot = (rslot + 1) & 15;
+      if (!broken) {
+        if (setup) {
+          rho = rho_new;
+        } else {
+          beta = rho > 1e-300 ? rho_new / rho : 0.0;
+          rho = rho_new;
+        }
+      }
+      // p = z + beta p, ap = az + beta ap; den = ap.(ap/d)
+      double dpart = 0.0;
+      if (has_el) {
+        const ClEl& el = me.el;
+        int rows[6];
+        const int nr = cl_rows(L, sb, el, rows);
+        for (int q = 0; q < nr; ++q) {
+          const int o = rows[q];
+          double ap;
+          if (setup) {
+            sb[L.oP + o] = sb[L.oZ + o];
+            ap = sb[L.oAZ + o];
+            sb[L.oAP + o] = ap;
+          } else if (!broken) {
+            sb[L.oP + o] = sb[L.oZ + o] + beta * sb[L.oP + o];
+            ap = sb[L.oAZ + o] + beta * sb[L.oAP + o];
+            sb[L.oAP + o] = ap;
+          } else {
+            ap = sb[L.oAP + o];
+          }
+          dpart += ap * (ap / sb[L.oD + o]);
+        }
+      }
+      CL_STAMP(7);
+      const double den = cl_cluster_sum(L, S, dpart, rslot, scratch);
+      CL_STAMP(8);
+      rslot = (rslot + 1) & 15;
+      if (!broken) {
+        if (den <= 1e-300 || !isfinite(den)) broken = true;
+        else alpha = rho / den;
+      }
+    }
+    // ---- last PCR step + multiplier update + projection + dlam column sums
+    double rzp = 0.0;
+    const bool step = c.p.pcr > 0 && !broken;
+    if (has_el) {
+      const ClEl& el = me.el;
+      int rows[6];
+      const int nr = cl_rows(L, sb, el, rows);
+      double dl[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int q = 0; q < nr; ++q) {
+        const int o = rows[q];
+        double x = sb[L.oX + o], r = sb[L.oR + o], z = sb[L.oZ + o];
+        if (step) {
+          x += alpha * sb[L.oP + o];
+          r -= alpha * sb[L.oAP + o];
+          z = r / sb[L.oD + o];
+        }
+        rzp += r * z;
+        dl[q] = x;
+      }
+      double dlam[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (el.fam != CF_SLOT) {
+        for (int q = 0; q < nr; ++q) {
+          const size_t gi = IX(cl_grow(c, el, q));
+          const double l0 = c.S.lam[gi];
+          const double l1 = l0 + dl[q];
+          c.S.lam[gi] = l1;
+          dlam[q] = l1 - l0;
+        }
+      } else {
+        const int ls = el.le, s = el.g;
+        double n1 = 0.0, a1 = 0.0, b1 = 0.0;
+        if (nr) {
+          const double n0 = sb[L.oLc + ls], a0 = sb[L.oLc + L.MS + ls], b0 = sb[L.oLc + 2 * L.MS + ls];
+          n1 = n0 + dl[0];
+          a1 = a0 + dl[1];
+          b1 = b0 + dl[2];
+          n1 = npmax(n1, 0.0);
+          const double rad = c.p.mu * npmax(n1, 0.0);
+          const double nrm = sqrt(a1 * a1 + b1 * b1);
+          if (nrm > rad) {
+            const double sc = nrm > 0.0 ? rad / nrm : 0.0;
+            a1 *= sc;
+            b1 *= sc;
+          }
+          sb[L.oLc + ls] = n1;
+          sb[L.oLc + L.MS + ls] = a1;
+          sb[L.oLc + 2 * L.MS + ls] = b1;
+          dlam[0] = n1 - n0;
+          dlam[1] = a1 - a0;
+          dlam[2] = b1 - b0;
+        }
+        if (lastn) {
+          const int ns = c.D.ns, nw = c.D.nw;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) c.K.lamc[IX(k * ns + s)] = sb[L.oLc + k * L.MS + ls];
+          if (s < nw) {
+            c.S.warm_valid[IX(s)] = nr ? 1 : 0;
+            c.S.warm[IX(s)] = n1;
+            c.S.warm[IX(nw + s)] = a1;
+            c.S.warm[IX(2 * nw + s)] = b1;
+          }
+        }
+      }
+      cl_contrib<EXACT>(c, L, S, me, dlam, 1);
+    }
+    const double rz = cl_cluster_sum(L, S, rzp, rslot, scratch);
+    rslot = (rslot + 1) & 15;
+    resid = sqrt(0.0 > rz ? 0.0 : rz);
+    // cl_cluster_sum ended with a cluster barrier: dlam column sums visible
+    cl_gather(L, S, has_node, mn, 1);  // v += M^-1 J^T dlam
+    cl.sync();
+  }
+
+  // ---- write back
+  for (int n = threadIdx.x; n < nP + nB; n += blockDim.x) {
+    const int gn = L.node[(size_t)rank * L.MN + n];
+    if (n < nP) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) c.K.v[IX(3 * gn + a)] = sb[L.oV + 3 * n + a];
+    } else {
+      const int lb = n - nP, o = c.D.bd0 + 6 * (gn - c.D.P);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) c.K.v[IX(o + k)] = sb[L.oV + 3 * nP + 6 * lb + k];
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0) c.K.resid[env] = resid;
+  cl.sync();  // no CTA may exit while peers can still read its shared memory
+}

@@ -43,6 +43,8 @@ class SolverConfig:
     # B200 extension: materialised-column tet Jacobian (bitwise numba sums)
     # instead of the structured chain-rule application (default)
     exact_jacobian: bool = False
+    # B200 extension: Newton-loop solver "auto" | "streaming" | "cluster"
+    solver: str = "auto"
 
     @property
     def h(self) -> float:
@@ -243,6 +245,13 @@ class BatchedSimulator:
     @property
     def stream(self) -> int:
         return int(_native.lib().ss_stream(self._ensure()) or 0)
+
+    @property
+    def solver_info(self) -> dict:
+        info = (C.c_int * 4)()
+        _native.check(_native.lib().ss_solver_info(self._ensure(), info))
+        return {"cluster": bool(info[0]), "cluster_size": info[1], "smem_bytes": info[2],
+                "env_lanes": info[3]}
 
     @property
     def launches_per_frame(self) -> int:

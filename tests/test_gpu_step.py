@@ -18,9 +18,10 @@ def built():
     g.build()
 
 
-def _sim(tag, n_envs=1, exact=False):
+def _sim(tag, n_envs=1, exact=False, solver="auto"):
     parts, cfg = scene_parts(tag)
     cfg.exact_jacobian = exact
+    cfg.solver = solver
     if n_envs == 1:
         return M.Simulator(config=cfg, **parts), parts, cfg
     return M.BatchedSimulator(n_envs, config=cfg, **parts), parts, cfg
@@ -30,11 +31,17 @@ def _one(a):
     return {k: v[0] for k, v in a.items()}
 
 
-@pytest.mark.parametrize("exact", [False, True], ids=["structuredJ", "exactJ"])
+SOLVERS = [(False, "streaming"), (True, "streaming"), (False, "cluster"), (True, "cluster")]
+SOLVER_IDS = ["structuredJ-streaming", "exactJ-streaming", "structuredJ-cluster",
+              "exactJ-cluster"]
+
+
+@pytest.mark.parametrize("exact,solver", SOLVERS, ids=SOLVER_IDS)
 @pytest.mark.parametrize("tag", ["B", "S"])
-def test_step_vs_reference_golden(tag, exact):
+def test_step_vs_reference_golden(tag, exact, solver):
     g = load_golden(f"step_{tag}.npz")
-    sim, _, _ = _sim(tag, exact=exact)
+    sim, _, _ = _sim(tag, exact=exact, solver=solver)
+    assert sim.solver_info["cluster"] == (solver == "cluster")
     for f in g["frames_captured"]:
         sim.set_state_arrays(golden_frame(g, f, "before"), 0, 1)
         st = sim.step(g[f"f{f}.commands"], latency=True)
@@ -46,11 +53,11 @@ def test_step_vs_reference_golden(tag, exact):
         assert st.residual == pytest.approx(float(g[f"f{f}.residual"]), rel=1e-8)
 
 
-@pytest.mark.parametrize("exact", [False, True], ids=["structuredJ", "exactJ"])
+@pytest.mark.parametrize("exact,solver", SOLVERS, ids=SOLVER_IDS)
 @pytest.mark.parametrize("tag", ["B", "S"])
-def test_step_vs_oracle(oracle_mod, tag, exact):
+def test_step_vs_oracle(oracle_mod, tag, exact, solver):
     g = load_golden(f"step_{tag}.npz")
-    sim, parts, cfg = _sim(tag, exact=exact)
+    sim, parts, cfg = _sim(tag, exact=exact, solver=solver)
     for f in g["frames_captured"]:
         before = golden_frame(g, f, "before")
         o = oracle_mod.OracleSim(config=cfg, **parts)
@@ -62,10 +69,11 @@ def test_step_vs_oracle(oracle_mod, tag, exact):
                            what=f"{tag} frame {f} vs oracle")
 
 
+@pytest.mark.parametrize("solver", ["streaming", "cluster"])
 @pytest.mark.parametrize("tag,frames", [("B", 50), ("S", 30)])
-def test_short_horizon_vs_reference(tag, frames):
+def test_short_horizon_vs_reference(tag, frames, solver):
     t = load_golden(f"traj_{tag}.npz")
-    sim, _, cfg = _sim(tag)
+    sim, _, cfg = _sim(tag, solver=solver)
     gait = M.GaitParams.from_scene(M.SceneConfig())
     for i in range(frames):
         cmd = np.array([8.0]) if tag == "B" else M.gait_commands(gait, i * cfg.dt, 4, 4)
@@ -78,11 +86,12 @@ def test_short_horizon_vs_reference(tag, frames):
             assert np.allclose(com, t[f"com{i + 1}"], rtol=1e-6, atol=1e-9)
 
 
-def test_batched_envs_match_oracle_per_env(oracle_mod):
+@pytest.mark.parametrize("solver", ["streaming", "cluster"])
+def test_batched_envs_match_oracle_per_env(oracle_mod, solver):
     """5 envs (padded to 8 lanes), each driven by different commands, each
     equal to its own single-env oracle run (envs are independent)."""
     n = 5
-    sim, parts, cfg = _sim("S", n)
+    sim, parts, cfg = _sim("S", n, solver=solver)
     rng = np.random.default_rng(20260817)
     bias = rng.uniform(-0.5, 0.5, n)
     ors = [oracle_mod.OracleSim(config=cfg, **parts) for _ in range(n)]
@@ -103,10 +112,11 @@ def test_batched_envs_match_oracle_per_env(oracle_mod):
     assert [s.contact_count for s in stats] == [o.stats().contact_count for o in ors]
 
 
-def test_run_to_run_bitwise_determinism():
+@pytest.mark.parametrize("solver", ["streaming", "cluster"])
+def test_run_to_run_bitwise_determinism(solver):
     outs = []
     for _ in range(2):
-        sim, _, cfg = _sim("S", 3)
+        sim, _, cfg = _sim("S", 3, solver=solver)
         for i in range(2):
             sim.step(np.tile(M.gait_commands(M.GaitParams(), i * cfg.dt, 4, 4), (3, 1)), True)
         outs.append(sim.get_state_arrays())
@@ -115,8 +125,9 @@ def test_run_to_run_bitwise_determinism():
         assert np.array_equal(outs[0][k], outs[1][k]), k
 
 
-def test_no_commands_and_latency_off(oracle_mod):
-    sim, parts, cfg = _sim("B")
+@pytest.mark.parametrize("solver", ["streaming", "cluster"])
+def test_no_commands_and_latency_off(oracle_mod, solver):
+    sim, parts, cfg = _sim("B", solver=solver)
     o = oracle_mod.OracleSim(config=cfg, **parts)
     sim.step(np.array([5.0]), latency=False)
     o.step(np.array([5.0]), False)
@@ -137,3 +148,20 @@ def test_simulator_drop_in_surface():
     assert sim.channels.pressures.max() > 0.0  # link 1 inflates at t=0 (sin(pi/2) = 1)
     assert np.isfinite(model.link_curvature(0)) and np.isfinite(model.center_of_mass()).all()
     assert sim.lam_tetra.shape == (4320, 6)
+
+
+def test_cluster_and_streaming_agree():
+    """Both Newton-loop solvers from the same state: same contacts, states
+    within the per-step tolerance (their dot-product trees differ)."""
+    outs = []
+    for solver in ("streaming", "cluster"):
+        sim, _, cfg = _sim("S", 4, solver=solver)
+        for i in range(2):
+            sim.step(np.tile(M.gait_commands(M.GaitParams(), i * cfg.dt, 4, 4), (4, 1)), True)
+        outs.append((sim.get_state_arrays(), [s.contact_count for s in sim.get_stats()]))
+    (a, ca), (b, cb) = outs
+    assert ca == cb
+    for e in range(4):
+        assert_state_close({k: v[e] for k, v in a.items()}, {k: v[e] for k, v in b.items()},
+                           tol={"positions": 1e-9, "velocities": 1e-7, "pressures": 0.0},
+                           keys=("positions", "velocities", "pressures"))
