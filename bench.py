@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--profile-frames", type=int, default=2)
     ap.add_argument("--cpu-frames", type=int, default=6, help="oracle frames per host core")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solver", default="auto", choices=["auto", "streaming", "cluster"],
+                    help="Newton-loop solver (SolverConfig.solver)")
     return ap.parse_args()
 
 
@@ -224,6 +226,7 @@ def main():
         total, scaling = world * args.envs, "weak"
     model = M.build_snake(M.SceneConfig(), n_envs=n, device=local)
     sim = model.sim
+    sim.config.solver = args.solver
     K, W = args.steps, args.warmup
     cmds = env_commands(n, W + K, 0, env0=env0)
     d_cmds = torch.from_numpy(cmds).to(f"cuda:{local}")

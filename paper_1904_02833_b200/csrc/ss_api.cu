@@ -408,9 +408,10 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
   for (int v : B.in_size) P.MIN = std::max(P.MIN, v);
   int off = 0;
   auto take = [&](int n) { const int o = off; off += (n + 1) & ~1; return o; };
-  P.oX = take(P.NR); P.oR = take(P.NR); P.oZ = take(P.NR); P.oP = take(P.NR);
+  P.oZ = take(P.NR); P.oP = take(P.NR);
   P.oAP = take(P.NR); P.oAZ = take(P.NR); P.oD = take(P.NR);
   P.oJR = take(9 * P.MT); P.oJS = take(6 * P.MT); P.oJK = take(6 * P.MT);
+  P.oRi = take(9 * P.MT); P.oE3 = take(3 * P.MT);
   P.oIn = take(P.MIN);
   P.oDir = take(3 * P.MD); P.oRw = take(3 * P.MA); P.oHJ = take(60 * P.MH);
   P.oWJ = take(18 * P.MW);
@@ -570,13 +571,13 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
     B.C = C;
     plan_partition(B, D, d_i, d_j, tets, a_p, a_b, h_a, h_b, w_body, slot_part, inc_ptr_g);
     if (B.smem_bytes > budget) continue;
-    // one element and one node per thread for the whole solve
+    // one element and one (node, axis) per thread; <= CL_RPT rows per thread
     {
-      bool ok = true;
+      bool ok = B.P.NR <= CL_RPT * CL_THREADS;
       for (int c2 = 0; c2 < C; ++c2) {
         const size_t ne = B.Lt[c2].size() + B.Ld[c2].size() + B.La[c2].size() + B.Lh[c2].size() +
                           B.Ls[c2].size();
-        if (ne > CL_THREADS || B.Lp[c2].size() + B.Lb[c2].size() > CL_THREADS) ok = false;
+        if (ne > CL_THREADS || 3 * B.Lp[c2].size() + 6 * B.Lb[c2].size() > CL_THREADS) ok = false;
       }
       if (!ok) continue;
     }

@@ -37,8 +37,9 @@ struct ClPlan {
                                             // (MW: wheel slots, the first local slots)
   int NR, ME, MN, MDOFX, MIN;               // rows, elements, owned nodes, owned+halo DOFs, inbox
   // shared-memory offsets (doubles)
-  int oX, oR, oZ, oP, oAP, oAZ, oD;         // row vectors [NR]
+  int oZ, oP, oAP, oAZ, oD;                 // row vectors [NR] (x, r live in registers)
   int oJR, oJS, oJK;                        // compact tet J [9][MT] [6][MT] [6][MT]
+  int oRi, oE3;                             // tet rest-shape inverse [9][MT], E_tet [3][MT]
   int oIn;                                  // inbox: per owned node, one 3/6-vector per incidence
   int oDir, oRw, oHJ, oWJ;                  // [3][MD] [3][MA] [60][MH] [18][MW]
   int oPres, oGap, oLc, oAct, oDyn, oBdn, oBdf;  // slots [MS] ... lamc [3][MS], bdf [2][MS]
@@ -102,60 +103,42 @@ DI double cl_cluster_sum(const ClPlan& L, const ClSmem& S, double v, int slot, d
 }
 
 // ------------------------------------------------------------ node gather
-// Per-thread owned-node state (a thread owns at most one node): inbox range,
-// halo push range, inverse mass, body index, local DOF base.
+// One thread per (owned node, axis): particles 3 threads each, bodies 6.
 struct ClMn {
-  int k0, k1, hp0, hp1, gb, base;
+  int k0, k1, hp0, hp1, lb, base, a, width;  // inbox range, halo range, body slot, DOF base
   double im;
 };
 
-// For the owned node: w = sum of its inbox (the incidences' column sums,
-// stored there by the element owners in the reference accumulation order),
-// u = M^-1 w (numba_backend.py:68-82); mode 0: U = u, mode 1: V += u; then
-// the new value is pushed into every consumer CTA's halo copy.
-DI void cl_gather(const ClPlan& L, const ClSmem& S, bool has_node, const ClMn& mn, int mode) {
-  if (!has_node) return;
-  double* sb = S.b;
+// w_a = sum of the node's inbox column a (incidence column sums stored by the
+// element owners in the reference accumulation order), u = M^-1 w
+// (numba_backend.py:68-82; body angular rows use all three angular sums);
+// mode 0: U = u, mode 1: V += u; the value is pushed to every halo copy.
+DI void cl_gather(const ClPlan& L, const ClSmem& S, bool has, const ClMn& mn, int mode) {
+  if (!has) return;
+  const double* sb = S.b;
   const int arr = mode == 0 ? L.oU : L.oV;
-  double out[6];
-  int nd;
-  if (mn.gb < 0) {
-    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-    for (int k = mn.k0; k < mn.k1; k += 3) {
-      w0 += sb[k];
-      w1 += sb[k + 1];
-      w2 += sb[k + 2];
-    }
-    out[0] = mn.im * w0;
-    out[1] = mn.im * w1;
-    out[2] = mn.im * w2;
-    nd = 3;
+  double u;
+  if (mn.width == 3 || mn.a < 3) {
+    double w = 0.0;
+    for (int k = mn.k0 + mn.a; k < mn.k1; k += mn.width) w += sb[k];
+    u = mn.im * w;
   } else {
-    const int lb = mn.gb;  // local body slot (ang_inv column)
-    double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    double w3 = 0.0, w4 = 0.0, w5 = 0.0;
     for (int k = mn.k0; k < mn.k1; k += 6) {
-#pragma unroll
-      for (int kk = 0; kk < 6; ++kk) w[kk] += sb[k + kk];
+      w3 += sb[k + 3];
+      w4 += sb[k + 4];
+      w5 += sb[k + 5];
     }
     const double* A = sb + L.oAng;
-    const int MB = L.MB;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) out[a] = mn.im * w[a];
-    out[3] = A[0 * MB + lb] * w[3] + A[1 * MB + lb] * w[4] + A[2 * MB + lb] * w[5];
-    out[4] = A[3 * MB + lb] * w[3] + A[4 * MB + lb] * w[4] + A[5 * MB + lb] * w[5];
-    out[5] = A[6 * MB + lb] * w[3] + A[7 * MB + lb] * w[4] + A[8 * MB + lb] * w[5];
-    nd = 6;
+    const int i = mn.a - 3, MB = L.MB, lb = mn.lb;
+    u = A[(3 * i) * MB + lb] * w3 + A[(3 * i + 1) * MB + lb] * w4 + A[(3 * i + 2) * MB + lb] * w5;
   }
-  double* dst = sb + arr + mn.base;
-  for (int k = 0; k < nd; ++k) {
-    const double val = mode == 0 ? out[k] : dst[k] + out[k];
-    dst[k] = val;
-    out[k] = val;
-  }
+  double* dst = S.b + arr + mn.base + mn.a;
+  const double val = mode == 0 ? u : *dst + u;
+  *dst = val;
   for (int q = mn.hp0; q < mn.hp1; ++q) {
     const int hp = L.hpush[q];
-    double* rem = S.peer[(unsigned)hp >> 24] + arr + (hp & 0xFFFFFF);
-    for (int k = 0; k < nd; ++k) rem[k] = out[k];
+    S.peer[(unsigned)hp >> 24][arr + (hp & 0xFFFFFF) + mn.a] = val;
   }
 }
 
@@ -337,30 +320,19 @@ DI int cl_nel(const ClPlan& L, int rank) {
   return cnt[0] + cnt[1] + cnt[2] + cnt[3] + cnt[4];
 }
 
-// rows of a local element (up to 6) and whether they are live (absent
-// contact slots have no rows)
-DI int cl_rows(const ClPlan& L, const double* sb, const ClEl& el, int* rows) {
+// rows of a local element: row q = base + q * stride for q < n (absent
+// contact slots have none). Arithmetic, so no per-thread arrays are needed.
+struct ClRows {
+  int base, stride, n;
+  DI int at(int q) const { return base + q * stride; }
+};
+DI ClRows cl_rows(const ClPlan& L, const double* sb, const ClEl& el) {
   switch (el.fam) {
-    case CF_TET:
-#pragma unroll
-      for (int i = 0; i < 6; ++i) rows[i] = cl_row_t(L, i, el.le);
-      return 6;
-    case CF_DIST:
-      rows[0] = cl_row_d(L, el.le);
-      return 1;
-    case CF_ATT:
-#pragma unroll
-      for (int i = 0; i < 3; ++i) rows[i] = cl_row_a(L, i, el.le);
-      return 3;
-    case CF_HINGE:
-#pragma unroll
-      for (int i = 0; i < 5; ++i) rows[i] = cl_row_h(L, i, el.le);
-      return 5;
-    default:
-      if (sb[L.oPres + el.le] == 0.0) return 0;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) rows[k] = cl_row_s(L, k, el.le);
-      return 3;
+    case CF_TET: return {cl_row_t(L, 0, el.le), L.MT, 6};
+    case CF_DIST: return {cl_row_d(L, el.le), 1, 1};
+    case CF_ATT: return {cl_row_a(L, 0, el.le), L.MA, 3};
+    case CF_HINGE: return {cl_row_h(L, 0, el.le), L.MH, 5};
+    default: return {cl_row_s(L, 0, el.le), L.MS, sb[L.oPres + el.le] == 0.0 ? 0 : 3};
   }
 }
 
@@ -378,7 +350,8 @@ DI void cl_contrib(const Ctx& c, const ClPlan& L, const ClSmem& S, const ClMe& m
       TetC T;
       double col12[12], Ri[9];
       cl_tet_load(L, sb, el.le, T);
-      tet_rinv(c, el.g, Ri);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) Ri[k] = sb[L.oRi + k * L.MT + el.le];
       cl_tet_jt<EXACT>(T, Ri, xr, col12);
 #pragma unroll
       for (int v = 0; v < 4; ++v) cl_put(S, L, dst[v], col12 + 3 * v, 3);
@@ -479,7 +452,8 @@ DI int cl_forward(const Ctx& c, const ClPlan& L, const ClSmem& S, const ClMe& me
       TetC T;
       double Ri[9];
       cl_tet_load(L, sb, el.le, T);
-      tet_rinv(c, el.g, Ri);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) Ri[k] = sb[L.oRi + k * L.MT + el.le];
       cl_tet_j<EXACT>(T, Ri, uu, y);
       return 6;
     }
@@ -577,11 +551,22 @@ DI int cl_grow(const Ctx& c, const ClEl& el, int i) {
   }
 }
 
+// Row scaling by the Jacobi diagonal: EXACT divides like the reference
+// (z = r/d); the structured mode keeps 1/d in the row vector and multiplies
+// (one rounding of 1/d, <= 1 ulp per quotient, ~20x fewer FP64 operations).
+template <bool EXACT>
+DI double cl_dstore(double d) { return EXACT ? d : 1.0 / d; }
+template <bool EXACT>
+DI double cl_ddiv(double x, double dstored) { return EXACT ? x / dstored : x * dstored; }
+
 // ===================================================================
 // The Newton loop of one substep for one environment per cluster:
 // grid.x = C * E, cluster (C,1,1), CL_THREADS threads, dynamic smem.
-// Reads the eval/contact outputs of this substep from global memory,
-// writes back velocities, multipliers, warm starts and the residual.
+// Thread roles: element phases (one local element per thread), row phases
+// (thread t owns rows t + j*CL_THREADS, j < CL_RPT; x and r of its rows live
+// in registers for the whole solve), node phases (one (node, axis) per
+// thread). Dead rows (absent contact slots, family padding) stay exactly 0.
+#define CL_RPT 5
 #define CL_STAMP(id)                                                                    \
   do {                                                                                  \
     if (L.dbg && blockIdx.x == 0 && threadIdx.x == 0 && itn == 1 && k == 3)             \
@@ -597,8 +582,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
   const int rank = (int)cl.block_rank();
   const int env = blockIdx.x / L.C;
   const int E = c.D.E;
-  if (threadIdx.x < L.C) peers[threadIdx.x] = cl.map_shared_rank(sm_, (int)threadIdx.x);
-  __syncthreads();
+  const int tid = threadIdx.x;
+  if (tid < L.C) peers[tid] = cl.map_shared_rank(sm_, tid);
   ClSmem S;
   S.b = sm_;
   S.peer = peers;
@@ -607,58 +592,77 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
   const int nEl = cl_nel(L, rank);
   const int nP = cnt[5], nB = cnt[6];
   const double g = c.p.gamma, h = c.p.h;
-  // per-thread element and node state for the whole solve
-  const bool has_el = (int)threadIdx.x < nEl;
+
+  // ---- per-thread element state
+  const bool has_el = tid < nEl;
   ClMe me;
   if (has_el) {
-    const int e = threadIdx.x;
-    me.el = cl_el(L, rank, e);
+    me.el = cl_el(L, rank, tid);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      me.ref[q] = L.eref[((size_t)rank * L.ME + e) * 4 + q];
-      me.dst[q] = L.dest[((size_t)rank * L.ME + e) * 4 + q];
+      me.ref[q] = L.eref[((size_t)rank * L.ME + tid) * 4 + q];
+      me.dst[q] = L.dest[((size_t)rank * L.ME + tid) * 4 + q];
     }
     me.dyn = 0.0;
     if (me.el.fam == CF_DIST) me.dyn = c.T.d_dyn[me.el.g];
     else if (me.el.fam == CF_ATT) me.dyn = c.T.a_dyn[me.el.g];
     else if (me.el.fam == CF_HINGE) me.dyn = c.T.h_dyn[me.el.g];
   }
-  const bool has_node = (int)threadIdx.x < nP + nB;
+  // ---- per-thread (node, axis) state
+  const bool has_na = tid < 3 * nP + 6 * nB;
   ClMn mn;
-  if (has_node) {
-    const int n = threadIdx.x;
+  if (has_na) {
+    int n;
+    if (tid < 3 * nP) {
+      n = tid / 3;
+      mn.a = tid % 3;
+      mn.width = 3;
+      mn.base = 3 * n;
+      mn.lb = -1;
+      mn.im = c.T.inv_mass[L.node[(size_t)rank * L.MN + n]];
+    } else {
+      const int q = tid - 3 * nP;
+      n = nP + q / 6;
+      mn.a = q % 6;
+      mn.width = 6;
+      mn.lb = q / 6;
+      mn.base = 3 * nP + 6 * mn.lb;
+      mn.im = c.T.body_inv_mass[L.node[(size_t)rank * L.MN + n] - c.D.P];
+    }
     const int* iptr = L.in_ptr + (size_t)rank * (L.MN + 1);
     const int* hptr = L.hp_ptr + (size_t)rank * (L.MN + 1);
     mn.k0 = L.oIn + iptr[n];
     mn.k1 = L.oIn + iptr[n + 1];
     mn.hp0 = hptr[n];
     mn.hp1 = hptr[n + 1];
-    const int gn = L.node[(size_t)rank * L.MN + n];
-    if (n < nP) {
-      mn.gb = -1;
-      mn.im = c.T.inv_mass[gn];
-      mn.base = 3 * n;
-    } else {
-      mn.gb = n - nP;  // local body slot (ang_inv column)
-      mn.im = c.T.body_inv_mass[gn - c.D.P];
-      mn.base = 3 * nP + 6 * (n - nP);
-    }
   }
 
+  // ---- dead rows = 0 (d = 1): init every row, elements overwrite theirs
+  for (int r = tid; r < L.NR; r += CL_THREADS) {
+    sb[L.oZ + r] = 0.0;
+    sb[L.oP + r] = 0.0;
+    sb[L.oAP + r] = 0.0;
+    sb[L.oAZ + r] = 0.0;
+    sb[L.oD + r] = 1.0;
+  }
   // ---- load substep inputs into shared memory
   if (has_el) {
     const ClEl& el = me.el;
-    int rows[6];
     switch (el.fam) {
       case CF_TET: {
         const int nt = c.D.nt, t = el.g;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) sb[L.oJR + k * L.MT + el.le] = c.K.tR[IX(k * nt + t)];
+        for (int k = 0; k < 9; ++k) {
+          sb[L.oJR + k * L.MT + el.le] = c.K.tR[IX(k * nt + t)];
+          sb[L.oRi + k * L.MT + el.le] = c.T.t_rinv[k * nt + t];
+        }
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
           sb[L.oJS + k * L.MT + el.le] = c.K.tS[IX(k * nt + t)];
           sb[L.oJK + k * L.MT + el.le] = c.K.tK[IX(k * nt + t)];
         }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) sb[L.oE3 + k * L.MT + el.le] = c.T.t_e3[k * nt + t];
         break;
       }
       case CF_DIST:
@@ -692,9 +696,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
         break;
       }
     }
-    (void)rows;
   }
-  for (int n = threadIdx.x; n < nP + nB; n += blockDim.x) {
+  for (int n = tid; n < nP + nB; n += CL_THREADS) {
     const int gn = L.node[(size_t)rank * L.MN + n];
     if (n < nP) {
 #pragma unroll
@@ -708,24 +711,19 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
     }
   }
   __syncthreads();
-  // halo copies of V: the loads above wrote owned DOFs; also fill halos
-  // directly from global memory (same values the owners hold)
-  {
-    const int* hptr = L.hp_ptr + (size_t)rank * (L.MN + 1);
-    for (int n = threadIdx.x; n < nP + nB; n += blockDim.x) {
-      const int nd = n < nP ? 3 : 6, base = n < nP ? 3 * n : 3 * nP + 6 * (n - nP);
-      for (int q = hptr[n]; q < hptr[n + 1]; ++q) {
-        const int hp = L.hpush[q];
-        double* rem = S.peer[(unsigned)hp >> 24] + L.oV + (hp & 0xFFFFFF);
-        for (int k = 0; k < nd; ++k) rem[k] = sb[L.oV + base + k];
-      }
+  // halo copies of V (owners push their loaded values)
+  if (has_na) {
+    const double val = sb[L.oV + mn.base + mn.a];
+    for (int q = mn.hp0; q < mn.hp1; ++q) {
+      const int hp = L.hpush[q];
+      S.peer[(unsigned)hp >> 24][L.oV + (hp & 0xFFFFFF) + mn.a] = val;
     }
   }
 
   // ---- initial impulse v = vt + M^-1 J^T lam (solver.py:428-436)
   if (has_el) {
     const ClEl& el = me.el;
-    double xr[6];
+    double xr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (el.fam == CF_SLOT) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) xr[k] = sb[L.oLc + k * L.MS + el.le];
@@ -738,21 +736,20 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
     cl_contrib<EXACT>(c, L, S, me, xr, 1);
   }
   cl.sync();
-  cl_gather(L, S, has_node, mn, 1);
+  cl_gather(L, S, has_na, mn, 1);
   cl.sync();
 
-  int rslot = 0;  // rotating reduction slot (16 slots: a slot is rewritten only
-                  // after 15 further cluster barriers, long after its readers)
+  int rslot = 0;  // rotating reduction slot (16 slots: rewritten only 15 barriers later)
   double resid = 0.0;
+  double xr_[CL_RPT], rr_[CL_RPT];  // x and r of this thread's rows
   for (int itn = 0; itn < c.p.newton; ++itn) {
     const bool lastn = itn == c.p.newton - 1;
-    // ---- rhs, FB, active set, diagonal; x = 0, r, z = r/d; J^T z
+    // ---- rhs, FB, active set, diagonal; z = r/d; r -> AZ scratch; J^T z
     if (has_el) {
       const ClEl& el = me.el;
-      int rows[6];
-      const int nr = cl_rows(L, sb, el, rows);
+      const ClRows R = cl_rows(L, sb, el);
       double jv[6];
-      cl_forward<EXACT>(c, L, S, me, L.oV, jv);
+      if (R.n) cl_forward<EXACT>(c, L, S, me, L.oV, jv);
       double zr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       if (el.fam == CF_TET) {
         TetC T;
@@ -761,21 +758,23 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
         tet_res(T, rs);
 #pragma unroll
         for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[IX(cl_grow(c, el, i))];
-        ereg6(c.T.t_e3[el.g], c.T.t_e3[c.D.nt + el.g], c.T.t_e3[2 * c.D.nt + el.g], lm, el6);
+        ereg6(sb[L.oE3 + el.le], sb[L.oE3 + L.MT + el.le], sb[L.oE3 + 2 * L.MT + el.le], lm, el6);
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
           const double dg = npmax(c.K.bdiag[IX(cl_grow(c, el, i))] + 0.0, 1e-30);
           const double d = dg > 1e-300 ? dg : 1.0;
           const double r = -(g * rs[i] / h + jv[i] + el6[i]);
-          sb[L.oR + rows[i]] = r;
-          sb[L.oD + rows[i]] = d;
-          sb[L.oX + rows[i]] = 0.0;
-          zr[i] = r / d;
-          sb[L.oZ + rows[i]] = zr[i];
+          const double ds = cl_dstore<EXACT>(d);
+          zr[i] = cl_ddiv<EXACT>(r, ds);
+          sb[L.oAZ + R.at(i)] = r;
+          sb[L.oD + R.at(i)] = ds;
+          sb[L.oZ + R.at(i)] = zr[i];
         }
       } else if (el.fam != CF_SLOT) {
         const double dyn = me.dyn;
-        for (int i = 0; i < nr; ++i) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          if (i >= R.n) break;
           const int gr = cl_grow(c, el, i);
           const double res = el.fam == CF_DIST ? sb[L.oResD + el.le]
                            : el.fam == CF_ATT ? sb[L.oResA + i * L.MA + el.le]
@@ -783,13 +782,13 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
           const double dg = npmax(c.K.bdiag[IX(gr)] + dyn, 1e-30);
           const double d = dg > 1e-300 ? dg : 1.0;
           const double r = -(g * res / h + jv[i] + dyn * c.S.lam[IX(gr)]);
-          sb[L.oR + rows[i]] = r;
-          sb[L.oD + rows[i]] = d;
-          sb[L.oX + rows[i]] = 0.0;
-          zr[i] = r / d;
-          sb[L.oZ + rows[i]] = zr[i];
+          const double ds = cl_dstore<EXACT>(d);
+          zr[i] = cl_ddiv<EXACT>(r, ds);
+          sb[L.oAZ + R.at(i)] = r;
+          sb[L.oD + R.at(i)] = ds;
+          sb[L.oZ + R.at(i)] = zr[i];
         }
-      } else if (nr) {
+      } else if (R.n) {
         const int ls = el.le;
         const double ln = sb[L.oLc + ls];
         const double a = sb[L.oGap + ls] / h + jv[0];
@@ -819,171 +818,181 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
         }
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          sb[L.oR + rows[k]] = rr[k];
-          sb[L.oD + rows[k]] = dd[k];
-          sb[L.oX + rows[k]] = 0.0;
-          zr[k] = rr[k] / dd[k];
-          sb[L.oZ + rows[k]] = zr[k];
+          const double ds = cl_dstore<EXACT>(dd[k]);
+          zr[k] = cl_ddiv<EXACT>(rr[k], ds);
+          sb[L.oAZ + R.at(k)] = rr[k];
+          sb[L.oD + R.at(k)] = ds;
+          sb[L.oZ + R.at(k)] = zr[k];
         }
       } else {
         sb[L.oAct + el.le] = 0.0;
       }
       cl_contrib<EXACT>(c, L, S, me, zr, 0);
     }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < CL_RPT; ++j) {
+      const int row = tid + j * CL_THREADS;
+      xr_[j] = 0.0;
+      rr_[j] = row < L.NR ? sb[L.oAZ + row] : 0.0;
+    }
     bool broken = false;
     double rho = 0.0, alpha = 0.0, beta = 0.0;
-    for (int k = 0; k <= c.p.pcr; ++k) {
-      const bool setup = k == 0;
+    for (int k = 0; k < c.p.pcr; ++k) {
       CL_STAMP(0);
-      if (k > 0 && c.p.pcr > 0) {
-        // x += alpha p, r -= alpha ap, z = r/d, then J^T z (k < pcr), or the
-        // Newton update (k == pcr)
-        if (k < c.p.pcr) {
-          if (!broken) {
-            if (has_el) {
-              const ClEl& el = me.el;
-              int rows[6];
-              const int nr = cl_rows(L, sb, el, rows);
-              double zr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-              for (int q = 0; q < nr; ++q) {
-                const int o = rows[q];
-                sb[L.oX + o] += alpha * sb[L.oP + o];
-                const double r = sb[L.oR + o] - alpha * sb[L.oAP + o];
-                sb[L.oR + o] = r;
-                zr[q] = r / sb[L.oD + o];
-                sb[L.oZ + o] = zr[q];
-              }
-              cl_contrib<EXACT>(c, L, S, me, zr, 0);
-            }
+      if (k > 0 && !broken) {
+        // x += alpha p, r -= alpha ap, z = r/d (row-parallel), then J^T z
+#pragma unroll
+        for (int j = 0; j < CL_RPT; ++j) {
+          const int row = tid + j * CL_THREADS;
+          if (row < L.NR) {
+            xr_[j] += alpha * sb[L.oP + row];
+            rr_[j] -= alpha * sb[L.oAP + row];
+            sb[L.oZ + row] = cl_ddiv<EXACT>(rr_[j], sb[L.oD + row]);
           }
         }
-      }
-      if (k == c.p.pcr) break;
-      if (!(k > 0 && broken)) {
-        CL_STAMP(1);
-        cl.sync();                               // column sums of J^T z visible
-        CL_STAMP(2);
-        cl_gather(L, S, has_node, mn, 0);        // U = M^-1 J^T z
-        CL_STAMP(3);
-        cl.sync();                               // U visible
-        CL_STAMP(4);
-      }
-      // az = J u + dyn z + E z; rho = z.az
-      double part = 0.0;
-      if (!broken) {
+        __syncthreads();
         if (has_el) {
           const ClEl& el = me.el;
-          int rows[6];
-          const int nr = cl_rows(L, sb, el, rows);
-          double y[6];
-          if (nr) cl_forward<EXACT>(c, L, S, me, L.oU, y);
-          if (!nr) {
-          } else if (el.fam == CF_TET) {
-            double zz[6], ez[6];
+          const ClRows R = cl_rows(L, sb, el);
+          double zr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int i = 0; i < 6; ++i) zz[i] = sb[L.oZ + rows[i]];
-            ereg6(c.T.t_e3[el.g], c.T.t_e3[c.D.nt + el.g], c.T.t_e3[2 * c.D.nt + el.g], zz, ez);
+          for (int q = 0; q < 6; ++q) {
+            if (q >= R.n) break;
+            zr[q] = sb[L.oZ + R.at(q)];
+          }
+          cl_contrib<EXACT>(c, L, S, me, zr, 0);
+        }
+      }
+      CL_STAMP(1);
+      if (!(k > 0 && broken)) {
+        cl.sync();                            // column sums of J^T z visible
+        CL_STAMP(2);
+        cl_gather(L, S, has_na, mn, 0);       // U = M^-1 J^T z (+ halo pushes)
+        CL_STAMP(3);
+        cl.sync();                            // U visible
+        CL_STAMP(4);
+      }
+      // az = J u + dyn z + E z; rho = z.az (element-parallel)
+      double part = 0.0;
+      if (!broken && has_el) {
+        const ClEl& el = me.el;
+        const ClRows R = cl_rows(L, sb, el);
+        const int nr = R.n;
+        double y[6];
+        if (nr) cl_forward<EXACT>(c, L, S, me, L.oU, y);
+        if (!nr) {
+        } else if (el.fam == CF_TET) {
+          double zz[6], ez[6];
 #pragma unroll
-            for (int i = 0; i < 6; ++i) {
-              const double az = y[i] + ez[i];
-              sb[L.oAZ + rows[i]] = az;
-              part += zz[i] * az;
-            }
-          } else if (el.fam == CF_SLOT) {
-            const int ls = el.le;
-            const double zn = sb[L.oZ + rows[0]], z0 = sb[L.oZ + rows[1]], z1 = sb[L.oZ + rows[2]];
-            const double an = y[0] + sb[L.oDyn + ls] * zn;
-            double a0 = z0, a1 = z1;
-            if (sb[L.oAct + ls] != 0.0) {
-              a0 = y[1] + c.p.fdyn * z0;
-              a1 = y[2] + c.p.fdyn * z1;
-            }
-            sb[L.oAZ + rows[0]] = an;
-            sb[L.oAZ + rows[1]] = a0;
-            sb[L.oAZ + rows[2]] = a1;
-            part += zn * an;
-            part += z0 * a0;
-            part += z1 * a1;
-          } else {
-            const double dyn = me.dyn;
-            for (int i = 0; i < nr; ++i) {
-              const double zr = sb[L.oZ + rows[i]];
-              const double az = y[i] + dyn * zr;
-              sb[L.oAZ + rows[i]] = az;
-              part += zr * az;
-            }
+          for (int i = 0; i < 6; ++i) zz[i] = sb[L.oZ + R.at(i)];
+          ereg6(sb[L.oE3 + el.le], sb[L.oE3 + L.MT + el.le], sb[L.oE3 + 2 * L.MT + el.le], zz, ez);
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            const double az = y[i] + ez[i];
+            sb[L.oAZ + R.at(i)] = az;
+            part += zz[i] * az;
+          }
+        } else if (el.fam == CF_SLOT) {
+          const int ls = el.le;
+          const double zn = sb[L.oZ + R.at(0)], z0 = sb[L.oZ + R.at(1)], z1 = sb[L.oZ + R.at(2)];
+          const double an = y[0] + sb[L.oDyn + ls] * zn;
+          double a0 = z0, a1 = z1;
+          if (sb[L.oAct + ls] != 0.0) {
+            a0 = y[1] + c.p.fdyn * z0;
+            a1 = y[2] + c.p.fdyn * z1;
+          }
+          sb[L.oAZ + R.at(0)] = an;
+          sb[L.oAZ + R.at(1)] = a0;
+          sb[L.oAZ + R.at(2)] = a1;
+          part += zn * an;
+          part += z0 * a0;
+          part += z1 * a1;
+        } else {
+          const double dyn = me.dyn;
+#pragma unroll
+          for (int i = 0; i < 5; ++i) {
+            if (i >= nr) break;
+            const double zr = sb[L.oZ + R.at(i)];
+            const double az = y[i] + dyn * zr;
+            sb[L.oAZ + R.at(i)] = az;
+            part += zr * az;
           }
         }
       }
       CL_STAMP(5);
       const double rho_new = cl_cluster_sum(L, S, part, rslot, scratch);
-      CL_STAMP(6);
       rslot = (rslot + 1) & 15;
+      CL_STAMP(6);
       if (!broken) {
-        if (setup) {
+        if (k == 0) {
           rho = rho_new;
         } else {
           beta = rho > 1e-300 ? rho_new / rho : 0.0;
           rho = rho_new;
         }
       }
-      // p = z + beta p, ap = az + beta ap; den = ap.(ap/d)
+      // p = z + beta p, ap = az + beta ap; den = ap.(ap/d) (row-parallel)
       double dpart = 0.0;
-      if (has_el) {
-        const ClEl& el = me.el;
-        int rows[6];
-        const int nr = cl_rows(L, sb, el, rows);
-        for (int q = 0; q < nr; ++q) {
-          const int o = rows[q];
+#pragma unroll
+      for (int j = 0; j < CL_RPT; ++j) {
+        const int row = tid + j * CL_THREADS;
+        if (row < L.NR) {
           double ap;
-          if (setup) {
-            sb[L.oP + o] = sb[L.oZ + o];
-            ap = sb[L.oAZ + o];
-            sb[L.oAP + o] = ap;
+          if (k == 0) {
+            sb[L.oP + row] = sb[L.oZ + row];
+            ap = sb[L.oAZ + row];
+            sb[L.oAP + row] = ap;
           } else if (!broken) {
-            sb[L.oP + o] = sb[L.oZ + o] + beta * sb[L.oP + o];
-            ap = sb[L.oAZ + o] + beta * sb[L.oAP + o];
-            sb[L.oAP + o] = ap;
+            sb[L.oP + row] = sb[L.oZ + row] + beta * sb[L.oP + row];
+            ap = sb[L.oAZ + row] + beta * sb[L.oAP + row];
+            sb[L.oAP + row] = ap;
           } else {
-            ap = sb[L.oAP + o];
+            ap = sb[L.oAP + row];
           }
-          dpart += ap * (ap / sb[L.oD + o]);
+          dpart += ap * cl_ddiv<EXACT>(ap, sb[L.oD + row]);
         }
       }
       CL_STAMP(7);
       const double den = cl_cluster_sum(L, S, dpart, rslot, scratch);
-      CL_STAMP(8);
       rslot = (rslot + 1) & 15;
+      CL_STAMP(8);
       if (!broken) {
         if (den <= 1e-300 || !isfinite(den)) broken = true;
         else alpha = rho / den;
       }
     }
-    // ---- last PCR step + multiplier update + projection + dlam column sums
+    // ---- last PCR step (row-parallel): dl = x + alpha p -> AZ scratch, r.z
     double rzp = 0.0;
     const bool step = c.p.pcr > 0 && !broken;
-    if (has_el) {
-      const ClEl& el = me.el;
-      int rows[6];
-      const int nr = cl_rows(L, sb, el, rows);
-      double dl[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      for (int q = 0; q < nr; ++q) {
-        const int o = rows[q];
-        double x = sb[L.oX + o], r = sb[L.oR + o], z = sb[L.oZ + o];
+#pragma unroll
+    for (int j = 0; j < CL_RPT; ++j) {
+      const int row = tid + j * CL_THREADS;
+      if (row < L.NR) {
+        double x = xr_[j], r = rr_[j], z = sb[L.oZ + row];
         if (step) {
-          x += alpha * sb[L.oP + o];
-          r -= alpha * sb[L.oAP + o];
-          z = r / sb[L.oD + o];
+          x += alpha * sb[L.oP + row];
+          r -= alpha * sb[L.oAP + row];
+          z = cl_ddiv<EXACT>(r, sb[L.oD + row]);
         }
         rzp += r * z;
-        dl[q] = x;
+        sb[L.oAZ + row] = x;
       }
+    }
+    __syncthreads();
+    // ---- multiplier update + projection + dlam column sums (element-parallel)
+    if (has_el) {
+      const ClEl& el = me.el;
+      const ClRows R = cl_rows(L, sb, el);
+      const int nr = R.n;
       double dlam[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       if (el.fam != CF_SLOT) {
-        for (int q = 0; q < nr; ++q) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          if (q >= nr) break;
           const size_t gi = IX(cl_grow(c, el, q));
           const double l0 = c.S.lam[gi];
-          const double l1 = l0 + dl[q];
+          const double l1 = l0 + sb[L.oAZ + R.at(q)];
           c.S.lam[gi] = l1;
           dlam[q] = l1 - l0;
         }
@@ -992,9 +1001,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
         double n1 = 0.0, a1 = 0.0, b1 = 0.0;
         if (nr) {
           const double n0 = sb[L.oLc + ls], a0 = sb[L.oLc + L.MS + ls], b0 = sb[L.oLc + 2 * L.MS + ls];
-          n1 = n0 + dl[0];
-          a1 = a0 + dl[1];
-          b1 = b0 + dl[2];
+          n1 = n0 + sb[L.oAZ + R.at(0)];
+          a1 = a0 + sb[L.oAZ + R.at(1)];
+          b1 = b0 + sb[L.oAZ + R.at(2)];
           n1 = npmax(n1, 0.0);
           const double rad = c.p.mu * npmax(n1, 0.0);
           const double nrm = sqrt(a1 * a1 + b1 * b1);
@@ -1027,13 +1036,13 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
     const double rz = cl_cluster_sum(L, S, rzp, rslot, scratch);
     rslot = (rslot + 1) & 15;
     resid = sqrt(0.0 > rz ? 0.0 : rz);
-    // cl_cluster_sum ended with a cluster barrier: dlam column sums visible
-    cl_gather(L, S, has_node, mn, 1);  // v += M^-1 J^T dlam
+    // the reduction's cluster barrier also published the dlam column sums
+    cl_gather(L, S, has_na, mn, 1);  // v += M^-1 J^T dlam (+ halo pushes)
     cl.sync();
   }
 
   // ---- write back
-  for (int n = threadIdx.x; n < nP + nB; n += blockDim.x) {
+  for (int n = tid; n < nP + nB; n += CL_THREADS) {
     const int gn = L.node[(size_t)rank * L.MN + n];
     if (n < nP) {
 #pragma unroll
@@ -1044,6 +1053,6 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
       for (int k = 0; k < 6; ++k) c.K.v[IX(o + k)] = sb[L.oV + 3 * nP + 6 * lb + k];
     }
   }
-  if (rank == 0 && threadIdx.x == 0) c.K.resid[env] = resid;
-  cl.sync();  // no CTA may exit while peers can still read its shared memory
+  if (rank == 0 && tid == 0) c.K.resid[env] = resid;
+  cl.sync();  // no CTA may exit while peers can still access its shared memory
 }

@@ -7,6 +7,7 @@ from paper_1904_02833_b200 import _native
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 7
 model = M.build_snake(M.SceneConfig(), n_envs=n)
 sim = model.sim
+sim.config.solver = "cluster"
 cmds = bench.env_commands(n, 3, 0)
 sim.step(cmds[:2], True, 2)
 sim.synchronize()
