@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--profile-frames", type=int, default=2)
     ap.add_argument("--cpu-frames", type=int, default=6, help="oracle frames per host core")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--wave-envs", type=int, default=0,
+                    help="envs per wave (SolverConfig.wave_envs; 0 = auto)")
     ap.add_argument("--solver", default="auto", choices=["auto", "streaming", "cluster"],
                     help="Newton-loop solver (SolverConfig.solver)")
     return ap.parse_args()
@@ -227,6 +229,7 @@ def main():
     model = M.build_snake(M.SceneConfig(), n_envs=n, device=local)
     sim = model.sim
     sim.config.solver = args.solver
+    sim.config.wave_envs = args.wave_envs
     K, W = args.steps, args.warmup
     cmds = env_commands(n, W + K, 0, env0=env0)
     d_cmds = torch.from_numpy(cmds).to(f"cuda:{local}")
@@ -277,7 +280,9 @@ def main():
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     nc_mean = float(np.mean([st.contact_count for st in sim.get_stats()])) / sim.config.substeps
-    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean) * n
+    # one launch covers one wave: envs per launch = n / waves on average
+    waves = sim.solver_info["waves"]
+    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean) * n / waves
     avg_ms = prof[top][0] / prof[top][1]
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
     traffic = None
@@ -285,7 +290,8 @@ def main():
     if os.path.exists(tp):
         tj = json.load(open(tp))
         if tj.get(top) is not None:
-            traffic = float(tj[top]) * n / float(tj.get("_envs", 1024))  # scaled to this env count
+            # scaled to the envs of one launch
+            traffic = float(tj[top]) * (n / waves) / float(tj.get("_envs", 1024))
 
     if rank != 0:
         if dist:
@@ -299,7 +305,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "envs_per_gpu": n, "global_envs": total,
+        "config": {"workload": WORKLOAD if total == 1024 * world and scaling == "weak" else
+                   f"{total} independent snakes batched on {world}xB200", "envs_per_gpu": n, "global_envs": total,
                    "frame_dt_s": 1 / 60, "substeps": 2, "newton": 4, "pcr": 20,
                    "gait": "default, per-env turn bias U(-0.5,0.5), t0 U(0,0.5s), seed 20260817",
                    "l2": "no flush: per-step working set "

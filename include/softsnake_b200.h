@@ -114,6 +114,11 @@ typedef struct ss_params {
    * 2 cluster-resident: one env per <=16-CTA cluster, PCR state in shared
    * memory (error if the scene does not fit). */
   int32_t solver_mode;
+  /* envs per wave (0 = auto: min(n_envs, 4096), lowered further if the
+   * workspace plus all env state would not fit in device memory). Persistent
+   * state is kept for every env; waves share one workspace and run back to
+   * back inside each frame. */
+  int32_t wave_envs;
 } ss_params;
 
 /* Full per-environment state. Host pointers;
@@ -188,7 +193,8 @@ int ss_launches_per_frame(ss_handle* h);
 /* Bytes of device memory held by the handle. */
 int64_t ss_device_bytes(ss_handle* h);
 /* info[0] 1 if the cluster-resident solver is used, info[1] CTAs per
- * cluster, info[2] shared bytes per CTA, info[3] padded env lanes. */
+ * cluster, info[2] shared bytes per CTA, info[3] env lanes per wave,
+ * info[4] number of waves. info must hold 5 ints. */
 int ss_solver_info(ss_handle* h, int* info);
 /* Debug: clock64 phase stamps of one PCR iteration of the cluster solver
  * (handle created with SS_CLUSTER_STAMPS set); out[16]. */

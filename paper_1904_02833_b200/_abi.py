@@ -46,7 +46,7 @@ class SsParams(C.Structure):
         ("max_strain_rate", C.c_double), ("constraint_damping", C.c_double),
         ("strain_youngs", C.c_double), ("k_inflate", C.c_double),
         ("k_deflate", C.c_double), ("deflate_cap", C.c_double), ("supply", C.c_double),
-        ("exact_jacobian", C.c_int32), ("solver_mode", C.c_int32),
+        ("exact_jacobian", C.c_int32), ("solver_mode", C.c_int32), ("wave_envs", C.c_int32),
     ]
 
 
@@ -208,6 +208,7 @@ def pack_params(config, packed: PackedTopology) -> SsParams:
     p.supply = float(getattr(ch, "supply", 8.0))
     p.exact_jacobian = 1 if getattr(config, "exact_jacobian", False) else 0
     p.solver_mode = {"auto": 0, "streaming": 1, "cluster": 2}[getattr(config, "solver", "auto")]
+    p.wave_envs = int(getattr(config, "wave_envs", 0))
     return p
 
 

@@ -58,7 +58,12 @@ struct Arena {
 struct ss_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
-  Ctx c{};
+  Ctx c{};                 // wave 0 (shared dims, topology, workspace)
+  // waves: persistent state of wave w lives in its own block; the workspace
+  // is shared and the waves of a frame run back to back on the stream
+  int n_waves = 1;
+  std::vector<Ctx> wave;   // per-wave contexts (State pointers, real lanes)
+  std::vector<std::vector<cudaGraphExec_t>> wave_graphs;  // [wave][key]
   int gy_red = 1;
   void* topo_mem = nullptr;
   void* state_mem = nullptr;
@@ -67,7 +72,6 @@ struct ss_handle {
   double* d_cmd = nullptr;      // [n_real * links] (one frame)
   double* d_stage = nullptr;    // staging for state I/O
   size_t stage_bytes = 0;
-  cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};
   int launches = 0;
   // cluster-resident Newton solver (0 = streaming kernels)
   int use_cluster = 0;
@@ -129,8 +133,8 @@ int kid(const char* name) {
 // EX: materialised-column tet Jacobian (bitwise numba sums) instead of the
 // structured application (default).
 template <bool EX>
-int enqueue_frame_t(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof) {
-  const Ctx& c = H->c;
+int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd, int latency,
+                    int* nl, Prof* prof) {
   const Dims& D = c.D;
   cudaStream_t st = H->stream;
   const dim3 blk(SS_THREADS);
@@ -151,7 +155,7 @@ int enqueue_frame_t(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof)
   const double* xc_z = c.K.z + (size_t)D.ms * D.E;
   const double* xs_dl = c.K.az;
   const double* xc_dl = c.K.az + (size_t)D.ms * D.E;
-  LAUNCH(k_frame_begin, g_links, c, H->d_cmd, has_cmd, latency);
+  LAUNCH(k_frame_begin, g_links, c, d_cmd, has_cmd, latency);
   for (int sub = 0; sub < c.p.substeps; ++sub) {
     LAUNCH(k_pre, g_pre, c);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
@@ -212,28 +216,31 @@ int enqueue_frame_t(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof)
 }
 #undef LAUNCH
 
-int enqueue_frame(ss_handle* H, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
-  return H->c.p.exact_j ? enqueue_frame_t<true>(H, has_cmd, latency, nl, prof)
-                        : enqueue_frame_t<false>(H, has_cmd, latency, nl, prof);
+int enqueue_frame(ss_handle* H, int w, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
+  const Ctx& c = H->wave[w];
+  const double* d_cmd = H->d_cmd + (size_t)w * H->c.D.E * std::max(1, H->c.D.links);
+  return H->c.p.exact_j ? enqueue_frame_t<true>(H, c, d_cmd, has_cmd, latency, nl, prof)
+                        : enqueue_frame_t<false>(H, c, d_cmd, has_cmd, latency, nl, prof);
 }
 
-int get_graph(ss_handle* H, int has_cmd, int latency, cudaGraphExec_t* out) {
+int get_graph(ss_handle* H, int w, int has_cmd, int latency, cudaGraphExec_t* out) {
   const int key = (has_cmd ? 2 : 0) | (latency ? 1 : 0);
-  if (H->graphs[key]) {
-    *out = H->graphs[key];
+  cudaGraphExec_t& slot = H->wave_graphs[w][key];
+  if (slot) {
+    *out = slot;
     return SS_OK;
   }
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(H->stream, cudaStreamCaptureModeThreadLocal));
   int nl = 0;
-  int rc = enqueue_frame(H, has_cmd, latency, &nl);
+  int rc = enqueue_frame(H, w, has_cmd, latency, &nl);
   cudaError_t e = cudaStreamEndCapture(H->stream, &g);
   if (rc) return rc;
   if (e != cudaSuccess) return fail(SS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
-  CK(cudaGraphInstantiate(&H->graphs[key], g, 0));
+  CK(cudaGraphInstantiate(&slot, g, 0));
   CK(cudaGraphDestroy(g));
   H->launches = nl;
-  *out = H->graphs[key];
+  *out = slot;
   return SS_OK;
 }
 
@@ -244,9 +251,9 @@ struct Field {
   void* host;
 };
 
-void state_fields(ss_handle* H, const ss_state_view* v, Field* f, int* nf) {
+void state_fields(ss_handle* H, int w, const ss_state_view* v, Field* f, int* nf) {
   const Dims& D = H->c.D;
-  const State& S = H->c.S;
+  const State& S = H->wave[w].S;
   const size_t E = D.E;
   int k = 0;
   auto add = [&](void* dev, int A, int B, int swap, int is_int, void* host) {
@@ -638,13 +645,24 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   CK(cudaSetDevice(device));
 
   Dims D{};
-  D.n_real = n_envs;
-  int E = 1;
-  if (n_envs <= 32) {
-    while (E < n_envs) E <<= 1;
-  } else {
-    E = ((n_envs + 31) / 32) * 32;
-  }
+  // lanes of one wave: ss_params.wave_envs, or by default at most
+  // kAutoWave lanes. An [item][E] row is 8E bytes, so E <= 4096 keeps >= 64
+  // item rows per 2 MB page and the per-env item walk inside the GPU's TLB
+  // reach (65536 envs: 4756 steps/s at 4096 lanes, 3895 at 38912; bench
+  // sweep in DESIGN.md). The memory cap is applied after the plan below.
+  constexpr int kAutoWave = 4096;
+  int wave_req = p->wave_envs > 0 ? std::min(p->wave_envs, n_envs) : std::min(kAutoWave, n_envs);
+  auto pad_lanes = [](int n) {
+    int E = 1;
+    if (n <= 32) {
+      while (E < n) E <<= 1;
+    } else {
+      E = ((n + 31) / 32) * 32;
+    }
+    return E;
+  };
+  D.n_real = std::min(n_envs, wave_req);
+  int E = pad_lanes(D.n_real);
   D.E = E;
   D.W = E < 32 ? E : 32;
   D.lgW = 0;
@@ -962,11 +980,10 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
     H->gy_red = (int)grid_items(D, n_el, kReduceBlocks).y;
   }
-  const int gy_max = H->gy_red;
 
-  // state + work
-  const size_t Es = D.E;
+  // state + work (lane count read at call time: the wave cap may shrink it)
   auto plan_state = [&](Arena& A) {
+    const size_t Es = H->c.D.E;
     State& S = H->c.S;
     S.pos = A.take<double>(3 * (size_t)D.P * Es);
     S.vel = A.take<double>(3 * (size_t)D.P * Es);
@@ -984,8 +1001,14 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     S.warm = A.take<double>(3 * (size_t)D.nw * Es);
     S.warm_valid = A.take<int>((size_t)D.nw * Es);
     S.time = A.take<double>(Es);
+    S.resid = A.take<double>(Es);
+    S.nc_cnt = A.take<int>(Es);
+    S.inv_cnt = A.take<int>(Es);
+    S.nonfinite = A.take<int>(Es);
   };
   auto plan_work = [&](Arena& A) {
+    const size_t Es = H->c.D.E;
+    const int gy_max = H->gy_red;
     Work& K = H->c.K;
     K.v = A.take<double>((size_t)D.ndof * Es);
     K.u = A.take<double>((size_t)D.ndof * Es);
@@ -1016,11 +1039,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.rho = A.take<double>(Es);
     K.alpha = A.take<double>(Es);
     K.beta = A.take<double>(Es);
-    K.resid = A.take<double>(Es);
     K.broken = A.take<int>(Es);
-    K.nc_cnt = A.take<int>(Es);
-    K.inv_cnt = A.take<int>(Es);
-    K.nonfinite = A.take<int>(Es);
   };
   Arena sa, wa;
   plan_state(sa);
@@ -1028,37 +1047,82 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   sa.cap = sa.off;
   wa.cap = wa.off;
   sa.off = wa.off = 0;
-  {
-    cudaError_t e1 = cudaMalloc(&H->state_mem, sa.cap);
-    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap) : e1;
-    if (e1 != cudaSuccess || e2 != cudaSuccess) {
-      ss_destroy(H);
-      return fail(SS_ENOMEM, "cudaMalloc state/work (%zu + %zu bytes) for %d envs failed", sa.cap,
-                  wa.cap, n_envs);
+  // auto wave cap: shrink the wave until workspace + all state blocks fit
+  if (p->wave_envs <= 0) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const double per_lane = (double)(sa.cap + wa.cap) / D.E;
+    const double state_lane = (double)sa.cap / D.E;
+    const double budget = 0.88 * (double)free_b;
+    if ((double)n_envs * per_lane > budget && D.E > 32) {
+      // work(E_w) + n_envs * state <= budget
+      const double wl = (budget - n_envs * state_lane) / (per_lane - state_lane);
+      int ew = (int)(wl / 32) * 32;
+      if (ew < 32) {
+        ss_destroy(H);
+        return fail(SS_ENOMEM, "%d envs do not fit in device memory even in waves", n_envs);
+      }
+      D.n_real = std::min(n_envs, ew);
+      D.E = pad_lanes(D.n_real);
+      D.W = D.E < 32 ? D.E : 32;
+      D.lgW = 0;
+      while ((1 << D.lgW) < D.W) ++D.lgW;
+      D.tiles = D.E / D.W;
+      H->c.D = D;
+      H->gy_red = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, kReduceBlocks).y;
+      sa = Arena();
+      wa = Arena();
+      plan_state(sa);
+      plan_work(wa);
+      sa.cap = sa.off;
+      wa.cap = wa.off;
+      sa.off = wa.off = 0;
     }
   }
-  sa.base = (char*)H->state_mem;
-  wa.base = (char*)H->work_mem;
-  plan_state(sa);
-  plan_work(wa);
-  H->bytes += sa.cap + wa.cap;
-  CK(cudaMemsetAsync(H->state_mem, 0, sa.cap, H->stream));
-  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap, H->stream));
-  // reference constructor defaults
+  H->n_waves = (n_envs + D.E - 1) / D.E;
+  const size_t sblock = sa.cap;
   {
-    const State& S = H->c.S;
+    cudaError_t e1 = cudaMalloc(&H->state_mem, sblock * H->n_waves);
+    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap) : e1;
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      cudaGetLastError();
+      ss_destroy(H);
+      return fail(SS_ENOMEM, "cudaMalloc state/work (%zu x %d + %zu bytes) for %d envs failed",
+                  sblock, H->n_waves, wa.cap, n_envs);
+    }
+  }
+  wa.base = (char*)H->work_mem;
+  plan_work(wa);
+  H->bytes += sblock * H->n_waves + wa.cap;
+  CK(cudaMemsetAsync(H->state_mem, 0, sblock * H->n_waves, H->stream));
+  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap, H->stream));
+  H->wave.assign(H->n_waves, H->c);
+  H->wave_graphs.assign(H->n_waves, std::vector<cudaGraphExec_t>(4, nullptr));
+  for (int w = 0; w < H->n_waves; ++w) {
+    Arena a;
+    a.base = (char*)H->state_mem + sblock * w;
+    plan_state(a);  // writes H->c.S
+    H->wave[w] = H->c;
+    H->wave[w].D.n_real = std::min(D.E, n_envs - w * D.E);
+    // reference constructor defaults
+    const State& S = H->wave[w].S;
     auto fill = [&](double* ptr, size_t n, double val) {
       if (n) k_fill<<<256, 256, 0, H->stream>>>(ptr, n, val);
     };
-    for (int b = 0; b < D.nb; ++b) fill(S.bquat + (size_t)(4 * b) * Es, Es, 1.0);
-    fill(S.quat, (size_t)D.nt * Es, 1.0);  // w component block [0][nt]
-    fill(S.dirs, (size_t)D.nd * Es, 1.0);  // x component block [0][nd]
-    fill(S.scale, (size_t)D.nd * Es, 1.0);
-    fill(S.live, (size_t)D.nch * Es, 1.0);
-    fill(S.target, (size_t)D.nch * Es, 1.0);
+    for (int b = 0; b < D.nb; ++b) fill(S.bquat + (size_t)(4 * b) * D.E, D.E, 1.0);
+    fill(S.quat, (size_t)D.nt * D.E, 1.0);  // w component block [0][nt]
+    fill(S.dirs, (size_t)D.nd * D.E, 1.0);  // x component block [0][nd]
+    fill(S.scale, (size_t)D.nd * D.E, 1.0);
+    fill(S.live, (size_t)D.nch * D.E, 1.0);
+    fill(S.target, (size_t)D.nch * D.E, 1.0);
   }
-  CK(cudaMalloc(&H->d_cmd, 8 * (size_t)std::max(1, n_envs * std::max(1, D.links))));
-  CK(cudaMemsetAsync(H->d_cmd, 0, 8 * (size_t)std::max(1, n_envs * std::max(1, D.links)), H->stream));
+  H->c = H->wave[0];
+  H->c.D.n_real = n_envs;  // handle-level: total real envs
+  {
+    const size_t cmd_n = (size_t)H->n_waves * H->c.D.E * std::max(1, D.links);
+    CK(cudaMalloc(&H->d_cmd, 8 * cmd_n));
+    CK(cudaMemsetAsync(H->d_cmd, 0, 8 * cmd_n, H->stream));
+  }
   CK(cudaStreamSynchronize(H->stream));
   *out = H;
   return SS_OK;
@@ -1067,14 +1131,16 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
 int ss_destroy(ss_handle* H) {
   if (!H) return SS_OK;
   cudaSetDevice(H->device);
-  for (auto& g : H->graphs)
-    if (g) cudaGraphExecDestroy(g);
+  for (auto& gw : H->wave_graphs)
+    for (auto& g : gw)
+      if (g) cudaGraphExecDestroy(g);
   if (H->topo_mem) cudaFree(H->topo_mem);
   if (H->state_mem) cudaFree(H->state_mem);
   if (H->work_mem) cudaFree(H->work_mem);
   if (H->d_cmd) cudaFree(H->d_cmd);
   if (H->d_stage) cudaFree(H->d_stage);
   if (H->plan_mem) cudaFree(H->plan_mem);
+  if (H->plan.dbg) cudaFree(H->plan.dbg);
   if (H->stream) cudaStreamDestroy(H->stream);
   delete H;
   return SS_OK;
@@ -1091,30 +1157,54 @@ static int ensure_stage(ss_handle* H, size_t bytes) {
   return SS_OK;
 }
 
+// split a global env range into (wave, first lane, count, offset in the range)
+struct WaveChunk {
+  int w, lane0, cnt, off;
+};
+static std::vector<WaveChunk> wave_chunks(const ss_handle* H, int env0, int n) {
+  std::vector<WaveChunk> out;
+  const int E = H->c.D.E;
+  int g = env0;
+  while (g < env0 + n) {
+    const int w = g / E, lane = g % E;
+    const int cnt = std::min(env0 + n - g, E - lane);
+    out.push_back({w, lane, cnt, g - env0});
+    g += cnt;
+  }
+  return out;
+}
+
 int ss_set_state(ss_handle* H, int env0, int n, const ss_state_view* v) {
   if (!H || !v) return fail(SS_EINVAL, "null argument");
   const Dims& D = H->c.D;
   if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
   if (n == 0) return SS_OK;
   CK(cudaSetDevice(H->device));
-  Field f[32];
-  int nf = 0;
-  state_fields(H, v, f, &nf);
-  for (int i = 0; i < nf; ++i) {
-    if (!f[i].host || f[i].A * f[i].B == 0) continue;
-    const size_t elem = f[i].is_int ? 4 : 8;
-    const size_t bytes = elem * (size_t)f[i].A * f[i].B * n;
-    int rc = ensure_stage(H, bytes);
-    if (rc) return rc;
-    CK(cudaMemcpyAsync(H->d_stage, f[i].host, bytes, cudaMemcpyHostToDevice, H->stream));
-    if (f[i].is_int)
-      k_scatter<int><<<512, 256, 0, H->stream>>>((int*)f[i].dev, (const int*)H->d_stage, n, f[i].A,
-                                                 f[i].B, f[i].swap, D.E, env0, D.n_real);
-    else
-      k_scatter<double><<<512, 256, 0, H->stream>>>((double*)f[i].dev, (const double*)H->d_stage, n,
-                                                    f[i].A, f[i].B, f[i].swap, D.E, env0, D.n_real);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(H->stream));
+  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
+    Field f[32];
+    int nf = 0;
+    state_fields(H, ch.w, v, f, &nf);
+    const int n_real_w = H->wave[ch.w].D.n_real;
+    for (int i = 0; i < nf; ++i) {
+      if (!f[i].host || f[i].A * f[i].B == 0) continue;
+      const size_t elem = f[i].is_int ? 4 : 8;
+      const size_t K = (size_t)f[i].A * f[i].B;
+      const size_t bytes = elem * K * ch.cnt;
+      int rc = ensure_stage(H, bytes);
+      if (rc) return rc;
+      CK(cudaMemcpyAsync(H->d_stage, (const char*)f[i].host + elem * K * ch.off, bytes,
+                         cudaMemcpyHostToDevice, H->stream));
+      if (f[i].is_int)
+        k_scatter<int><<<512, 256, 0, H->stream>>>((int*)f[i].dev, (const int*)H->d_stage, ch.cnt,
+                                                   f[i].A, f[i].B, f[i].swap, D.E, ch.lane0,
+                                                   n_real_w);
+      else
+        k_scatter<double><<<512, 256, 0, H->stream>>>((double*)f[i].dev, (const double*)H->d_stage,
+                                                      ch.cnt, f[i].A, f[i].B, f[i].swap, D.E,
+                                                      ch.lane0, n_real_w);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(H->stream));
+    }
   }
   return SS_OK;
 }
@@ -1125,25 +1215,30 @@ int ss_get_state(ss_handle* H, int env0, int n, ss_state_view* v) {
   if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
   if (n == 0) return SS_OK;
   CK(cudaSetDevice(H->device));
-  Field f[32];
-  int nf = 0;
-  state_fields(H, v, f, &nf);
-  for (int i = 0; i < nf; ++i) {
-    if (!f[i].host || f[i].A * f[i].B == 0) continue;
-    const size_t elem = f[i].is_int ? 4 : 8;
-    const size_t bytes = elem * (size_t)f[i].A * f[i].B * n;
-    int rc = ensure_stage(H, bytes);
-    if (rc) return rc;
-    if (f[i].is_int)
-      k_gather_state<int><<<512, 256, 0, H->stream>>>((int*)H->d_stage, (const int*)f[i].dev, n,
-                                                      f[i].A, f[i].B, f[i].swap, D.E, env0);
-    else
-      k_gather_state<double><<<512, 256, 0, H->stream>>>((double*)H->d_stage,
-                                                         (const double*)f[i].dev, n, f[i].A,
-                                                         f[i].B, f[i].swap, D.E, env0);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(f[i].host, H->d_stage, bytes, cudaMemcpyDeviceToHost, H->stream));
-    CK(cudaStreamSynchronize(H->stream));
+  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
+    Field f[32];
+    int nf = 0;
+    state_fields(H, ch.w, v, f, &nf);
+    for (int i = 0; i < nf; ++i) {
+      if (!f[i].host || f[i].A * f[i].B == 0) continue;
+      const size_t elem = f[i].is_int ? 4 : 8;
+      const size_t K = (size_t)f[i].A * f[i].B;
+      const size_t bytes = elem * K * ch.cnt;
+      int rc = ensure_stage(H, bytes);
+      if (rc) return rc;
+      if (f[i].is_int)
+        k_gather_state<int><<<512, 256, 0, H->stream>>>((int*)H->d_stage, (const int*)f[i].dev,
+                                                        ch.cnt, f[i].A, f[i].B, f[i].swap, D.E,
+                                                        ch.lane0);
+      else
+        k_gather_state<double><<<512, 256, 0, H->stream>>>((double*)H->d_stage,
+                                                           (const double*)f[i].dev, ch.cnt, f[i].A,
+                                                           f[i].B, f[i].swap, D.E, ch.lane0);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync((char*)f[i].host + elem * K * ch.off, H->d_stage, bytes,
+                         cudaMemcpyDeviceToHost, H->stream));
+      CK(cudaStreamSynchronize(H->stream));
+    }
   }
   return SS_OK;
 }
@@ -1154,16 +1249,21 @@ static int step_impl(ss_handle* H, const double* cmd, int on_device, int latency
   CK(cudaSetDevice(H->device));
   const Dims& D = H->c.D;
   const int has_cmd = cmd != nullptr && D.nch > 0;
-  cudaGraphExec_t g;
-  int rc = get_graph(H, has_cmd, latency ? 1 : 0, &g);
-  if (rc) return rc;
-  const size_t frame_bytes = 8 * (size_t)D.n_real * D.links;
-  for (int f = 0; f < n_frames; ++f) {
-    if (has_cmd)
-      CK(cudaMemcpyAsync(H->d_cmd, cmd + (size_t)f * D.n_real * D.links, frame_bytes,
-                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, H->stream));
-    CK(cudaGraphLaunch(g, H->stream));
+  const int links = std::max(1, D.links);
+  for (int w = 0; w < H->n_waves; ++w) {
+    cudaGraphExec_t g;
+    int rc = get_graph(H, w, has_cmd, latency ? 1 : 0, &g);
+    if (rc) return rc;
   }
+  for (int f = 0; f < n_frames; ++f) {
+    // every env of the frame, wave after wave (envs are independent)
+    if (has_cmd)
+      CK(cudaMemcpyAsync(H->d_cmd, cmd + (size_t)f * D.n_real * D.links,
+                         8 * (size_t)D.n_real * D.links,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, H->stream));
+    for (int w = 0; w < H->n_waves; ++w) CK(cudaGraphLaunch(H->wave_graphs[w][(has_cmd ? 2 : 0) | (latency ? 1 : 0)], H->stream));
+  }
+  (void)links;
   return SS_OK;
 }
 
@@ -1181,11 +1281,14 @@ int ss_get_stats(ss_handle* H, int env0, int n, ss_env_stats* out) {
   CK(cudaSetDevice(H->device));
   std::vector<int> nc(n), inv(n), nf(n);
   std::vector<double> res(n);
-  const Work& K = H->c.K;
-  CK(cudaMemcpyAsync(nc.data(), K.nc_cnt + env0, 4 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
-  CK(cudaMemcpyAsync(inv.data(), K.inv_cnt + env0, 4 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
-  CK(cudaMemcpyAsync(nf.data(), K.nonfinite + env0, 4 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
-  CK(cudaMemcpyAsync(res.data(), K.resid + env0, 8 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
+  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
+    const State& S = H->wave[ch.w].S;
+    const size_t c4 = 4 * (size_t)ch.cnt;
+    CK(cudaMemcpyAsync(nc.data() + ch.off, S.nc_cnt + ch.lane0, c4, cudaMemcpyDeviceToHost, H->stream));
+    CK(cudaMemcpyAsync(inv.data() + ch.off, S.inv_cnt + ch.lane0, c4, cudaMemcpyDeviceToHost, H->stream));
+    CK(cudaMemcpyAsync(nf.data() + ch.off, S.nonfinite + ch.lane0, c4, cudaMemcpyDeviceToHost, H->stream));
+    CK(cudaMemcpyAsync(res.data() + ch.off, S.resid + ch.lane0, 2 * c4, cudaMemcpyDeviceToHost, H->stream));
+  }
   CK(cudaStreamSynchronize(H->stream));
   const Par& P = H->c.p;
   for (int i = 0; i < n; ++i) {
@@ -1208,8 +1311,11 @@ int ss_get_com(ss_handle* H, int env0, int n, double* out) {
   CK(cudaSetDevice(H->device));
   int rc = ensure_stage(H, 24 * (size_t)n);
   if (rc) return rc;
-  k_com<<<(n + 127) / 128, 128, 0, H->stream>>>(H->c, env0, n, H->d_stage);
-  CK(cudaGetLastError());
+  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
+    k_com<<<(ch.cnt + 127) / 128, 128, 0, H->stream>>>(H->wave[ch.w], ch.lane0, ch.cnt,
+                                                       H->d_stage + 3 * (size_t)ch.off);
+    CK(cudaGetLastError());
+  }
   CK(cudaMemcpyAsync(out, H->d_stage, 24 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
   CK(cudaStreamSynchronize(H->stream));
   return SS_OK;
@@ -1228,9 +1334,9 @@ int ss_launches_per_frame(ss_handle* H) {
   if (!H) return 0;
   if (!H->launches) {
     cudaGraphExec_t g;
-    if (get_graph(H, 1, 1, &g)) return -1;
+    if (get_graph(H, 0, 1, 1, &g)) return -1;
   }
-  return H->launches;
+  return H->launches * H->n_waves;
 }
 
 int64_t ss_device_bytes(ss_handle* H) { return H ? (int64_t)H->bytes : 0; }
@@ -1248,6 +1354,7 @@ int ss_solver_info(ss_handle* H, int* info) {
   info[1] = H->use_cluster ? H->plan.C : 0;
   info[2] = H->use_cluster ? 8 * H->plan.smem_doubles : 0;
   info[3] = H->c.D.E;
+  info[4] = H->n_waves;
   return SS_OK;
 }
 
@@ -1272,9 +1379,11 @@ int ss_profile_frames(ss_handle* H, const double* commands, int latency, int n_f
       CK(cudaMemcpyAsync(H->d_cmd, commands + (size_t)f * D.n_real * D.links, frame_bytes,
                          cudaMemcpyHostToDevice, H->stream));
     Prof prof;
-    int nl = 0;
-    int rc = enqueue_frame(H, has_cmd, latency, &nl, &prof);
-    if (rc) return rc;
+    for (int w = 0; w < H->n_waves; ++w) {
+      int nl = 0;
+      int rc = enqueue_frame(H, w, has_cmd, latency, &nl, &prof);
+      if (rc) return rc;
+    }
     CK(cudaStreamSynchronize(H->stream));
     for (auto& e : prof.ev) {
       float ms = 0.f;

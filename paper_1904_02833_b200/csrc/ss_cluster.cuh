@@ -1053,6 +1053,6 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
       for (int k = 0; k < 6; ++k) c.K.v[IX(o + k)] = sb[L.oV + 3 * nP + 6 * lb + k];
     }
   }
-  if (rank == 0 && tid == 0) c.K.resid[env] = resid;
+  if (rank == 0 && tid == 0) c.S.resid[env] = resid;
   cl.sync();  // no CTA may exit while peers can still access its shared memory
 }

@@ -69,6 +69,9 @@ struct State {
   double* warm;                         // [3][nw]
   int* warm_valid;                      // [nw]
   double* time;                         // [1]
+  // per-frame statistics (StepStats, solver.py:142-151), per env
+  double* resid;                        // [1]
+  int *nc_cnt, *inv_cnt, *nonfinite;    // [1]
 };
 
 // per-substep workspace, [item][E]
@@ -88,8 +91,8 @@ struct Work {
   double *x, *r, *z, *p, *ap, *az, *d;  // [m]
   double* part;             // [gy_red][E]
   int* cnt;                 // [tiles]
-  double *rho, *alpha, *beta, *resid;  // [E]
-  int *broken, *nc_cnt, *inv_cnt, *nonfinite;  // [E]
+  double *rho, *alpha, *beta;  // [E]
+  int* broken;                  // [E]
 };
 
 struct Ctx {
@@ -265,9 +268,9 @@ __global__ void k_frame_begin(const Ctx c, const double* __restrict__ cmd, int h
   const int n = c.D.links > 0 ? c.D.links : 1;
   FOR_ITEMS(i, n) {
     if (i == 0) {
-      c.K.nc_cnt[env] = 0;
-      c.K.inv_cnt[env] = 0;
-      c.K.nonfinite[env] = 0;
+      c.S.nc_cnt[env] = 0;
+      c.S.inv_cnt[env] = 0;
+      c.S.nonfinite[env] = 0;
     }
     if (i < c.D.links) {
       if (has_cmd) {
@@ -451,7 +454,7 @@ __global__ void k_slots(const Ctx c) {
     c.K.lamc[IX(s)] = lam_n;
     c.K.lamc[IX(ns + s)] = lam_f0;
     c.K.lamc[IX(2 * ns + s)] = lam_f1;
-    if (present) atomicAdd(&c.K.nc_cnt[env], 1);
+    if (present) atomicAdd(&c.S.nc_cnt[env], 1);
   }
 }
 
@@ -834,7 +837,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_eval_tet(const Ctx c) {
 #pragma unroll
     for (int i = 0; i < 6; ++i) lam6[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
     tet_jt<EXACT>(c, t, env, T, Ri, lam6);
-    if (inv) atomicAdd(&c.K.inv_cnt[env], 1);
+    if (inv) atomicAdd(&c.S.inv_cnt[env], 1);
   }
 }
 
@@ -1718,7 +1721,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_final(const Ctx c, int do
     }
   }
   double rz;
-  if (reduce_env(c, part, &rz)) c.K.resid[env] = sqrt(0.0 > rz ? 0.0 : rz);
+  if (reduce_env(c, part, &rz)) c.S.resid[env] = sqrt(0.0 > rz ? 0.0 : rz);
 }
 
 // set_velocities + integrate_pose + quat_step (state.py:155-160, 171-192)
@@ -1738,7 +1741,7 @@ __global__ void k_integrate(const Ctx c) {
         c.S.pos[IX(3 * it + a)] = x;
         bad |= !isfinite(x);
       }
-      if (bad) c.K.nonfinite[env] = 1;
+      if (bad) c.S.nonfinite[env] = 1;
     } else {
       const int b = it - P, o = c.D.bd0 + 6 * b;
       double w[3];

@@ -45,6 +45,8 @@ class SolverConfig:
     exact_jacobian: bool = False
     # B200 extension: Newton-loop solver "auto" | "streaming" | "cluster"
     solver: str = "auto"
+    # B200 extension: envs per wave (0 = auto from device memory)
+    wave_envs: int = 0
 
     @property
     def h(self) -> float:
@@ -248,10 +250,10 @@ class BatchedSimulator:
 
     @property
     def solver_info(self) -> dict:
-        info = (C.c_int * 4)()
+        info = (C.c_int * 5)()
         _native.check(_native.lib().ss_solver_info(self._ensure(), info))
         return {"cluster": bool(info[0]), "cluster_size": info[1], "smem_bytes": info[2],
-                "env_lanes": info[3]}
+                "env_lanes": info[3], "waves": info[4]}
 
     @property
     def launches_per_frame(self) -> int:

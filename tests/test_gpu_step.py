@@ -165,3 +165,45 @@ def test_cluster_and_streaming_agree():
         assert_state_close({k: v[e] for k, v in a.items()}, {k: v[e] for k, v in b.items()},
                            tol={"positions": 1e-9, "velocities": 1e-7, "pressures": 0.0},
                            keys=("positions", "velocities", "pressures"))
+
+
+@pytest.mark.gpu
+def test_waves_match_oracle_per_env(oracle_mod):
+    """10 envs run as 3 waves of 4 lanes (last wave 2 real + 2 padding):
+    state I/O, commands, stats and COM are routed to the right wave/lane and
+    each env equals its own single-env oracle run."""
+    n = 10
+    parts, cfg = scene_parts("S")
+    cfg.wave_envs = 4
+    sim = M.BatchedSimulator(n, config=cfg, **parts)
+    assert sim.solver_info["waves"] == 3 and sim.solver_info["env_lanes"] == 4
+    rng = np.random.default_rng(7)
+    bias = rng.uniform(-0.5, 0.5, n)
+    ors = [oracle_mod.OracleSim(config=cfg, **parts) for _ in range(n)]
+    # perturb envs 3..8 (crosses two wave boundaries) through a ranged set_state
+    st = sim.get_state_arrays()
+    kick = rng.normal(0.0, 0.05, st["velocities"][3:9].shape)
+    st["velocities"][3:9] += kick
+    sim.set_state_arrays({"velocities": st["velocities"][3:9]}, env0=3, n=6)
+    for e in range(3, 9):
+        s0 = ors[e].get_state()
+        s0["velocities"] = s0["velocities"] + kick[e - 3]
+        ors[e].set_state(s0)
+    for i in range(3):
+        cmds = np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4)
+                         for b in bias])
+        sim.step(cmds, latency=True)
+        for e in range(n):
+            ors[e].step(cmds[e], True)
+    got = sim.get_state_arrays()
+    for e in range(n):
+        assert_state_close({k: v[e] for k, v in got.items()}, ors[e].get_state(),
+                           tol={"positions": 1e-9, "velocities": 1e-6, "pressures": 0.0},
+                           keys=("positions", "velocities", "pressures"), what=f"env {e}")
+    assert [s.contact_count for s in sim.get_stats()] == [o.stats().contact_count for o in ors]
+    # COM per env: a single-env device run of each env's final state
+    com = sim.center_of_mass()
+    for e in (0, 4, 9):
+        one = M.BatchedSimulator(1, config=cfg, **parts)
+        one.set_state_arrays({k: v[e] for k, v in got.items()})
+        assert np.array_equal(one.center_of_mass()[0], com[e]), f"env {e}"
