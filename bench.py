@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--profile-frames", type=int, default=2)
     ap.add_argument("--cpu-frames", type=int, default=6, help="oracle frames per host core")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scene", default="S", choices=["S", "H"],
+                    help="S: the snake (configs 3/4); H: the 1M-tet snake, 1 env per GPU "
+                         "(config 5, replicas only)")
     ap.add_argument("--wave-envs", type=int, default=0,
                     help="envs per wave (SolverConfig.wave_envs; 0 = auto)")
     ap.add_argument("--solver", default="auto", choices=["auto", "streaming", "cluster"],
@@ -53,14 +56,21 @@ def parse():
     return ap.parse_args()
 
 
-def env_commands(n_envs: int, frames: int, first_frame: int, env0: int = 0):
+H_SCENE = dict(sections=101, width_nodes=26, height_nodes=21)
+
+
+def env_commands(n_envs: int, frames: int, first_frame: int, env0: int = 0,
+                 default_gait: bool = False):
     """[frames, n_envs, 4] gait commands: per-env turn bias and time offset
-    from the conftest seed."""
+    from the conftest seed; default_gait: the
+    GaitParams defaults for every env (configs 2 and 5)."""
     import paper_1904_02833_b200 as M
     sc = M.SceneConfig()
     # one (bias, t0) row per env: env e's draw does not depend on the sharding
     draws = np.random.default_rng(20260817).uniform(size=(env0 + n_envs, 2))[env0:]
     bias, t0 = draws[:, 0] - 0.5, 0.5 * draws[:, 1]
+    if default_gait:
+        bias, t0 = np.zeros(n_envs), np.zeros(n_envs)
     w = 2.0 * np.pi * sc.frequency
     i = np.arange(4)
     t = t0[None, :] + (first_frame + np.arange(frames))[:, None] * sc.dt
@@ -220,18 +230,25 @@ def main():
     from paper_1904_02833_b200 import roofline
     from paper_1904_02833_b200.distributed import env_slice, gather_env_stats, max_over_ranks
 
-    if args.total_envs:
+    hires = args.scene == "H"
+    if hires:
+        # config 5: one 1M-tet snake per GPU (replicas only)
+        env0, n = rank, 1
+        total, scaling = world, "weak"
+    elif args.total_envs:
         env0, n = env_slice(args.total_envs, world, rank)
         total, scaling = args.total_envs, "strong"
     else:
         env0, n = rank * args.envs, args.envs
         total, scaling = world * args.envs, "weak"
-    model = M.build_snake(M.SceneConfig(), n_envs=n, device=local)
+    scene = M.SceneConfig(**H_SCENE) if hires else M.SceneConfig()
+    model = M.build_snake(scene, n_envs=n, device=local)
     sim = model.sim
     sim.config.solver = args.solver
     sim.config.wave_envs = args.wave_envs
     K, W = args.steps, args.warmup
-    cmds = env_commands(n, W + K, 0, env0=env0)
+    gcmd = lambda nn, fr, f0, env0=0: env_commands(nn, fr, f0, env0=env0, default_gait=hires)  # noqa: E731
+    cmds = gcmd(n, W + K, 0, env0=env0)
     d_cmds = torch.from_numpy(cmds).to(f"cuda:{local}")
     stream = torch.cuda.ExternalStream(sim.stream, device=f"cuda:{local}")
     frame_elems = n * 4
@@ -257,7 +274,7 @@ def main():
     finite = all(s.finite for s in sim.get_stats())
 
     # ---- e2e through the public API: host commands (pinned) in, COM out
-    host_cmd = torch.from_numpy(env_commands(n, K, W + K, env0=env0)).pin_memory()
+    host_cmd = torch.from_numpy(gcmd(n, K, W + K, env0=env0)).pin_memory()
     com_bytes = n * 3 * 8
     torch.cuda.synchronize()
     if dist:
@@ -271,7 +288,7 @@ def main():
     all_com = gather_env_stats(com, total, device=f"cuda:{local}")
 
     # ---- live per-kernel timing (CUDA events around each launch)
-    prof_cmds = env_commands(n, args.profile_frames, W + 2 * K, env0=env0)
+    prof_cmds = gcmd(n, args.profile_frames, W + 2 * K, env0=env0)
     prof = sim.profile_frames(prof_cmds, True, args.profile_frames)
     step_ms_prof = sum(v[0] for v in prof.values()) / args.profile_frames
     top = max(prof, key=lambda k: prof[k][0])
@@ -287,7 +304,7 @@ def main():
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and not hires:  # traffic.json holds the S-scene capture
         tj = json.load(open(tp))
         if tj.get(top) is not None:
             # scaled to the envs of one launch
@@ -305,10 +322,13 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD if total == 1024 * world and scaling == "weak" else
-                   f"{total} independent snakes batched on {world}xB200", "envs_per_gpu": n, "global_envs": total,
+        "config": {"workload": WORKLOAD if total == 1024 * world and scaling == "weak" and
+                   not hires else (f"1M-tet snake (config 5, {H_SCENE}), 1 per GPU, default gait"
+                                   if hires else f"{total} independent snakes batched on "
+                                   f"{world}xB200"), "envs_per_gpu": n, "global_envs": total,
                    "frame_dt_s": 1 / 60, "substeps": 2, "newton": 4, "pcr": 20,
-                   "gait": "default, per-env turn bias U(-0.5,0.5), t0 U(0,0.5s), seed 20260817",
+                   "gait": "GaitParams defaults" if hires else
+                           "default, per-env turn bias U(-0.5,0.5), t0 U(0,0.5s), seed 20260817",
                    "l2": "no flush: per-step working set "
                          f"{sim.device_bytes / 1e9:.1f} GB >> 126 MB L2",
                    "parallelism": f"env-sharded x{world}",
@@ -331,7 +351,18 @@ def main():
                        "residual": stats[0].residual},
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    if hires and not args.no_cpu_baseline:
+        from oracle.oracle import OracleSim
+        from paper_1904_02833_b200.model import build_scene_parts
+        parts, *_ = build_scene_parts(scene)
+        o = OracleSim(config=scene.solver_config(), **parts)
+        t = time.perf_counter()
+        o.step(cmds[0, 0], True)
+        secs = time.perf_counter() - t
+        line["cpu_baseline"] = {"value": 1.0 / secs, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"oracle C port, 1 frame of the 1M-tet snake from rest "
+                                          f"({secs:.1f} s)"}
+    elif not args.no_cpu_baseline:
         rate, cores, secs = cpu_oracle_rate(args.cpu_frames)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"oracle C port, {cores} snakes x {args.cpu_frames} "

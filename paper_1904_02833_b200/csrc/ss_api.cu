@@ -1014,9 +1014,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.u = A.take<double>((size_t)D.ndof * Es);
     K.ang_inv = A.take<double>(9 * (size_t)D.nb * Es);
     K.res = A.take<double>((size_t)D.ms * Es);
-    K.tR = A.take<double>(9 * (size_t)D.nt * Es);
     K.tS = A.take<double>(6 * (size_t)D.nt * Es);
-    K.tK = A.take<double>(6 * (size_t)D.nt * Es);
     K.tC = A.take<double>(12 * (size_t)D.nt * Es);
     K.rw = A.take<double>(3 * (size_t)D.na * Es);
     K.hJ = A.take<double>(60 * (size_t)D.nh * Es);
@@ -1312,7 +1310,8 @@ int ss_get_com(ss_handle* H, int env0, int n, double* out) {
   int rc = ensure_stage(H, 24 * (size_t)n);
   if (rc) return rc;
   for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
-    k_com<<<(ch.cnt + 127) / 128, 128, 0, H->stream>>>(H->wave[ch.w], ch.lane0, ch.cnt,
+    const int L = H->c.D.W;
+    k_com<<<(ch.cnt + L - 1) / L, 256, 0, H->stream>>>(H->wave[ch.w], ch.lane0, ch.cnt,
                                                        H->d_stage + 3 * (size_t)ch.off);
     CK(cudaGetLastError());
   }

@@ -651,15 +651,18 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
     switch (el.fam) {
       case CF_TET: {
         const int nt = c.D.nt, t = el.g;
+        TetC T;
+        tet_load(c, t, env, T);  // R, K^-1 rebuilt from q and S
+        const int sym[6] = {0, 4, 8, 5, 2, 1};
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-          sb[L.oJR + k * L.MT + el.le] = c.K.tR[IX(k * nt + t)];
+          sb[L.oJR + k * L.MT + el.le] = T.R[k];
           sb[L.oRi + k * L.MT + el.le] = c.T.t_rinv[k * nt + t];
         }
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-          sb[L.oJS + k * L.MT + el.le] = c.K.tS[IX(k * nt + t)];
-          sb[L.oJK + k * L.MT + el.le] = c.K.tK[IX(k * nt + t)];
+          sb[L.oJS + k * L.MT + el.le] = T.S[sym[k]];
+          sb[L.oJK + k * L.MT + el.le] = T.K[sym[k]];
         }
 #pragma unroll
         for (int k = 0; k < 3; ++k) sb[L.oE3 + k * L.MT + el.le] = c.T.t_e3[k * nt + t];

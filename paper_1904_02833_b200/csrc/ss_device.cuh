@@ -79,7 +79,7 @@ struct Work {
   double *v, *u;            // [ndof]
   double* ang_inv;          // [9][nb]
   double* res;              // [ms] (tet rows unused: derived from S)
-  double *tR, *tS, *tK;     // [9][nt] [6][nt] [6][nt] compact tet Jacobian: R, sym(R^T F), K^-1
+  double* tS;               // [6][nt] compact tet Jacobian sym(R^T F) (R from S.quat)
   double* tC;               // [12][nt] per-tet J^T x column sums (gather input)
   double* rw;               // [3][na]
   double* hJ;               // [60][nh]
@@ -510,6 +510,32 @@ DI void tet_col(const TetC& T, const double* wv, int a, double* o) {
 }
 
 // polar decomposition + strain + K^-1; returns det(F) <= 0
+// K^-1 with K = tr(S) I - S (+1e-14 on the diagonal), by cofactors
+// (numba_backend.py:221-240). Pure function of S: the compact tet Jacobian
+// stores S only and every consumer recomputes K^-1 bitwise.
+DI void tet_kinv(const double* S, double* Ki) {
+  const double trS = S[0] + S[4] + S[8];
+  double K[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) K[i] = -S[i];
+  K[0] += trS + 1e-14;
+  K[4] += trS + 1e-14;
+  K[8] += trS + 1e-14;
+  double detK = K[0] * (K[4] * K[8] - K[5] * K[7]) - K[1] * (K[3] * K[8] - K[5] * K[6]) +
+                K[2] * (K[3] * K[7] - K[4] * K[6]);
+  if (fabs(detK) < 1e-30) detK = detK >= 0 ? 1e-30 : -1e-30;
+  const double id = 1.0 / detK;
+  Ki[0] = (K[4] * K[8] - K[5] * K[7]) * id;
+  Ki[1] = (K[2] * K[7] - K[1] * K[8]) * id;
+  Ki[2] = (K[1] * K[5] - K[2] * K[4]) * id;
+  Ki[3] = (K[5] * K[6] - K[3] * K[8]) * id;
+  Ki[4] = (K[0] * K[8] - K[2] * K[6]) * id;
+  Ki[5] = (K[2] * K[3] - K[0] * K[5]) * id;
+  Ki[6] = (K[3] * K[7] - K[4] * K[6]) * id;
+  Ki[7] = (K[1] * K[6] - K[0] * K[7]) * id;
+  Ki[8] = (K[0] * K[4] - K[1] * K[3]) * id;
+}
+
 DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, int maxiter,
                      TetC& T, int* iters) {
   double F[9];
@@ -574,27 +600,7 @@ DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, i
     const double m12 = 0.5 * (S[5] + S[7]);
     S[5] = m12; S[7] = m12;
   }
-  const double trS = S[0] + S[4] + S[8];
-  double K[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) K[i] = -S[i];
-  K[0] += trS + 1e-14;
-  K[4] += trS + 1e-14;
-  K[8] += trS + 1e-14;
-  double detK = K[0] * (K[4] * K[8] - K[5] * K[7]) - K[1] * (K[3] * K[8] - K[5] * K[6]) +
-                K[2] * (K[3] * K[7] - K[4] * K[6]);
-  if (fabs(detK) < 1e-30) detK = detK >= 0 ? 1e-30 : -1e-30;
-  const double id = 1.0 / detK;
-  double* Ki = T.K;
-  Ki[0] = (K[4] * K[8] - K[5] * K[7]) * id;
-  Ki[1] = (K[2] * K[7] - K[1] * K[8]) * id;
-  Ki[2] = (K[1] * K[5] - K[2] * K[4]) * id;
-  Ki[3] = (K[5] * K[6] - K[3] * K[8]) * id;
-  Ki[4] = (K[0] * K[8] - K[2] * K[6]) * id;
-  Ki[5] = (K[2] * K[3] - K[0] * K[5]) * id;
-  Ki[6] = (K[3] * K[7] - K[4] * K[6]) * id;
-  Ki[7] = (K[1] * K[6] - K[0] * K[7]) * id;
-  Ki[8] = (K[0] * K[4] - K[1] * K[3]) * id;
+  tet_kinv(S, T.K);
   return detF <= 0.0 ? 1 : 0;
 }
 
@@ -608,38 +614,33 @@ DI void tet_res(const TetC& T, double* r) {
   r[5] = T.S[1];
 }
 
-// compact storage: R (9), S (6 unique), K^-1 (6 unique); both symmetric
-// bitwise (S symmetrised explicitly; K^-1 cofactors of a symmetric K)
+// compact storage: S (6 unique, symmetrised explicitly in tet_eval_core).
+// R = quat_to_mat(q) of the tet's persistent quaternion (tet_eval_core builds
+// R from exactly that q) and K^-1 = tet_kinv(S) are recomputed bitwise on
+// load: 10 doubles per tet read instead of 21.
 DI void tet_store(const Ctx& c, int t, int env, const TetC& T) {
   const int E = c.D.E, nt = c.D.nt;
-#pragma unroll
-  for (int k = 0; k < 9; ++k) c.K.tR[IX(k * nt + t)] = T.R[k];
   const int sym[6] = {0, 4, 8, 5, 2, 1};
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    c.K.tS[IX(k * nt + t)] = T.S[sym[k]];
-    c.K.tK[IX(k * nt + t)] = T.K[sym[k]];
-  }
+  for (int k = 0; k < 6; ++k) c.K.tS[IX(k * nt + t)] = T.S[sym[k]];
 }
-DI void tet_load(const Ctx& c, int t, int env, TetC& T) {
-  const int E = c.D.E, nt = c.D.nt;
-#pragma unroll
-  for (int k = 0; k < 9; ++k) T.R[k] = c.K.tR[IX(k * nt + t)];
-  double s[6], q[6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    s[k] = c.K.tS[IX(k * nt + t)];
-    q[k] = c.K.tK[IX(k * nt + t)];
-  }
+DI void tet_unpack(const double* q, const double* s, TetC& T) {
+  quat_to_mat(q[0], q[1], q[2], q[3], T.R);
   // [0 1 2; 3 4 5; 6 7 8] <- (00 11 22 12 02 01)
   T.S[0] = s[0]; T.S[4] = s[1]; T.S[8] = s[2];
   T.S[5] = s[3]; T.S[7] = s[3];
   T.S[2] = s[4]; T.S[6] = s[4];
   T.S[1] = s[5]; T.S[3] = s[5];
-  T.K[0] = q[0]; T.K[4] = q[1]; T.K[8] = q[2];
-  T.K[5] = q[3]; T.K[7] = q[3];
-  T.K[2] = q[4]; T.K[6] = q[4];
-  T.K[1] = q[5]; T.K[3] = q[5];
+  tet_kinv(T.S, T.K);
+}
+DI void tet_load(const Ctx& c, int t, int env, TetC& T) {
+  const int E = c.D.E, nt = c.D.nt;
+  double q[4], s[6];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) s[k] = c.K.tS[IX(k * nt + t)];
+  tet_unpack(q, s, T);
 }
 DI void tet_rinv(const Ctx& c, int t, double* Ri) {
   const int nt = c.D.nt;
@@ -1771,12 +1772,17 @@ __global__ void k_integrate(const Ctx c) {
 }
 
 // center_of_mass (state.py:285-292), one thread per env (readback only)
-__global__ void k_com(const Ctx c, int env0, int n, double* out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  const int env = env0 + e, E = c.D.E;
+// mass-weighted centre of mass (state.py:285-292). Block = L env lanes x
+// (256/L) particle groups; group g sums particles g, g+G, ... and the groups
+// are combined in a fixed order (deterministic for any env count).
+__global__ void __launch_bounds__(256) k_com(const Ctx c, int env0, int n, double* out) {
+  __shared__ double sh[4][256];
+  const int L = c.D.W, G = 256 / L;
+  const int lane = threadIdx.x % L, g = threadIdx.x / L;
+  const int e = blockIdx.x * L + lane;
+  const int env = env0 + (e < n ? e : 0), E = c.D.E;
   double tot = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
-  for (int i = 0; i < c.D.P; ++i) {
+  for (int i = g; i < c.D.P; i += G) {
     const double im = c.T.inv_mass[i];
     if (!(im > 0.0)) continue;
     const double m = 1.0 / im;
@@ -1785,6 +1791,21 @@ __global__ void k_com(const Ctx c, int env0, int n, double* out) {
     cy += m * c.S.pos[IX(3 * i + 1)];
     cz += m * c.S.pos[IX(3 * i + 2)];
   }
+  sh[0][threadIdx.x] = tot;
+  sh[1][threadIdx.x] = cx;
+  sh[2][threadIdx.x] = cy;
+  sh[3][threadIdx.x] = cz;
+  __syncthreads();
+  for (int h = G / 2; h > 0; h >>= 1) {
+    if (g < h)
+      for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + h * L];
+    __syncthreads();
+  }
+  if (g != 0 || e >= n) return;
+  tot = sh[0][lane];
+  cx = sh[1][lane];
+  cy = sh[2][lane];
+  cz = sh[3][lane];
   for (int b = 0; b < c.D.nb; ++b) {
     const double m = 1.0 / c.T.body_inv_mass[b];
     tot += m;

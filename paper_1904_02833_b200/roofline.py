@@ -28,13 +28,16 @@ def dims_of(sim) -> dict:
 
 def bytes_per_launch_per_env(kernel: str, d: dict, nc: float) -> float:
     rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches
-    jc = F8 * 21 * d["nt"]                       # compact tet J: R(9) S(6) K^-1(6)
+    jc = F8 * 10 * d["nt"]                       # compact tet J: quat(4) S(6); R, K^-1 rebuilt
     tc = F8 * 12 * d["nt"]                       # tet column sums J^T x
     small_j = F8 * (3 * d["nd"] + 3 * d["na"] + 60 * d["nh"] + 18 * d["nw"])
     flags = 4 * d["ns"] + F8 * 2 * nc            # present flags, actf/dynn of present
     if kernel == "k_pcr_step":
-        # read x p r ap d, write x r z (rows); compact J; write tC
-        return F8 * 8 * rows + jc + tc + flags
+        # read x p r ap d, write x r z (rows)
+        return F8 * 8 * rows + flags
+    if kernel == "k_tet_jt":
+        # z of the tet rows, compact J; write tC
+        return F8 * 6 * d["nt"] + jc + tc
     if kernel == "k_pcr_dir":
         # read z az p ap d, write p ap
         return F8 * 7 * rows + flags
@@ -52,7 +55,7 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float) -> float:
         # read x r z p ap d + lam, write lam + dlam, compact J, write tC
         return F8 * 9 * rows + jc + tc + flags
     if kernel == "k_eval_tet":
-        # positions once, quats r/w, compact J + diag + tC written, lam read
-        return F8 * (3 * d["P"] + 8 * d["nt"] + 21 * d["nt"] + 6 * d["nt"] + 12 * d["nt"]
+        # positions once, quats r/w, S + diag + tC written, lam read
+        return F8 * (3 * d["P"] + 8 * d["nt"] + 6 * d["nt"] + 6 * d["nt"] + 12 * d["nt"]
                      + 6 * d["nt"])
     return 0.0

@@ -201,9 +201,10 @@ def test_waves_match_oracle_per_env(oracle_mod):
                            tol={"positions": 1e-9, "velocities": 1e-6, "pressures": 0.0},
                            keys=("positions", "velocities", "pressures"), what=f"env {e}")
     assert [s.contact_count for s in sim.get_stats()] == [o.stats().contact_count for o in ors]
-    # COM per env: a single-env device run of each env's final state
+    # COM per env equals a single-env device run of that env's final state
+    # (the particle-sum tree depends on the lane count: equal to rounding)
     com = sim.center_of_mass()
     for e in (0, 4, 9):
         one = M.BatchedSimulator(1, config=cfg, **parts)
         one.set_state_arrays({k: v[e] for k, v in got.items()})
-        assert np.array_equal(one.center_of_mass()[0], com[e]), f"env {e}"
+        assert np.allclose(one.center_of_mass()[0], com[e], rtol=1e-14, atol=1e-15), f"env {e}"

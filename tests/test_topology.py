@@ -60,3 +60,20 @@ def test_snake_counts_match_survey():
 def test_degenerate_grid_rejected():
     with pytest.raises(ValueError):
         M.build_snake(M.SceneConfig(width_nodes=4))
+
+
+def test_hires_topology_bit_identical():
+    """Config 5 (1,000,000 tets): every topology array equals the reference
+    builder's (digests in tests/golden/step_H.npz)."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "step_H.npz")
+    if not os.path.exists(path):
+        pytest.skip("step_H.npz not generated")
+    g = np.load(path)
+    model = M.build_snake(M.SceneConfig(sections=101, width_nodes=26, height_nodes=21))
+    assert model.sim.tetras.count == 1_000_000
+    arrays = _arrays(model)
+    keys = sorted(k.split(":", 1)[1] for k in g.files if k.startswith("topo:"))
+    assert keys == sorted(arrays)
+    for k in keys:
+        assert _digest(arrays[k]) == str(g[f"topo:{k}"]), f"H {k} differs from reference"

@@ -13,8 +13,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--envs", type=int, default=1024)
 ap.add_argument("--frames", type=int, default=2)
 ap.add_argument("--warmup", type=int, default=1)
+ap.add_argument("--scene", default="S", choices=["S", "H"])
 a = ap.parse_args()
-model = M.build_snake(M.SceneConfig(), n_envs=a.envs)
+if a.scene == "H":
+    a.envs = 1
+scene = M.SceneConfig(**bench.H_SCENE) if a.scene == "H" else M.SceneConfig()
+model = M.build_snake(scene, n_envs=a.envs)
 sim = model.sim
 cmds = bench.env_commands(a.envs, a.warmup + a.frames, 0)
 sim.step(cmds[:a.warmup], True, a.warmup)
