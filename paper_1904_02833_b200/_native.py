@@ -11,7 +11,7 @@ import os
 from ._abi import SsEnvStats, SsParams, SsStateView, SsTopology
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libsoftsnake_b200.so")
+LIB_PATH = os.environ.get("SS_LIB_OVERRIDE") or os.path.join(LIB_DIR, "libsoftsnake_b200.so")
 
 SS_EINVAL, SS_ECUDA, SS_ENOMEM, SS_EUNSUP = -1, -2, -3, -4
 

@@ -731,24 +731,16 @@ DI void tet_contrib_fast(const Ctx& c, int t, int env, const TetC& T, const doub
   }
 }
 
-DI void tet_forward_fast(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
-                         const double* vec, double* y) {
-  const int E = c.D.E, nt = c.D.nt;
+// J u of one tet from its 4 node values uv[3v+a] (structured chain rule)
+DI void tet_forward_uv(const TetC& T, const double* Ri, const double* uv, double* y) {
   const double* R = T.R;
   const double* S = T.S;
   const double* Ki = T.K;
-  double u0[3], du[9];
-  {
-    const int n0 = c.T.t_idx[t];
+  double du[9];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) u0[a] = vec[IX(3 * n0 + a)];
-  }
+  for (int v = 1; v < 4; ++v)
 #pragma unroll
-  for (int v = 1; v < 4; ++v) {
-    const int node = c.T.t_idx[v * nt + t];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) du[3 * (v - 1) + a] = vec[IX(3 * node + a)] - u0[a];
-  }
+    for (int a = 0; a < 3; ++a) du[3 * (v - 1) + a] = uv[3 * v + a] - uv[a];
   // L_aj = sum_{v=1..3} (u_v - u_0)_a Ri[v-1][j]   (w_0 = -(w_1 + w_2 + w_3))
   double L[9];
 #pragma unroll
@@ -779,6 +771,21 @@ DI void tet_forward_fast(const Ctx& c, int t, int env, const TetC& T, const doub
   y[3] = 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21);
   y[4] = 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20);
   y[5] = 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10);
+}
+DI void tet_node_vals(const Ctx& c, int t, int env, const double* vec, double* uv) {
+  const int E = c.D.E, nt = c.D.nt;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int node = c.T.t_idx[v * nt + t];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) uv[3 * v + a] = vec[IX(3 * node + a)];
+  }
+}
+DI void tet_forward_fast(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
+                         const double* vec, double* y) {
+  double uv[12];
+  tet_node_vals(c, t, env, vec, uv);
+  tet_forward_uv(T, Ri, uv, y);
 }
 
 // EXACT selects the materialised-column path (bitwise numba sums)
@@ -1407,7 +1414,10 @@ __global__ void __launch_bounds__(SS_THREADS) k_newton_rhs(const Ctx c) {
 // setup != 0: rho = z.az (pcr_solve setup, solver.py:70-73); else
 // beta = rho_new / rho (solver.py:87-89). Absent contact slots are skipped.
 template <bool EXACT>
-__global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setup) {
+#ifndef SS_APPLY_MINB
+#define SS_APPLY_MINB 2
+#endif
+__global__ void __launch_bounds__(SS_THREADS, SS_APPLY_MINB) k_apply_rows(const Ctx c, int setup) {
   SETUP
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
   const double* u = c.K.u;
@@ -1424,11 +1434,27 @@ __global__ void __launch_bounds__(SS_THREADS) k_apply_rows(const Ctx c, int setu
       const int t = it - nd;
       TetC T;
       double Ri[9], y[6], zz[6], ez[6];
-      tet_load(c, t, env, T);
-      tet_rinv(c, t, Ri);
-      tet_j<EXACT>(c, t, env, T, Ri, u, y);
+      if (EXACT) {
+        tet_load(c, t, env, T);
+        tet_rinv(c, t, Ri);
+        tet_j<EXACT>(c, t, env, T, Ri, u, y);
 #pragma unroll
-      for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
+        for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
+      } else {
+        // every load of the tet issued before any arithmetic (one memory
+        // round trip per item instead of three)
+        double q[4], sv[6], uv[12];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) sv[k] = c.K.tS[IX(k * nt + t)];
+        tet_node_vals(c, t, env, u, uv);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
+        tet_rinv(c, t, Ri);
+        tet_unpack(q, sv, T);
+        tet_forward_uv(T, Ri, uv, y);
+      }
       ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], zz, ez);
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
