@@ -182,9 +182,24 @@ int ss_step(ss_handle* h, const double* commands, int latency, int n_frames);
 /* Same, commands already on the device ([n_frames, n_envs, links]). */
 int ss_step_device(ss_handle* h, const double* d_commands, int latency, int n_frames);
 
+/* On-device gait generator (snake.py:235-241): per env params[n][6] =
+ * {amplitude psi, angular rate rad/s, phase offset, turn bias, time offset
+ * t0 s, links per snake}; frame0[n] (nullable = 0) is the frame index the
+ * env's gait clock starts at. ss_step_gait then advances every env with
+ * a_i = clamp(sin(w (t0 + f dt) + alpha (i mod lps)) + bias, -1, 1) * A
+ * computed inside the frame graph (no host commands), f += 1 per frame. */
+int ss_set_gait(ss_handle* h, int env0, int n, const double* params, const int* frame0);
+int ss_step_gait(ss_handle* h, int latency, int n_frames);
+
 int ss_get_stats(ss_handle* h, int env0, int n, ss_env_stats* out);
 /* center_of_mass (state.py:285-292) per env -> host [n,3]. */
 int ss_get_com(ss_handle* h, int env0, int n, double* out);
+/* Rollout observables of envs [env0, env0+n) into host out[n][4 + nb]:
+ * centre of mass (3, state.py:285-292), kinetic energy (state.py:271-282)
+ * and the heading yaw of every body (snake.py:185-188; link curvature and
+ * head yaw follow from the frame bodies' yaws, snake.py:212-232).
+ * Replaces the per-frame host readbacks of harness.py:183-205. */
+int ss_observe(ss_handle* h, int env0, int n, double* out);
 int ss_synchronize(ss_handle* h);
 /* cudaStream_t of the handle, as void* (for timing with CUDA events). */
 void* ss_stream(ss_handle* h);

@@ -32,6 +32,9 @@ SIGNATURES = {
     "ss_step_device": (C.c_int, [_vp, _vp, _i, _i]),
     "ss_get_stats": (C.c_int, [_vp, _i, _i, C.POINTER(SsEnvStats)]),
     "ss_get_com": (C.c_int, [_vp, _i, _i, _dp]),
+    "ss_observe": (C.c_int, [_vp, _i, _i, _dp]),
+    "ss_set_gait": (C.c_int, [_vp, _i, _i, _dp, C.POINTER(C.c_int)]),
+    "ss_step_gait": (C.c_int, [_vp, _i, _i]),
     "ss_synchronize": (C.c_int, [_vp]),
     "ss_stream": (_vp, [_vp]),
     "ss_launches_per_frame": (C.c_int, [_vp]),

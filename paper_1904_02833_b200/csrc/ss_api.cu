@@ -155,9 +155,11 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const double* xc_z = c.K.z + (size_t)D.ms * D.E;
   const double* xs_dl = c.K.az;
   const double* xc_dl = c.K.az + (size_t)D.ms * D.E;
-  LAUNCH(k_frame_begin, g_links, c, d_cmd, has_cmd, latency);
+  // has_cmd: 0 no commands, 1 commands in d_cmd, 2 on-device gait generator
+  const int gait = has_cmd == 2 ? 1 : 0;
+  LAUNCH(k_frame_begin, g_links, c, d_cmd, has_cmd == 1 ? 1 : 0, latency, gait);
   for (int sub = 0; sub < c.p.substeps; ++sub) {
-    LAUNCH(k_pre, g_pre, c);
+    LAUNCH(k_pre, g_pre, c, gait && sub == 0 ? 1 : 0);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
     if (D.nt) LAUNCH(k_eval_tet<EX>, g_tet, c);  // + tet J^T lam
     if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
@@ -224,7 +226,7 @@ int enqueue_frame(ss_handle* H, int w, int has_cmd, int latency, int* nl, Prof* 
 }
 
 int get_graph(ss_handle* H, int w, int has_cmd, int latency, cudaGraphExec_t* out) {
-  const int key = (has_cmd ? 2 : 0) | (latency ? 1 : 0);
+  const int key = 2 * has_cmd + (latency ? 1 : 0);
   cudaGraphExec_t& slot = H->wave_graphs[w][key];
   if (slot) {
     *out = slot;
@@ -718,6 +720,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   Par P{};
   const double h = p->dt / p->substeps;
   P.h = h;
+  P.dt = p->dt;
   const double dmp = 0.0 > p->constraint_damping ? 0.0 : p->constraint_damping;
   P.gamma = 1.0 / (1.0 + dmp);
   for (int a = 0; a < 3; ++a) P.hg[a] = h * p->gravity[a];
@@ -1005,6 +1008,8 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     S.nc_cnt = A.take<int>(Es);
     S.inv_cnt = A.take<int>(Es);
     S.nonfinite = A.take<int>(Es);
+    S.gait = A.take<double>(6 * Es);
+    S.gait_frame = A.take<int>(Es);
   };
   auto plan_work = [&](Arena& A) {
     const size_t Es = H->c.D.E;
@@ -1095,7 +1100,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   CK(cudaMemsetAsync(H->state_mem, 0, sblock * H->n_waves, H->stream));
   CK(cudaMemsetAsync(H->work_mem, 0, wa.cap, H->stream));
   H->wave.assign(H->n_waves, H->c);
-  H->wave_graphs.assign(H->n_waves, std::vector<cudaGraphExec_t>(4, nullptr));
+  H->wave_graphs.assign(H->n_waves, std::vector<cudaGraphExec_t>(6, nullptr));
   for (int w = 0; w < H->n_waves; ++w) {
     Arena a;
     a.base = (char*)H->state_mem + sblock * w;
@@ -1241,13 +1246,14 @@ int ss_get_state(ss_handle* H, int env0, int n, ss_state_view* v) {
   return SS_OK;
 }
 
+// on_device: 0 host commands, 1 device commands, 2 on-device gait (cmd unused)
 static int step_impl(ss_handle* H, const double* cmd, int on_device, int latency, int n_frames) {
   if (!H) return fail(SS_EINVAL, "null handle");
   if (n_frames < 0) return fail(SS_EINVAL, "n_frames must be >= 0");
   CK(cudaSetDevice(H->device));
   const Dims& D = H->c.D;
-  const int has_cmd = cmd != nullptr && D.nch > 0;
-  const int links = std::max(1, D.links);
+  const int has_cmd = D.nch == 0 ? 0 : (on_device == 2 ? 2 : (cmd != nullptr ? 1 : 0));
+  const int key = 2 * has_cmd + (latency ? 1 : 0);
   for (int w = 0; w < H->n_waves; ++w) {
     cudaGraphExec_t g;
     int rc = get_graph(H, w, has_cmd, latency ? 1 : 0, &g);
@@ -1255,13 +1261,12 @@ static int step_impl(ss_handle* H, const double* cmd, int on_device, int latency
   }
   for (int f = 0; f < n_frames; ++f) {
     // every env of the frame, wave after wave (envs are independent)
-    if (has_cmd)
+    if (has_cmd == 1)
       CK(cudaMemcpyAsync(H->d_cmd, cmd + (size_t)f * D.n_real * D.links,
                          8 * (size_t)D.n_real * D.links,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, H->stream));
-    for (int w = 0; w < H->n_waves; ++w) CK(cudaGraphLaunch(H->wave_graphs[w][(has_cmd ? 2 : 0) | (latency ? 1 : 0)], H->stream));
+    for (int w = 0; w < H->n_waves; ++w) CK(cudaGraphLaunch(H->wave_graphs[w][key], H->stream));
   }
-  (void)links;
   return SS_OK;
 }
 
@@ -1270,6 +1275,43 @@ int ss_step(ss_handle* H, const double* commands, int latency, int n_frames) {
 }
 int ss_step_device(ss_handle* H, const double* d_commands, int latency, int n_frames) {
   return step_impl(H, d_commands, 1, latency, n_frames);
+}
+int ss_step_gait(ss_handle* H, int latency, int n_frames) {
+  return step_impl(H, nullptr, 2, latency, n_frames);
+}
+
+int ss_set_gait(ss_handle* H, int env0, int n, const double* params, const int* frame0) {
+  if (!H || (!params && n > 0)) return fail(SS_EINVAL, "null argument");
+  const Dims& D = H->c.D;
+  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
+  for (int i = 0; i < n; ++i) {
+    const double* g = params + 6 * (size_t)i;
+    for (int k = 0; k < 6; ++k)
+      if (!std::isfinite(g[k])) return fail(SS_EINVAL, "gait parameter %d of env %d not finite", k, env0 + i);
+    if (g[5] < 1.0 || g[5] != std::floor(g[5]))
+      return fail(SS_EINVAL, "links_per_snake of env %d must be a positive integer", env0 + i);
+  }
+  if (frame0)
+    for (int i = 0; i < n; ++i)
+      if (frame0[i] < 0) return fail(SS_EINVAL, "negative gait frame for env %d", env0 + i);
+  CK(cudaSetDevice(H->device));
+  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
+    const State& S = H->wave[ch.w].S;
+    // [6][E] items: copy item-major rows for this chunk
+    std::vector<double> rows(6 * (size_t)ch.cnt);
+    for (int k = 0; k < 6; ++k)
+      for (int i = 0; i < ch.cnt; ++i) rows[(size_t)k * ch.cnt + i] = params[6 * (size_t)(ch.off + i) + k];
+    for (int k = 0; k < 6; ++k)
+      CK(cudaMemcpyAsync(S.gait + (size_t)k * D.E + ch.lane0, rows.data() + (size_t)k * ch.cnt,
+                         8 * (size_t)ch.cnt, cudaMemcpyHostToDevice, H->stream));
+    std::vector<int> fr(ch.cnt, 0);
+    if (frame0)
+      for (int i = 0; i < ch.cnt; ++i) fr[i] = frame0[ch.off + i];
+    CK(cudaMemcpyAsync(S.gait_frame + ch.lane0, fr.data(), 4 * (size_t)ch.cnt,
+                       cudaMemcpyHostToDevice, H->stream));
+    CK(cudaStreamSynchronize(H->stream));  // host staging vectors go out of scope
+  }
+  return SS_OK;
 }
 
 int ss_get_stats(ss_handle* H, int env0, int n, ss_env_stats* out) {
@@ -1316,6 +1358,26 @@ int ss_get_com(ss_handle* H, int env0, int n, double* out) {
     CK(cudaGetLastError());
   }
   CK(cudaMemcpyAsync(out, H->d_stage, 24 * (size_t)n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  return SS_OK;
+}
+
+int ss_observe(ss_handle* H, int env0, int n, double* out) {
+  if (!H || !out) return fail(SS_EINVAL, "null argument");
+  const Dims& D = H->c.D;
+  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
+  if (n == 0) return SS_OK;
+  CK(cudaSetDevice(H->device));
+  const size_t per = 4 + (size_t)D.nb;
+  int rc = ensure_stage(H, 8 * per * n);
+  if (rc) return rc;
+  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
+    const int L = D.W;
+    k_observe<<<(ch.cnt + L - 1) / L, 256, 0, H->stream>>>(H->wave[ch.w], ch.lane0, ch.cnt,
+                                                           H->d_stage + per * ch.off);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(out, H->d_stage, 8 * per * n, cudaMemcpyDeviceToHost, H->stream));
   CK(cudaStreamSynchronize(H->stream));
   return SS_OK;
 }

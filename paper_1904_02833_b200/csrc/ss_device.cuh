@@ -37,7 +37,7 @@ struct Dims {
 
 struct Par {
   double h, gamma, hg[3], ground_h, margin, mu, fdyn, fb_delta, smin, smax, dmax;
-  double youngs, ki, kd, cap, supply, half_h;
+  double youngs, ki, kd, cap, supply, half_h, dt;
   int newton, pcr, substeps, exact_j;
 };
 
@@ -72,6 +72,11 @@ struct State {
   // per-frame statistics (StepStats, solver.py:142-151), per env
   double* resid;                        // [1]
   int *nc_cnt, *inv_cnt, *nonfinite;    // [1]
+  // on-device gait generator (snake.py:235-241): [6] = amplitude psi,
+  // angular rate rad/s, phase offset, turn bias, time offset t0, links per
+  // snake; gait_frame = frames stepped since ss_set_gait
+  double* gait;                         // [6]
+  int* gait_frame;                      // [1]
 };
 
 // per-substep workspace, [item][E]
@@ -262,8 +267,24 @@ DI bool reduce_env(const Ctx& c, double val, double* tot) {
 // ================================================================ frame
 // Simulator.step head: ChannelBank.tick + _update_actuation
 // (solver.py:296-301, pneumatics.py:102-116, solver.py:279-282)
+// gait command of link i at frame f: clamp(sin(w t + alpha (i mod lps)) +
+// bias, -1, 1) * A with t = t0 + f dt (snake.py:235-241, harness.py:190-192)
+DI double gait_cmd(const Ctx& c, int env, int i) {
+  const int E = c.D.E;
+  const double A = c.S.gait[IX(0)], w = c.S.gait[IX(1)], al = c.S.gait[IX(2)];
+  const double bias = c.S.gait[IX(3)], t0 = c.S.gait[IX(4)];
+  const int lps = (int)c.S.gait[IX(5)];
+  const double t = t0 + (double)c.S.gait_frame[env] * c.p.dt;
+  const int k = lps > 0 ? i % lps : i;
+  double raw = sin(w * t + al * (double)k) + bias;
+  raw = raw < -1.0 ? -1.0 : (raw > 1.0 ? 1.0 : raw);
+  return raw * A;
+}
+
+// gait: commands from the per-env generator instead of cmd (the frame
+// counter advances in k_pre of the first substep, after every link read it)
 __global__ void k_frame_begin(const Ctx c, const double* __restrict__ cmd, int has_cmd,
-                              int latency) {
+                              int latency, int gait) {
   SETUP
   const int n = c.D.links > 0 ? c.D.links : 1;
   FOR_ITEMS(i, n) {
@@ -273,9 +294,9 @@ __global__ void k_frame_begin(const Ctx c, const double* __restrict__ cmd, int h
       c.S.nonfinite[env] = 0;
     }
     if (i < c.D.links) {
-      if (has_cmd) {
+      if (has_cmd || gait) {
         int ce = env < c.D.n_real ? env : 0;
-        double a = cmd[(size_t)ce * c.D.links + i];
+        double a = gait ? gait_cmd(c, env, i) : cmd[(size_t)ce * c.D.links + i];
         double left = 0.0, right = 0.0;
         if (a > 0.0) right = a;
         else if (a < 0.0) left = -a;
@@ -304,9 +325,10 @@ __global__ void k_frame_begin(const Ctx c, const double* __restrict__ cmd, int h
 // _slew_actuation (solver.py:284-292), build_mass_inverse (state.py:246-268)
 // and _predict_velocities (solver.py:316-332). Items: P particles, nb
 // bodies, nch channels.
-__global__ void k_pre(const Ctx c) {
+__global__ void k_pre(const Ctx c, int gait_tick) {
   SETUP
   const int P = c.D.P, nb = c.D.nb;
+  if (gait_tick && blockIdx.y == 0 && il == 0) c.S.gait_frame[env] += 1;
   FOR_ITEMS(it, P + nb + c.D.nch) {
     if (it < P) {
       const bool live = c.T.inv_mass[it] > 0.0;
@@ -1842,6 +1864,77 @@ __global__ void __launch_bounds__(256) k_com(const Ctx c, int env0, int n, doubl
   out[3 * e] = cx / tot;
   out[3 * e + 1] = cy / tot;
   out[3 * e + 2] = cz / tot;
+}
+
+// Per-env rollout observables for the batched harness (snake.py:208-232,
+// state.py:271-292): out[env] = [com(3), kinetic energy, yaw of every body
+// (nb)]. Same lane x group layout and fixed combine order as k_com.
+__global__ void __launch_bounds__(256) k_observe(const Ctx c, int env0, int n, double* out) {
+  __shared__ double sh[5][256];
+  const int L = c.D.W, G = 256 / L;
+  const int lane = threadIdx.x % L, g = threadIdx.x / L;
+  const int e = blockIdx.x * L + lane;
+  const int env = env0 + (e < n ? e : 0), E = c.D.E;
+  double tot = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, ke = 0.0;
+  for (int i = g; i < c.D.P; i += G) {
+    const double im = c.T.inv_mass[i];
+    if (!(im > 0.0)) continue;
+    const double m = 1.0 / im;
+    tot += m;
+    cx += m * c.S.pos[IX(3 * i)];
+    cy += m * c.S.pos[IX(3 * i + 1)];
+    cz += m * c.S.pos[IX(3 * i + 2)];
+    const double v0 = c.S.vel[IX(3 * i)], v1 = c.S.vel[IX(3 * i + 1)], v2 = c.S.vel[IX(3 * i + 2)];
+    ke += m * (v0 * v0 + v1 * v1 + v2 * v2);
+  }
+  sh[0][threadIdx.x] = tot;
+  sh[1][threadIdx.x] = cx;
+  sh[2][threadIdx.x] = cy;
+  sh[3][threadIdx.x] = cz;
+  sh[4][threadIdx.x] = ke;
+  __syncthreads();
+  for (int h = G / 2; h > 0; h >>= 1) {
+    if (g < h)
+      for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + h * L];
+    __syncthreads();
+  }
+  if (g != 0 || e >= n) return;
+  tot = sh[0][lane];
+  cx = sh[1][lane];
+  cy = sh[2][lane];
+  cz = sh[3][lane];
+  ke = 0.5 * sh[4][lane];
+  const int nb = c.D.nb;
+  double* o = out + (size_t)e * (4 + nb);
+  for (int b = 0; b < nb; ++b) {
+    const double m = 1.0 / c.T.body_inv_mass[b];
+    tot += m;
+    cx += m * c.S.bpos[IX(3 * b)];
+    cy += m * c.S.bpos[IX(3 * b + 1)];
+    cz += m * c.S.bpos[IX(3 * b + 2)];
+    double qw = c.S.bquat[IX(4 * b)], qx = c.S.bquat[IX(4 * b + 1)];
+    double qy = c.S.bquat[IX(4 * b + 2)], qz = c.S.bquat[IX(4 * b + 3)];
+    const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+    double R[9];
+    quat_to_mat(qw, qx, qy, qz, R);
+    const double lv0 = c.S.blin[IX(3 * b)], lv1 = c.S.blin[IX(3 * b + 1)], lv2 = c.S.blin[IX(3 * b + 2)];
+    const double w0 = c.S.bang[IX(3 * b)], w1 = c.S.bang[IX(3 * b + 1)], w2 = c.S.bang[IX(3 * b + 2)];
+    // body-frame omega = R^T w; 0.5 w^T (R I R^T) w
+    const double b0 = R[0] * w0 + R[3] * w1 + R[6] * w2;
+    const double b1 = R[1] * w0 + R[4] * w1 + R[7] * w2;
+    const double b2 = R[2] * w0 + R[5] * w1 + R[8] * w2;
+    const double* I = c.T.body_inertia + 9 * b;
+    const double i0 = I[0] * b0 + I[1] * b1 + I[2] * b2;
+    const double i1 = I[3] * b0 + I[4] * b1 + I[5] * b2;
+    const double i2 = I[6] * b0 + I[7] * b1 + I[8] * b2;
+    ke += 0.5 * m * (lv0 * lv0 + lv1 * lv1 + lv2 * lv2) + 0.5 * (b0 * i0 + b1 * i1 + b2 * i2);
+    o[4 + b] = atan2(R[3], R[0]);  // heading of the body x axis (snake.py:185-188)
+  }
+  o[0] = cx / tot;
+  o[1] = cy / tot;
+  o[2] = cz / tot;
+  o[3] = ke;
 }
 
 // host env-major [n][A*B] <-> device [item][E] (item = swap ? b*A+a : a*B+b).

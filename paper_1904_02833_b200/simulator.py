@@ -199,7 +199,41 @@ class BatchedSimulator:
         _native.check(_native.lib().ss_get_com(h, env0, n, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
+    def observe(self, env0: int = 0, n: int | None = None) -> dict:
+        """Per-env rollout observables computed on the device (ss_observe):
+        com [n,3], kinetic_energy [n], body_yaw [n, nb]."""
+        h = self._ensure()
+        n = self.n_envs - env0 if n is None else n
+        nb = self._packed.dims["nb"]
+        out = np.zeros((n, 4 + nb))
+        _native.check(_native.lib().ss_observe(h, env0, n, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return {"com": out[:, :3], "kinetic_energy": out[:, 3], "body_yaw": out[:, 4:]}
+
     # ----------------------------------------------------------------- step
+    def set_gait(self, gaits, links_per_snake: int, t0=0.0, frame0=0, env0: int = 0) -> None:
+        """Arm the on-device gait generator (snake.py:235-241) for envs
+        [env0, env0+len(gaits)): gaits is one GaitParams or a list (one per
+        env); t0 a per-env time offset (s); frame0 the starting frame index
+        (t = t0 + frame * dt, like harness.py:190 with t0 = 0)."""
+        from .model import GaitParams
+        if isinstance(gaits, GaitParams):
+            gaits = [gaits] * (self.n_envs - env0)
+        n = len(gaits)
+        t0 = np.broadcast_to(np.asarray(t0, np.float64), (n,))
+        fr = np.ascontiguousarray(np.broadcast_to(np.asarray(frame0, np.int32), (n,)))
+        prm = np.array([[g.amplitude_psi, g.angular_rate(), g.phase_offset, g.turn_bias, t0[i],
+                         float(links_per_snake)] for i, g in enumerate(gaits)], np.float64)
+        prm = np.ascontiguousarray(prm.reshape(n, 6))
+        _native.check(_native.lib().ss_set_gait(
+            self._ensure(), env0, n, prm.ctypes.data_as(C.POINTER(C.c_double)),
+            fr.ctypes.data_as(C.POINTER(C.c_int))))
+
+    def step_gait(self, latency: bool = True, n_frames: int = 1) -> None:
+        """Advance all envs n_frames frames with commands generated on the
+        device by the gait armed in set_gait (no host commands)."""
+        _native.check(_native.lib().ss_step_gait(self._ensure(), 1 if latency else 0, int(n_frames)))
+        self.frames += n_frames
+
     def step(self, commands=None, latency: bool = True, n_frames: int = 1) -> None:
         """Advance all envs n_frames frames (asynchronous on the device).
         commands: [n_envs, links] or [n_frames, n_envs, links] psi, or None."""

@@ -1,0 +1,90 @@
+"""Batched rollout harness on the device: on-device gait generator, device
+observables, and the batched curvature sweep against the reference harness
+(tests/golden/sweep_B.npz, made by tests/golden/make_golden_sweep.py)."""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_1904_02833_b200 as M
+from paper_1904_02833_b200 import rollout
+from paper_1904_02833_b200.structures import rotation_matrix
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sweep_B.npz")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__ as g
+    g.build()
+
+
+def test_device_gait_matches_host_commands():
+    """ss_step_gait == ss_step with gait_commands built on the host
+    (snake.py:235-241): per-env bias and t0, 4 frames."""
+    sc = M.SceneConfig()
+    n = 4
+    biases = [-0.4, 0.0, 0.2, 0.45]
+    t0 = np.array([0.0, 0.1, 0.25, 0.4])
+    a = M.build_snake(sc, n_envs=n)
+    b = M.build_snake(sc, n_envs=n)
+    gaits = [M.GaitParams(turn_bias=x) for x in biases]
+    a.sim.set_gait(gaits, a.links_per_snake, t0=t0)
+    for f in range(4):
+        cmds = np.stack([M.gait_commands(g, t0[e] + f * sc.dt, 4, 4) for e, g in enumerate(gaits)])
+        b.sim.step(cmds, latency=True)
+        a.sim.step_gait(latency=True)
+    sa, sb = a.sim.get_state_arrays(), b.sim.get_state_arrays()
+    # numpy and CUDA sin may differ in the last bit of a command
+    assert np.allclose(sa["pressures"], sb["pressures"], rtol=1e-13, atol=1e-13)
+    scale = np.max(np.abs(sb["positions"]))
+    assert np.max(np.abs(sa["positions"] - sb["positions"])) <= 1e-10 * scale
+
+
+def test_observe_matches_host_formulas():
+    sc = M.SceneConfig()
+    model = M.build_snake(sc, n_envs=3)
+    sim = model.sim
+    sim.set_gait(M.GaitParams(), model.links_per_snake, t0=[0.0, 0.2, 0.3])
+    sim.step_gait(latency=True, n_frames=3)
+    obs = sim.observe()
+    st = sim.get_state_arrays()
+    inv_mass = sim.state.particles.inv_mass
+    live = inv_mass > 0
+    bm = sim.state.body_mass
+    bi = sim.state.body_inertia
+    for e in range(3):
+        m = 1.0 / inv_mass[live]
+        v = st["velocities"][e][live]
+        ke = 0.5 * float(np.sum(m * np.einsum("ij,ij->i", v, v)))
+        for b in range(bm.size):
+            R = rotation_matrix(st["body_quat"][e][b])
+            lv, av = st["body_lin_vel"][e][b], st["body_ang_vel"][e][b]
+            ke += 0.5 * bm[b] * float(lv @ lv) + 0.5 * float(av @ (R @ bi[b] @ R.T) @ av)
+        assert math.isclose(obs["kinetic_energy"][e], ke, rel_tol=1e-12)
+        com = ((m[:, None] * st["positions"][e][live]).sum(0) + (bm[:, None] * st["body_pos"][e]).sum(0)) \
+            / (m.sum() + bm.sum())
+        assert np.allclose(obs["com"][e], com, rtol=1e-13, atol=1e-15)
+        yaw = [math.atan2(rotation_matrix(q)[1, 0], rotation_matrix(q)[0, 0]) for q in st["body_quat"][e]]
+        assert np.allclose(obs["body_yaw"][e], yaw, rtol=0, atol=1e-13)
+
+
+def test_curvature_sweep_vs_reference_harness():
+    """Config 1: the reference's run_curvature_sweep levels as one batch."""
+    if not os.path.exists(GOLD):
+        pytest.skip("sweep_B.npz not generated")
+    g = np.load(GOLD)
+    rows = g["rows"]  # tick time p mean std settled
+    got = rollout.curvature_sweep(M.SceneConfig(), pressures=list(g["levels"]))
+    assert np.array_equal(got["settled"], rows[:, 5].astype(int))
+    assert np.allclose(got["time_s"], rows[:, 1], rtol=1e-12)
+    # ~930 frames of a damped, contact-free fixture: the sample mean agrees
+    # to 1e-6 relative of the largest level (SURVEY.md §8(c) horizons)
+    ref = rows[:, 3]
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(got["curvature_mean"] - ref)) <= 1e-6 * scale, (got["curvature_mean"], ref)
+    assert np.allclose(got["curvature_std"], rows[:, 4], rtol=1e-3, atol=1e-6 * scale)
