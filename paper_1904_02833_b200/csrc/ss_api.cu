@@ -572,6 +572,9 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
                         int allow) {
   H->use_cluster = 0;
   if (!allow) return SS_OK;
+  // rows of the largest cluster (16 CTAs x CL_RPT rows x CL_THREADS threads): a
+  // larger scene (e.g. the 1M-tet snake) cannot fit, skip the partitioning
+  if ((long)D.m > 16L * CL_RPT * CL_THREADS) return SS_OK;
   int dev = H->device, max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t budget = (size_t)max_smem - 1024;  // static reduction scratch
@@ -961,13 +964,17 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     return SS_ECUDA;
   }
 
-  // cluster-resident Newton solver plan (ss_params.solver_mode: 0 auto = streaming, 1 streaming,
-  // 2 cluster). The cluster solver is opt-in: it is correct (parity-tested) but latency-bound
-  // (DESIGN.md §7); the streaming kernels are faster on the batched workload.
+  // cluster-resident Newton solver plan (ss_params.solver_mode: 0 auto, 1 streaming,
+  // 2 cluster). Auto picks the cluster solver for small batches, where the streaming
+  // kernels are launch/latency-bound, and streaming from kAutoClusterMaxEnvs up
+  // (measured crossover: 1 env 483 vs 128 steps/s, 64 envs 3528 vs 2754, 128 envs
+  // 3770 vs 3750, 256 envs 3878 vs 4470; tools/solver_crossover.sh).
   {
+    constexpr int kAutoClusterMaxEnvs = 128;
+    const bool want = p->solver_mode == 2 || (p->solver_mode == 0 && n_envs <= kAutoClusterMaxEnvs);
     std::vector<int> tets_v(t->tets, t->tets + 4 * (size_t)D.nt);
     int prc = plan_cluster(H, D, d_i, d_j, tets_v, a_p, a_b, h_a, h_b, w_body, slot_part,
-                           inc_ptr, inc, p->solver_mode == 2);
+                           inc_ptr, inc, want);
     if (prc) {
       ss_destroy(H);
       return prc;
@@ -1057,15 +1064,16 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     const double per_lane = (double)(sa.cap + wa.cap) / D.E;
     const double state_lane = (double)sa.cap / D.E;
     const double budget = 0.88 * (double)free_b;
-    if ((double)n_envs * per_lane > budget && D.E > 32) {
-      // work(E_w) + n_envs * state <= budget
+    // work(E_w) + n_envs * state <= budget
+    const double need = (double)n_envs * state_lane + (double)D.E * (per_lane - state_lane);
+    if (need > budget && D.E > 32) {
       const double wl = (budget - n_envs * state_lane) / (per_lane - state_lane);
       int ew = (int)(wl / 32) * 32;
       if (ew < 32) {
         ss_destroy(H);
         return fail(SS_ENOMEM, "%d envs do not fit in device memory even in waves", n_envs);
       }
-      D.n_real = std::min(n_envs, ew);
+      D.n_real = std::min(D.n_real, ew);  // only ever shrinks the wave
       D.E = pad_lanes(D.n_real);
       D.W = D.E < 32 ? D.E : 32;
       D.lgW = 0;
