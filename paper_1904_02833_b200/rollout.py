@@ -136,3 +136,54 @@ def locomotion(scene, n_envs: int, frames: int, gaits=None, t0=0.0, latency: boo
         contacts[i] = [s.contact_count for s in sim.get_stats()]
     return {"com": com, "head_yaw": yaw, "path_xy": path, "contacts": contacts,
             "curvature": curv, "diverged": diverged}
+
+
+def benchmark(scene, snake_counts=(1, 2, 3, 4), frames: int = 60, warmup: int = 5,
+              include_single_link: bool = True, device: int = 0) -> list[dict]:
+    """harness.run_benchmark (harness.py:212-262, the paper's Table II) on
+    the device: per scene size (the 1-link bend fixture, then coupled
+    n-snake scenes — one system each), device time per frame from CUDA
+    events around each graph replay, and the assembly / solve split from a
+    per-launch profile (eval kernels vs the Newton loop)."""
+    import torch
+    rows = []
+    cases = []
+    if include_single_link:
+        cases.append((0.25, lambda: build_bend_fixture(scene, device=device)))
+    for n in snake_counts:
+        if n < 1:
+            raise ValueError("snake counts must be >= 1")
+        cases.append((float(n), lambda n=n: build_snake(scene, n_snakes=n, device=device)))
+    g = GaitParams.from_scene(scene)
+    for count, make in cases:
+        m = make()
+        sim = m.sim
+        dt = sim.config.dt
+        for i in range(warmup):
+            sim.step(m.commands(i * dt, g))
+        sim.synchronize()
+        stream = torch.cuda.ExternalStream(sim.stream, device=f"cuda:{device}")
+        times = np.empty(frames)
+        for i in range(frames):
+            c = m.commands((warmup + i) * dt, g)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sim.step(c, latency=True)
+            e1.record(stream)
+            e1.synchronize()
+            times[i] = e0.elapsed_time(e1)
+        cmds = m.commands((warmup + frames) * dt, g)
+        prof = sim.profile_frames(cmds.reshape(1, 1, -1), True, 1)
+        asm = sum(v[0] for k, v in prof.items()
+                  if k in ("k_frame_begin", "k_pre", "k_slots", "k_eval_tet", "k_eval_misc",
+                           "k_integrate"))
+        tot = sum(v[0] for v in prof.values())
+        total_ms = float(np.mean(times))
+        rows.append({"snakes": count, "particles": sim.state.num_particles,
+                     "bodies": sim.state.num_bodies, "constraint_rows": sim.static_rows,
+                     "frames": frames, "assembly_ms": total_ms * asm / tot,
+                     "solve_ms": total_ms * (tot - asm) / tot, "total_ms": total_ms,
+                     "total_ms_std": float(np.std(times)), "total_per_snake_ms": total_ms / count,
+                     "solver": "cluster" if sim.solver_info["cluster"] else "streaming"})
+    return rows

@@ -62,13 +62,14 @@ def golden_frame(g, f, which):
 
 
 def scene_parts(tag: str):
-    """(parts, config, model-info) for 'S' (snake) or 'B' (bend fixture),
-    built by this package's builder (bit-identical to the reference)."""
+    """(parts, config) for 'S' (snake), 'S2' (two coupled snakes in one
+    system) or 'B' (bend fixture), built by this package's builder
+    (bit-identical to the reference)."""
     import paper_1904_02833_b200 as M
     from paper_1904_02833_b200.model import build_scene_parts
     sc = M.SceneConfig()
-    if tag == "S":
-        parts, ns, links, fids = build_scene_parts(sc)
+    if tag in ("S", "S2"):
+        parts, ns, links, fids = build_scene_parts(sc, 2 if tag == "S2" else None)
         cfg = sc.solver_config()
     else:
         one = M.SceneConfig(**{**sc.__dict__, "links": 1, "snakes": 1})

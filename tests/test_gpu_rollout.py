@@ -113,3 +113,13 @@ def test_curvature_sweep_full_protocol():
     assert np.allclose(got["time_s"], rows[:, 1], rtol=1e-12)
     assert np.all(np.isfinite(got["curvature_mean"]))
     assert np.all(np.abs(got["curvature_mean"]) < 2.0 * np.max(np.abs(rows[:, 3])) + 10.0)
+
+
+def test_benchmark_table_rows():
+    """rollout.benchmark reproduces harness.run_benchmark's rows (Table II):
+    the single link and coupled 1/2-snake scenes, device-timed."""
+    rows = rollout.benchmark(M.SceneConfig(), snake_counts=(1, 2), frames=5, warmup=2)
+    assert [r["snakes"] for r in rows] == [0.25, 1.0, 2.0]
+    assert rows[1]["constraint_rows"] == 27194 and rows[2]["constraint_rows"] == 2 * 27194
+    for r in rows:
+        assert r["total_ms"] > 0 and abs(r["assembly_ms"] + r["solve_ms"] - r["total_ms"]) < 1e-9

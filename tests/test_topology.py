@@ -77,3 +77,18 @@ def test_hires_topology_bit_identical():
     assert keys == sorted(arrays)
     for k in keys:
         assert _digest(arrays[k]) == str(g[f"topo:{k}"]), f"H {k} differs from reference"
+
+
+def test_two_snake_topology_bit_identical():
+    """build_snake(n_snakes=2) (the coupled scene) equals the reference
+    builder's arrays (digests in tests/golden/step_S2.npz)."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "step_S2.npz")
+    if not os.path.exists(path):
+        pytest.skip("step_S2.npz not generated")
+    g = np.load(path)
+    arrays = _arrays(M.build_snake(M.SceneConfig(), n_snakes=2))
+    keys = sorted(k.split(":", 1)[1] for k in g.files if k.startswith("topo:"))
+    assert keys == sorted(arrays)
+    for k in keys:
+        assert _digest(arrays[k]) == str(g[f"topo:{k}"]), f"S2 {k} differs from reference"
