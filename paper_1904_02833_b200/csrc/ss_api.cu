@@ -770,10 +770,10 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     d_dyn[e] = g * t->dist_compliance[e] / (h * h);
   }
   std::vector<int> t_idx(4 * (size_t)D.nt);
-  std::vector<double> t_rinv(9 * (size_t)D.nt), t_e3(3 * (size_t)D.nt);
+  std::vector<double> t_rinv(10 * (size_t)D.nt, 0.0), t_e3(3 * (size_t)D.nt);
   for (int e = 0; e < D.nt; ++e) {
     for (int v = 0; v < 4; ++v) t_idx[(size_t)v * D.nt + e] = t->tets[4 * (size_t)e + v];
-    for (int k = 0; k < 9; ++k) t_rinv[(size_t)k * D.nt + e] = t->tet_rest_inv[9 * (size_t)e + k];
+    for (int k = 0; k < 9; ++k) t_rinv[10 * (size_t)e + k] = t->tet_rest_inv[9 * (size_t)e + k];
     // eh2 = gamma * compliance / (h*h) (solver.py:210); isotropic pattern
     // (constraints.py:26-40) stored as (diag, off-diagonal, shear)
     double eh[36];
@@ -888,7 +888,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     T.d_rest = A.take<double>(D.nd);
     T.d_dyn = A.take<double>(D.nd);
     T.t_idx = A.take<int>(4 * (size_t)D.nt);
-    T.t_rinv = A.take<double>(9 * (size_t)D.nt);
+    T.t_rinv = A.take<double>(10 * (size_t)D.nt);
     T.t_e3 = A.take<double>(3 * (size_t)D.nt);
     T.a_p = A.take<int>(D.na);
     T.a_b = A.take<int>(D.na);

@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
           sb[L.oJR + k * L.MT + el.le] = T.R[k];
-          sb[L.oRi + k * L.MT + el.le] = c.T.t_rinv[k * nt + t];
+          sb[L.oRi + k * L.MT + el.le] = c.T.t_rinv[10 * (size_t)t + k];
         }
 #pragma unroll
         for (int k = 0; k < 6; ++k) {

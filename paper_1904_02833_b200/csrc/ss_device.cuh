@@ -47,7 +47,7 @@ struct Topo {
   const int *d_i, *d_j, *d_chan;                                  // [nd]
   const double *d_rest, *d_dyn;                                   // [nd]
   const int* t_idx;                                               // [4][nt]
-  const double *t_rinv, *t_e3;                                    // [9][nt] [3][nt]
+  const double *t_rinv, *t_e3;                                    // [nt][10] (9 + pad) [3][nt]
   const int *a_p, *a_b;                                           // [na]
   const double *a_anc, *a_dyn;                                    // [3][na] [na]
   const int *h_a, *h_b;                                           // [nh]
@@ -666,9 +666,15 @@ DI void tet_load(const Ctx& c, int t, int env, TetC& T) {
   tet_unpack(q, s, T);
 }
 DI void tet_rinv(const Ctx& c, int t, double* Ri) {
-  const int nt = c.D.nt;
+  // one tet's rest inverse is 80 contiguous bytes: 5 broadcast 16-byte loads
+  const double2* p = reinterpret_cast<const double2*>(c.T.t_rinv + 10 * (size_t)t);
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Ri[k] = c.T.t_rinv[k * nt + t];
+  for (int k = 0; k < 4; ++k) {
+    const double2 v = __ldg(p + k);
+    Ri[2 * k] = v.x;
+    Ri[2 * k + 1] = v.y;
+  }
+  Ri[8] = __ldg(c.T.t_rinv + 10 * (size_t)t + 8);
 }
 
 // J^T x for one tet: the 12 column sums acc_j = sum_i J[i][j] x_i in the
