@@ -119,6 +119,10 @@ typedef struct ss_params {
    * state is kept for every env; waves share one workspace and run back to
    * back inside each frame. */
   int32_t wave_envs;
+  /* SolverConfig.keep_matrix (solver.py:113, 511-518): keep the last
+   * substep's Newton system readable through ss_export_system (forces the
+   * streaming solver; one extra rhs copy per frame). */
+  int32_t keep_matrix;
 } ss_params;
 
 /* Full per-environment state. Host pointers;
@@ -192,6 +196,33 @@ int ss_set_gait(ss_handle* h, int env0, int n, const double* params, const int* 
 int ss_step_gait(ss_handle* h, int latency, int n_frames);
 
 int ss_get_stats(ss_handle* h, int env0, int n, ss_env_stats* out);
+
+/* The last substep's Newton system of one env (keep_matrix handles only),
+ * in the reference's snapshot layout (solver.py:511-518) for
+ * Simulator.last_system / export_system (solver.py:548-581): per-family
+ * Jacobian blocks and DOF indices, static rows in reference row order,
+ * contact slots uncompacted (present flags; present slots in slot order are
+ * the reference's contacts), the mass inverse. Host pointers, caller-owned. */
+typedef struct {
+  double* dist_vals;   /* [nd][1][6] */
+  int32_t* dist_idx;   /* [nd][6] */
+  double* tet_vals;    /* [nt][6][12] */
+  int32_t* tet_idx;    /* [nt][12] */
+  double* att_vals;    /* [na][3][9] */
+  int32_t* att_idx;    /* [na][9] */
+  double* hinge_vals;  /* [nh][5][12] */
+  int32_t* hinge_idx;  /* [nh][12] */
+  double* slot_vals;   /* [ns][3][6] normal, friction t1, friction t2 */
+  int32_t* slot_idx;   /* [ns][6] */
+  int32_t* slot_present; /* [ns] */
+  double* rhs_static;  /* [m_static] */
+  double* dyn_static;  /* [m_static] (0 on tet rows: E_tet enters as blocks) */
+  double* rhs_slot;    /* [ns][3] */
+  double* dyn_slot;    /* [ns][3] */
+  double* minv_diag;   /* [ndof] (angular entries 0) */
+  double* ang_inv;     /* [nb][3][3] */
+} ss_system_view;
+int ss_export_system(ss_handle* h, int env, ss_system_view* out);
 /* center_of_mass (state.py:285-292) per env -> host [n,3]. */
 int ss_get_com(ss_handle* h, int env0, int n, double* out);
 /* Rollout observables of envs [env0, env0+n) into host out[n][4 + nb]:

@@ -47,6 +47,7 @@ class SsParams(C.Structure):
         ("strain_youngs", C.c_double), ("k_inflate", C.c_double),
         ("k_deflate", C.c_double), ("deflate_cap", C.c_double), ("supply", C.c_double),
         ("exact_jacobian", C.c_int32), ("solver_mode", C.c_int32), ("wave_envs", C.c_int32),
+        ("keep_matrix", C.c_int32),
     ]
 
 
@@ -84,6 +85,16 @@ class SsEnvStats(C.Structure):
         ("contact_count", C.c_int32), ("inverted_tets", C.c_int32),
         ("residual", C.c_double), ("finite", C.c_int32), ("_pad", C.c_int32),
     ]
+
+
+class SsSystemView(C.Structure):
+    """ss_system_view (include/softsnake_b200.h)."""
+    _fields_ = [(n, C.POINTER(C.c_double) if t == "d" else C.POINTER(C.c_int32)) for n, t in (
+        ("dist_vals", "d"), ("dist_idx", "i"), ("tet_vals", "d"), ("tet_idx", "i"),
+        ("att_vals", "d"), ("att_idx", "i"), ("hinge_vals", "d"), ("hinge_idx", "i"),
+        ("slot_vals", "d"), ("slot_idx", "i"), ("slot_present", "i"), ("rhs_static", "d"),
+        ("dyn_static", "d"), ("rhs_slot", "d"), ("dyn_slot", "d"), ("minv_diag", "d"),
+        ("ang_inv", "d"))]
 
 
 def _ptr(a: np.ndarray | None, kind):
@@ -209,6 +220,7 @@ def pack_params(config, packed: PackedTopology) -> SsParams:
     p.exact_jacobian = 1 if getattr(config, "exact_jacobian", False) else 0
     p.solver_mode = {"auto": 0, "streaming": 1, "cluster": 2}[getattr(config, "solver", "auto")]
     p.wave_envs = int(getattr(config, "wave_envs", 0))
+    p.keep_matrix = 1 if getattr(config, "keep_matrix", False) else 0
     return p
 
 

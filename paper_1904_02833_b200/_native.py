@@ -8,7 +8,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from ._abi import SsEnvStats, SsParams, SsStateView, SsTopology
+from ._abi import SsEnvStats, SsParams, SsStateView, SsSystemView, SsTopology
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.environ.get("SS_LIB_OVERRIDE") or os.path.join(LIB_DIR, "libsoftsnake_b200.so")
@@ -31,6 +31,7 @@ SIGNATURES = {
     "ss_step": (C.c_int, [_vp, _dp, _i, _i]),
     "ss_step_device": (C.c_int, [_vp, _vp, _i, _i]),
     "ss_get_stats": (C.c_int, [_vp, _i, _i, C.POINTER(SsEnvStats)]),
+    "ss_export_system": (C.c_int, [_vp, _i, C.POINTER(SsSystemView)]),
     "ss_get_com": (C.c_int, [_vp, _i, _i, _dp]),
     "ss_observe": (C.c_int, [_vp, _i, _i, _dp]),
     "ss_set_gait": (C.c_int, [_vp, _i, _i, _dp, C.POINTER(C.c_int)]),

@@ -75,6 +75,7 @@ struct ss_handle {
   int launches = 0;
   // cluster-resident Newton solver (0 = streaming kernels)
   int use_cluster = 0;
+  int keep = 0;  // keep_matrix: snapshot the last Newton rhs each frame
   ClPlan plan{};
   void* plan_mem = nullptr;
 };
@@ -195,6 +196,9 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
     LAUNCH(k_gather, g_gather, c, 1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
     for (int it = 0; it < c.p.newton; ++it) {
       LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
+      if (H->keep && sub == c.p.substeps - 1 && it == c.p.newton - 1)
+        CK(cudaMemcpyAsync(c.K.snap_rhs, c.K.r, 8 * (size_t)D.m * D.E, cudaMemcpyDeviceToDevice,
+                           st));  // the snapshot's rhs (solver.py:515)
       if (c.p.pcr > 0) {
         LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
         LAUNCH(k_apply_rows<EX>, g_red, c, 1);
@@ -971,7 +975,13 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // 3770 vs 3750, 256 envs 3878 vs 4470; tools/solver_crossover.sh).
   {
     constexpr int kAutoClusterMaxEnvs = 128;
-    const bool want = p->solver_mode == 2 || (p->solver_mode == 0 && n_envs <= kAutoClusterMaxEnvs);
+    H->keep = p->keep_matrix ? 1 : 0;
+    if (H->keep && p->solver_mode == 2) {
+      ss_destroy(H);
+      return fail(SS_EUNSUP, "keep_matrix needs the streaming solver");
+    }
+    const bool want = p->solver_mode == 2 ||
+                      (p->solver_mode == 0 && !H->keep && n_envs <= kAutoClusterMaxEnvs);
     std::vector<int> tets_v(t->tets, t->tets + 4 * (size_t)D.nt);
     int prc = plan_cluster(H, D, d_i, d_j, tets_v, a_p, a_b, h_a, h_b, w_body, slot_part,
                            inc_ptr, inc, want);
@@ -1050,6 +1060,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.alpha = A.take<double>(Es);
     K.beta = A.take<double>(Es);
     K.broken = A.take<int>(Es);
+    K.snap_rhs = p->keep_matrix ? A.take<double>((size_t)D.m * Es) : nullptr;
   };
   Arena sa, wa;
   plan_state(sa);
@@ -1386,6 +1397,54 @@ int ss_observe(ss_handle* H, int env0, int n, double* out) {
     CK(cudaGetLastError());
   }
   CK(cudaMemcpyAsync(out, H->d_stage, 8 * per * n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  return SS_OK;
+}
+
+int ss_export_system(ss_handle* H, int env, ss_system_view* v) {
+  if (!H || !v) return fail(SS_EINVAL, "null argument");
+  if (!H->keep) return fail(SS_EINVAL, "no system snapshot; create with keep_matrix and step");
+  const Dims& D = H->c.D;
+  if (env < 0 || env >= D.n_real) return fail(SS_EINVAL, "env out of range");
+  CK(cudaSetDevice(H->device));
+  const int w = env / D.E, lane = env % D.E;
+  // staging layout: doubles then ints
+  const size_t nD[] = {6 * (size_t)D.nd, 72 * (size_t)D.nt, 27 * (size_t)D.na, 60 * (size_t)D.nh,
+                       18 * (size_t)D.ns, (size_t)D.ms, (size_t)D.ms, 3 * (size_t)D.ns,
+                       3 * (size_t)D.ns, (size_t)D.ndof, 9 * (size_t)D.nb};
+  const size_t nI[] = {6 * (size_t)D.nd, 12 * (size_t)D.nt, 9 * (size_t)D.na, 12 * (size_t)D.nh,
+                       6 * (size_t)D.ns, (size_t)D.ns};
+  size_t td = 0, ti = 0;
+  for (size_t x : nD) td += x;
+  for (size_t x : nI) ti += x;
+  int rc = ensure_stage(H, 8 * td + 4 * ti);
+  if (rc) return rc;
+  double* dp[11];
+  int* ip[6];
+  {
+    double* q = H->d_stage;
+    for (int k = 0; k < 11; ++k) {
+      dp[k] = q;
+      q += nD[k];
+    }
+    int* r = reinterpret_cast<int*>(q);
+    for (int k = 0; k < 6; ++k) {
+      ip[k] = r;
+      r += nI[k];
+    }
+  }
+  SysOut o{dp[0], dp[1], dp[2], dp[3], dp[4], ip[0], ip[1], ip[2], ip[3], ip[4], ip[5],
+           dp[5], dp[6], dp[7], dp[8], dp[9], dp[10]};
+  const long items = (long)D.nd + D.nt + D.na + D.nh + D.ns + D.P + D.nb;
+  k_export_system<<<(unsigned)((items + 255) / 256), 256, 0, H->stream>>>(H->wave[w], lane, o);
+  CK(cudaGetLastError());
+  double* hd[] = {v->dist_vals, v->tet_vals, v->att_vals, v->hinge_vals, v->slot_vals,
+                  v->rhs_static, v->dyn_static, v->rhs_slot, v->dyn_slot, v->minv_diag, v->ang_inv};
+  int32_t* hi[] = {v->dist_idx, v->tet_idx, v->att_idx, v->hinge_idx, v->slot_idx, v->slot_present};
+  for (int k = 0; k < 11; ++k)
+    if (nD[k] && hd[k]) CK(cudaMemcpyAsync(hd[k], dp[k], 8 * nD[k], cudaMemcpyDeviceToHost, H->stream));
+  for (int k = 0; k < 6; ++k)
+    if (nI[k] && hi[k]) CK(cudaMemcpyAsync(hi[k], ip[k], 4 * nI[k], cudaMemcpyDeviceToHost, H->stream));
   CK(cudaStreamSynchronize(H->stream));
   return SS_OK;
 }

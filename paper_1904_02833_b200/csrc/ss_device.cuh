@@ -98,6 +98,7 @@ struct Work {
   int* cnt;                 // [tiles]
   double *rho, *alpha, *beta;  // [E]
   int* broken;                  // [E]
+  double* snap_rhs;             // [m] rhs of the last Newton pass (keep_matrix only)
 };
 
 struct Ctx {
@@ -1957,6 +1958,120 @@ __global__ void __launch_bounds__(256) k_observe(const Ctx c, int env0, int n, d
   o[1] = cy / tot;
   o[2] = cz / tot;
   o[3] = ke;
+}
+
+// System inspection (solver.py:511-518 snapshot, 548-575 last_system): the
+// last substep's Newton system of env lane `env` in the reference's block
+// layout. Static rows are permuted to the reference row order; contact
+// slots stay uncompacted (the host compacts present slots in slot order,
+// which is the reference's contact order). Items: nd + nt + na + nh + ns
+// elements, then P + nb mass-inverse nodes.
+struct SysOut {
+  double *dist_v, *tet_v, *att_v, *hinge_v, *slot_v;  // [nd][6] [nt][72] [na][27] [nh][60] [ns][18]
+  int *dist_i, *tet_i, *att_i, *hinge_i, *slot_i, *slot_p;  // [nd][6] [nt][12] [na][9] [nh][12] [ns][6] [ns]
+  double *rhs_s, *dyn_s, *rhs_c, *dyn_c;  // [ms] [ms] [ns][3] [ns][3]
+  double *minv_d, *ang;                   // [ndof] [nb][9]
+};
+__global__ void k_export_system(const Ctx c, int env, SysOut o) {
+  const int E = c.D.E;
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns, nw = c.D.nw;
+  const int bd0 = c.D.bd0, n_el = nd + nt + na + nh + ns;
+  const int ot_ref = nd, oa_ref = nd + 6 * nt, oh_ref = oa_ref + 3 * na;
+  const double* snap = c.K.snap_rhs;
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_el + c.D.P + c.D.nb;
+       it += gridDim.x * blockDim.x) {
+    if (it < nd) {
+      const int d = it, i = c.T.d_i[d], j = c.T.d_j[d];
+      for (int a = 0; a < 3; ++a) {
+        const double u = c.S.dirs[IX(a * nd + d)];
+        o.dist_v[6 * d + a] = u;
+        o.dist_v[6 * d + 3 + a] = -u;
+        o.dist_i[6 * d + a] = 3 * i + a;
+        o.dist_i[6 * d + 3 + a] = 3 * j + a;
+      }
+      o.rhs_s[d] = snap[IX(c.D.od + d)];
+      o.dyn_s[d] = c.T.d_dyn[d];
+    } else if (it < nd + nt) {
+      const int t = it - nd;
+      TetC T;
+      double Ri[9];
+      tet_load(c, t, env, T);
+      tet_rinv(c, t, Ri);
+      for (int v = 0; v < 4; ++v) {
+        double wv[3];
+        tet_wv(Ri, v, wv);
+        const int node = c.T.t_idx[v * nt + t];
+        for (int a = 0; a < 3; ++a) {
+          double col[6];
+          tet_col(T, wv, a, col);
+          for (int i = 0; i < 6; ++i) o.tet_v[72 * (size_t)t + 12 * i + 3 * v + a] = col[i];
+          o.tet_i[12 * (size_t)t + 3 * v + a] = 3 * node + a;
+        }
+      }
+      for (int i = 0; i < 6; ++i) {
+        o.rhs_s[ot_ref + 6 * t + i] = snap[IX(c.D.ot + i * nt + t)];
+        o.dyn_s[ot_ref + 6 * t + i] = 0.0;  // E_tet enters as 6x6 blocks
+      }
+    } else if (it < nd + nt + na) {
+      const int a = it - nd - nt;
+      double rw[3];
+      for (int k = 0; k < 3; ++k) rw[k] = c.K.rw[IX(k * na + a)];
+      for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 9; ++j) o.att_v[27 * a + 9 * i + j] = att_val(i, j, rw);
+        o.rhs_s[oa_ref + 3 * a + i] = snap[IX(c.D.oa + i * na + a)];
+        o.dyn_s[oa_ref + 3 * a + i] = c.T.a_dyn[a];
+      }
+      for (int k = 0; k < 3; ++k) o.att_i[9 * a + k] = 3 * c.T.a_p[a] + k;
+      for (int k = 0; k < 6; ++k) o.att_i[9 * a + 3 + k] = bd0 + 6 * c.T.a_b[a] + k;
+    } else if (it < nd + nt + na + nh) {
+      const int h = it - nd - nt - na;
+      for (int i = 0; i < 5; ++i) {
+        for (int j = 0; j < 12; ++j) o.hinge_v[60 * h + 12 * i + j] = c.K.hJ[IX((size_t)(12 * i + j) * nh + h)];
+        o.rhs_s[oh_ref + 5 * h + i] = snap[IX(c.D.oh + i * nh + h)];
+        o.dyn_s[oh_ref + 5 * h + i] = c.T.h_dyn[h];
+      }
+      for (int k = 0; k < 6; ++k) {
+        o.hinge_i[12 * h + k] = bd0 + 6 * c.T.h_a[h] + k;
+        o.hinge_i[12 * h + 6 + k] = bd0 + 6 * c.T.h_b[h] + k;
+      }
+    } else if (it < n_el) {
+      const int sl = it - nd - nt - na - nh;
+      const int pres = c.K.present[IX(sl)] != 0;
+      o.slot_p[sl] = pres;
+      double* v = o.slot_v + 18 * (size_t)sl;
+      int* ix = o.slot_i + 6 * sl;
+      if (sl < nw) {
+        const int ob = bd0 + 6 * c.T.w_body[sl];
+        for (int k = 0; k < 6; ++k) ix[k] = ob + k;
+        for (int r = 0; r < 3; ++r)
+          for (int k = 0; k < 6; ++k) v[6 * r + k] = c.K.wJ[IX((size_t)(6 * r + k) * nw + sl)];
+      } else {
+        // particle contact: 3 DOFs, columns 3..5 padded with DOF 0 (contact.py:208-214)
+        const int pi = c.T.slot_part[sl - nw];
+        for (int k = 0; k < 6; ++k) ix[k] = k < 3 ? 3 * pi + k : 0;
+        for (int k = 0; k < 18; ++k) v[k] = 0.0;
+        v[2] = 1.0;       // normal (0, 0, 1)
+        v[6 + 0] = 1.0;   // t1 (1, 0, 0)
+        v[12 + 1] = 1.0;  // t2 (0, 1, 0)
+      }
+      o.rhs_c[3 * sl] = pres ? snap[IX(c.D.on + sl)] : 0.0;
+      o.rhs_c[3 * sl + 1] = pres ? snap[IX(c.D.of + sl)] : 0.0;
+      o.rhs_c[3 * sl + 2] = pres ? snap[IX(c.D.of + ns + sl)] : 0.0;
+      o.dyn_c[3 * sl] = pres ? c.K.dynn[IX(sl)] : 0.0;
+      o.dyn_c[3 * sl + 1] = c.p.fdyn;
+      o.dyn_c[3 * sl + 2] = c.p.fdyn;
+    } else if (it < n_el + c.D.P) {
+      const int i = it - n_el;
+      for (int a = 0; a < 3; ++a) o.minv_d[3 * i + a] = c.T.inv_mass[i];
+    } else {
+      const int b = it - n_el - c.D.P;
+      for (int a = 0; a < 3; ++a) {
+        o.minv_d[bd0 + 6 * b + a] = c.T.body_inv_mass[b];
+        o.minv_d[bd0 + 6 * b + 3 + a] = 0.0;  // angular block in ang
+      }
+      for (int k = 0; k < 9; ++k) o.ang[9 * b + k] = c.K.ang_inv[IX((size_t)k * c.D.nb + b)];
+    }
+  }
 }
 
 // host env-major [n][A*B] <-> device [item][E] (item = swap ? b*A+a : a*B+b).

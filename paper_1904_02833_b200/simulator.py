@@ -127,8 +127,26 @@ class BatchedSimulator:
         _native.check(L.ss_create(C.byref(self._packed.struct), C.byref(params),
                                   self.n_envs, self.device, C.byref(h)))
         self._h = h
-        self.set_state_arrays(self._initial_state_arrays(), env0=0, n=self.n_envs)
+        self._keep_built = bool(self.config.keep_matrix)
+        self._snap_ready = False
+        init = getattr(self, "_initial_override", None)
+        self.set_state_arrays(init if init is not None else self._initial_state_arrays(),
+                              env0=0, n=self.n_envs)
         return h
+
+    def _sync_keep(self) -> None:
+        """config.keep_matrix is read per step in the reference (solver.py:
+        511); the device snapshot buffer is sized at ss_create, so a toggle
+        recreates the handle with every env's state carried over."""
+        if self._h is None or bool(self.config.keep_matrix) == self._keep_built:
+            return
+        st = self.get_state_arrays()
+        self.close()
+        self._initial_override = st
+        try:
+            self._ensure()
+        finally:
+            self._initial_override = None
 
     def close(self):
         if self._h is not None:
@@ -231,12 +249,15 @@ class BatchedSimulator:
     def step_gait(self, latency: bool = True, n_frames: int = 1) -> None:
         """Advance all envs n_frames frames with commands generated on the
         device by the gait armed in set_gait (no host commands)."""
+        self._sync_keep()
         _native.check(_native.lib().ss_step_gait(self._ensure(), 1 if latency else 0, int(n_frames)))
         self.frames += n_frames
+        self._snap_ready = self._keep_built
 
     def step(self, commands=None, latency: bool = True, n_frames: int = 1) -> None:
         """Advance all envs n_frames frames (asynchronous on the device).
         commands: [n_envs, links] or [n_frames, n_envs, links] psi, or None."""
+        self._sync_keep()
         h = self._ensure()
         ptr = None
         if commands is not None:
@@ -250,12 +271,37 @@ class BatchedSimulator:
             ptr = cmd.ctypes.data_as(C.POINTER(C.c_double))
         _native.check(_native.lib().ss_step(h, ptr, 1 if latency else 0, int(n_frames)))
         self.frames += n_frames
+        self._snap_ready = self._keep_built
 
     def step_device(self, d_commands_ptr: int, latency: bool = True, n_frames: int = 1) -> None:
+        self._sync_keep()
         h = self._ensure()
         _native.check(_native.lib().ss_step_device(h, C.c_void_p(d_commands_ptr),
                                                    1 if latency else 0, int(n_frames)))
         self.frames += n_frames
+
+    # ----------------------------------------------------------- inspection
+    def last_system(self, env: int = 0):
+        """Explicit CSR of the most recent Newton system (keep_matrix on;
+        solver.py:548-575) of one env."""
+        from .system import assemble, export_blocks
+        if not getattr(self, "_snap_ready", False):
+            raise RuntimeError("no system snapshot; set config.keep_matrix and step")
+        cfg = self.config
+        h = cfg.dt / cfg.substeps
+        gamma = 1.0 / (1.0 + max(0.0, cfg.constraint_damping))
+        eh2 = None
+        if self.tetras is not None and self.tetras.count:
+            eh2 = gamma * self.tetras.compliance / (h * h)
+        return assemble(export_blocks(self, env), eh2)
+
+    def export_system(self, path_a: str, path_b: str, env: int = 0) -> None:
+        """Write the last Newton system as Matrix Market files
+        (solver.py:577-581)."""
+        from .system import mmwrite, mmwrite_dense
+        s = self.last_system(env)
+        mmwrite(path_a, s.matrix)
+        mmwrite_dense(path_b, s.rhs)
 
     def synchronize(self) -> None:
         _native.check(_native.lib().ss_synchronize(self._ensure()))
