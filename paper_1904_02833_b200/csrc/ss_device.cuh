@@ -119,6 +119,9 @@ struct Ctx {
   (void)IL;
 #define FOR_ITEMS(it, n) for (int it = blockIdx.y * IL + il; it < (n); it += gridDim.y * IL)
 #define IX(item) ((size_t)(item) * E + env)
+// tet column sums tC: [12][nt][E] (a [nt][12] layout for E = 1 was tried:
+// the gather did not speed up and the strided writes cost k_tet_jt 35%)
+#define TCX(k, t) (((size_t)(k) * nt + (t)) * E + env)
 
 // ------------------------------------------------------------ small math
 // numpy.maximum: NaN in a propagates
@@ -258,10 +261,18 @@ DI bool reduce_env(const Ctx& c, double val, double* tot) {
   __syncthreads();
   if (!amlast) return false;
   if (threadIdx.x == 0) c.K.cnt[blockIdx.x] = 0;
-  if (il != 0) return false;
+  // the last block combines the gridDim.y partials with all its item lanes
+  // (lane il sums rows il, il + IL, ... in order, then the same fixed tree)
   double s = 0.0;
-  for (int y = 0; y < (int)gridDim.y; ++y) s += __ldcg(&c.K.part[(size_t)y * E + env]);
-  *tot = s;
+  for (int y = il; y < (int)gridDim.y; y += IL) s += __ldcg(&c.K.part[(size_t)y * E + env]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = IL >> 1; st > 0; st >>= 1) {
+    if (il < st) red[threadIdx.x] += red[threadIdx.x + st * c.D.W];
+    __syncthreads();
+  }
+  if (il != 0) return false;
+  *tot = red[lane];
   return true;
 }
 
@@ -694,7 +705,7 @@ DI void tet_contrib(const Ctx& c, int t, int env, const TetC& T, const double* R
       double acc = 0.0;
 #pragma unroll
       for (int i = 0; i < 6; ++i) acc += col[i] * x6[i];
-      c.K.tC[IX((3 * v + a) * nt + t)] = acc;
+      c.K.tC[TCX(3 * v + a, t)] = acc;
     }
   }
 }
@@ -757,7 +768,7 @@ DI void tet_contrib_fast(const Ctx& c, int t, int env, const TetC& T, const doub
     const double q2 = (Z02 * wv[0] + Z12 * wv[1] + Z22 * wv[2]) - (n0 * wv[1] - n1 * wv[0]);
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-      c.K.tC[IX((3 * v + a) * nt + t)] = R[3 * a] * q0 + R[3 * a + 1] * q1 + R[3 * a + 2] * q2;
+      c.K.tC[TCX(3 * v + a, t)] = R[3 * a] * q0 + R[3 * a + 1] * q1 + R[3 * a + 2] * q2;
   }
 }
 
@@ -1044,10 +1055,9 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
             for (int j = 0; j < 4; ++j) {
               const int code = c.T.inc[k + j];
               const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
-              const size_t base = (size_t)(3 * v) * nt + e;
-              a[3 * j] = tC[base * E + env];
-              a[3 * j + 1] = tC[(base + nt) * E + env];
-              a[3 * j + 2] = tC[(base + 2 * (size_t)nt) * E + env];
+              a[3 * j] = tC[TCX(3 * v, e)];
+              a[3 * j + 1] = tC[TCX(3 * v + 1, e)];
+              a[3 * j + 2] = tC[TCX(3 * v + 2, e)];
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -1059,10 +1069,9 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
           for (; k < tr.y; ++k) {
             const int code = c.T.inc[k];
             const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
-            const size_t base = (size_t)(3 * v) * nt + e;
-            w0 += tC[base * E + env];
-            w1 += tC[(base + nt) * E + env];
-            w2 += tC[(base + 2 * (size_t)nt) * E + env];
+            w0 += tC[TCX(3 * v, e)];
+            w1 += tC[TCX(3 * v + 1, e)];
+            w2 += tC[TCX(3 * v + 2, e)];
           }
           if (k >= k1) break;
         }
@@ -1070,10 +1079,9 @@ __global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
         const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
         double a0, a1, a2;
         if (fam == F_TET) {
-          const size_t base = (size_t)(3 * v) * nt + e;
-          a0 = c.K.tC[base * E + env];
-          a1 = c.K.tC[(base + nt) * E + env];
-          a2 = c.K.tC[(base + 2 * (size_t)nt) * E + env];
+          a0 = c.K.tC[TCX(3 * v, e)];
+          a1 = c.K.tC[TCX(3 * v + 1, e)];
+          a2 = c.K.tC[TCX(3 * v + 2, e)];
         } else if (fam == F_DIST) {
           const int nd = c.D.nd;
           const double xr = xs[IX(c.D.od + e)];
