@@ -199,31 +199,7 @@ DI void cl_tet_jt(const TetC& T, const double* Ri, const double* x6, double* col
       }
     }
   } else {
-    const double* S_ = T.S;
-    const double* Ki = T.K;
-    const double* R = T.R;
-    const double Z00 = x6[0], Z11 = x6[1], Z22 = x6[2];
-    const double Z12 = 0.5 * x6[3], Z02 = 0.5 * x6[4], Z01 = 0.5 * x6[5];
-    const double N21 = Z02 * S_[1] + Z12 * S_[4] + Z22 * S_[7];
-    const double N12 = Z01 * S_[2] + Z11 * S_[5] + Z12 * S_[8];
-    const double N02 = Z00 * S_[2] + Z01 * S_[5] + Z02 * S_[8];
-    const double N20 = Z02 * S_[0] + Z12 * S_[3] + Z22 * S_[6];
-    const double N10 = Z01 * S_[0] + Z11 * S_[3] + Z12 * S_[6];
-    const double N01 = Z00 * S_[1] + Z01 * S_[4] + Z02 * S_[7];
-    const double m0 = N21 - N12, m1 = N02 - N20, m2 = N10 - N01;
-    const double n0 = Ki[0] * m0 + Ki[1] * m1 + Ki[2] * m2;
-    const double n1 = Ki[3] * m0 + Ki[4] * m1 + Ki[5] * m2;
-    const double n2 = Ki[6] * m0 + Ki[7] * m1 + Ki[8] * m2;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      double wv[3];
-      tet_wv(Ri, v, wv);
-      const double q0 = (Z00 * wv[0] + Z01 * wv[1] + Z02 * wv[2]) - (n1 * wv[2] - n2 * wv[1]);
-      const double q1 = (Z01 * wv[0] + Z11 * wv[1] + Z12 * wv[2]) - (n2 * wv[0] - n0 * wv[2]);
-      const double q2 = (Z02 * wv[0] + Z12 * wv[1] + Z22 * wv[2]) - (n0 * wv[1] - n1 * wv[0]);
-#pragma unroll
-      for (int a = 0; a < 3; ++a) col12[3 * v + a] = R[3 * a] * q0 + R[3 * a + 1] * q1 + R[3 * a + 2] * q2;
-    }
+    tet_jt_cols(T, Ri, x6, col12);
   }
 }
 
@@ -247,43 +223,7 @@ DI void cl_tet_j(const TetC& T, const double* Ri, const double* uu, double* y) {
     }
     return;
   }
-  const double* R = T.R;
-  const double* S_ = T.S;
-  const double* Ki = T.K;
-  double du[9];
-#pragma unroll
-  for (int v = 1; v < 4; ++v)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) du[3 * (v - 1) + a] = uu[3 * v + a] - uu[a];
-  double Lm[9], G[9];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      Lm[3 * a + j] = du[a] * Ri[j] + du[3 + a] * Ri[3 + j] + du[6 + a] * Ri[6 + j];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) G[3 * i + j] = R[i] * Lm[j] + R[3 + i] * Lm[3 + j] + R[6 + i] * Lm[6 + j];
-  const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
-  const double w0 = Ki[0] * g0 + Ki[1] * g1 + Ki[2] * g2;
-  const double w1 = Ki[3] * g0 + Ki[4] * g1 + Ki[5] * g2;
-  const double w2 = Ki[6] * g0 + Ki[7] * g1 + Ki[8] * g2;
-  const double ws00 = -w2 * S_[3] + w1 * S_[6];
-  const double ws01 = -w2 * S_[4] + w1 * S_[7];
-  const double ws02 = -w2 * S_[5] + w1 * S_[8];
-  const double ws10 = w2 * S_[0] - w0 * S_[6];
-  const double ws11 = w2 * S_[1] - w0 * S_[7];
-  const double ws12 = w2 * S_[2] - w0 * S_[8];
-  const double ws20 = -w1 * S_[0] + w0 * S_[3];
-  const double ws21 = -w1 * S_[1] + w0 * S_[4];
-  const double ws22 = -w1 * S_[2] + w0 * S_[5];
-  y[0] = G[0] - ws00;
-  y[1] = G[4] - ws11;
-  y[2] = G[8] - ws22;
-  y[3] = 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21);
-  y[4] = 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20);
-  y[5] = 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10);
+  tet_forward_uv(T, Ri, uu, y);
 }
 
 // ---------------------------------------------------------------- family

@@ -741,38 +741,54 @@ DI void tet_forward(const Ctx& c, int t, int env, const TetC& T, const double* R
 // Algebraically identical to the columns of tet_col (numba_backend.py:283-311);
 // only the association of the sums differs (~1e-16 relative), for ~5x fewer
 // FP64 operations. ax(M) = (M21 - M12, M02 - M20, M10 - M01) as g in the ref.
-DI void tet_contrib_fast(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
-                         const double* z) {
-  const int E = c.D.E, nt = c.D.nt;
+// Structured tet operators (the default, non-bitwise mode): explicit fused
+// multiply-adds (the file is built with --fmad=false so that every
+// reference-order expression elsewhere keeps numba's rounding). dot3(a..) =
+// a0 b0 + a1 b1 + a2 b2 as two FMAs.
+DI double dot3(double a0, double b0, double a1, double b1, double a2, double b2) {
+  return __fma_rn(a2, b2, __fma_rn(a1, b1, a0 * b0));
+}
+
+// J^T z of one tet as its 12 column sums: (J^T z)_{3v+a} = R_a . (Z w_v -
+// n x w_v) with Z = sym-voigt(z), n = K^-1 ax(Z S)
+DI void tet_jt_cols(const TetC& T, const double* Ri, const double* z, double* col12) {
   const double* S = T.S;
   const double* Ki = T.K;
   const double* R = T.R;
   const double Z00 = z[0], Z11 = z[1], Z22 = z[2];
   const double Z12 = 0.5 * z[3], Z02 = 0.5 * z[4], Z01 = 0.5 * z[5];
-  const double N21 = Z02 * S[1] + Z12 * S[4] + Z22 * S[7];
-  const double N12 = Z01 * S[2] + Z11 * S[5] + Z12 * S[8];
-  const double N02 = Z00 * S[2] + Z01 * S[5] + Z02 * S[8];
-  const double N20 = Z02 * S[0] + Z12 * S[3] + Z22 * S[6];
-  const double N10 = Z01 * S[0] + Z11 * S[3] + Z12 * S[6];
-  const double N01 = Z00 * S[1] + Z01 * S[4] + Z02 * S[7];
+  const double N21 = dot3(Z02, S[1], Z12, S[4], Z22, S[7]);
+  const double N12 = dot3(Z01, S[2], Z11, S[5], Z12, S[8]);
+  const double N02 = dot3(Z00, S[2], Z01, S[5], Z02, S[8]);
+  const double N20 = dot3(Z02, S[0], Z12, S[3], Z22, S[6]);
+  const double N10 = dot3(Z01, S[0], Z11, S[3], Z12, S[6]);
+  const double N01 = dot3(Z00, S[1], Z01, S[4], Z02, S[7]);
   const double m0 = N21 - N12, m1 = N02 - N20, m2 = N10 - N01;
-  const double n0 = Ki[0] * m0 + Ki[1] * m1 + Ki[2] * m2;
-  const double n1 = Ki[3] * m0 + Ki[4] * m1 + Ki[5] * m2;
-  const double n2 = Ki[6] * m0 + Ki[7] * m1 + Ki[8] * m2;
+  const double n0 = dot3(Ki[0], m0, Ki[1], m1, Ki[2], m2);
+  const double n1 = dot3(Ki[3], m0, Ki[4], m1, Ki[5], m2);
+  const double n2 = dot3(Ki[6], m0, Ki[7], m1, Ki[8], m2);
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
     double wv[3];
     tet_wv(Ri, v, wv);
-    const double q0 = (Z00 * wv[0] + Z01 * wv[1] + Z02 * wv[2]) - (n1 * wv[2] - n2 * wv[1]);
-    const double q1 = (Z01 * wv[0] + Z11 * wv[1] + Z12 * wv[2]) - (n2 * wv[0] - n0 * wv[2]);
-    const double q2 = (Z02 * wv[0] + Z12 * wv[1] + Z22 * wv[2]) - (n0 * wv[1] - n1 * wv[0]);
+    const double q0 = dot3(Z00, wv[0], Z01, wv[1], Z02, wv[2]) - __fma_rn(n1, wv[2], -n2 * wv[1]);
+    const double q1 = dot3(Z01, wv[0], Z11, wv[1], Z12, wv[2]) - __fma_rn(n2, wv[0], -n0 * wv[2]);
+    const double q2 = dot3(Z02, wv[0], Z12, wv[1], Z22, wv[2]) - __fma_rn(n0, wv[1], -n1 * wv[0]);
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      c.K.tC[TCX(3 * v + a, t)] = R[3 * a] * q0 + R[3 * a + 1] * q1 + R[3 * a + 2] * q2;
+    for (int a = 0; a < 3; ++a) col12[3 * v + a] = dot3(R[3 * a], q0, R[3 * a + 1], q1, R[3 * a + 2], q2);
   }
 }
+DI void tet_contrib_fast(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
+                         const double* z) {
+  const int E = c.D.E, nt = c.D.nt;
+  double col12[12];
+  tet_jt_cols(T, Ri, z, col12);
+#pragma unroll
+  for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
+}
 
-// J u of one tet from its 4 node values uv[3v+a] (structured chain rule)
+// J u of one tet from its 4 node values uv[3v+a] (structured chain rule):
+// voigt(sym(G) - sym(skew(K^-1 ax G) S)), G = R^T sum_v u_v w_v^T
 DI void tet_forward_uv(const TetC& T, const double* Ri, const double* uv, double* y) {
   const double* R = T.R;
   const double* S = T.S;
@@ -787,31 +803,31 @@ DI void tet_forward_uv(const TetC& T, const double* Ri, const double* uv, double
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) L[3 * a + j] = du[a] * Ri[j] + du[3 + a] * Ri[3 + j] + du[6 + a] * Ri[6 + j];
+    for (int j = 0; j < 3; ++j) L[3 * a + j] = dot3(du[a], Ri[j], du[3 + a], Ri[3 + j], du[6 + a], Ri[6 + j]);
   double G[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) G[3 * i + j] = R[i] * L[j] + R[3 + i] * L[3 + j] + R[6 + i] * L[6 + j];
+    for (int j = 0; j < 3; ++j) G[3 * i + j] = dot3(R[i], L[j], R[3 + i], L[3 + j], R[6 + i], L[6 + j]);
   const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
-  const double w0 = Ki[0] * g0 + Ki[1] * g1 + Ki[2] * g2;
-  const double w1 = Ki[3] * g0 + Ki[4] * g1 + Ki[5] * g2;
-  const double w2 = Ki[6] * g0 + Ki[7] * g1 + Ki[8] * g2;
-  const double ws00 = -w2 * S[3] + w1 * S[6];
-  const double ws01 = -w2 * S[4] + w1 * S[7];
-  const double ws02 = -w2 * S[5] + w1 * S[8];
-  const double ws10 = w2 * S[0] - w0 * S[6];
-  const double ws11 = w2 * S[1] - w0 * S[7];
-  const double ws12 = w2 * S[2] - w0 * S[8];
-  const double ws20 = -w1 * S[0] + w0 * S[3];
-  const double ws21 = -w1 * S[1] + w0 * S[4];
-  const double ws22 = -w1 * S[2] + w0 * S[5];
+  const double w0 = dot3(Ki[0], g0, Ki[1], g1, Ki[2], g2);
+  const double w1 = dot3(Ki[3], g0, Ki[4], g1, Ki[5], g2);
+  const double w2 = dot3(Ki[6], g0, Ki[7], g1, Ki[8], g2);
+  const double ws00 = __fma_rn(w1, S[6], -w2 * S[3]);
+  const double ws01 = __fma_rn(w1, S[7], -w2 * S[4]);
+  const double ws02 = __fma_rn(w1, S[8], -w2 * S[5]);
+  const double ws10 = __fma_rn(w2, S[0], -w0 * S[6]);
+  const double ws11 = __fma_rn(w2, S[1], -w0 * S[7]);
+  const double ws12 = __fma_rn(w2, S[2], -w0 * S[8]);
+  const double ws20 = __fma_rn(w0, S[3], -w1 * S[0]);
+  const double ws21 = __fma_rn(w0, S[4], -w1 * S[1]);
+  const double ws22 = __fma_rn(w0, S[5], -w1 * S[2]);
   y[0] = G[0] - ws00;
   y[1] = G[4] - ws11;
   y[2] = G[8] - ws22;
-  y[3] = 0.5 * (G[5] + G[7]) - 0.5 * (ws12 + ws21);
-  y[4] = 0.5 * (G[2] + G[6]) - 0.5 * (ws02 + ws20);
-  y[5] = 0.5 * (G[1] + G[3]) - 0.5 * (ws01 + ws10);
+  y[3] = 0.5 * ((G[5] + G[7]) - (ws12 + ws21));
+  y[4] = 0.5 * ((G[2] + G[6]) - (ws02 + ws20));
+  y[5] = 0.5 * ((G[1] + G[3]) - (ws01 + ws10));
 }
 DI void tet_node_vals(const Ctx& c, int t, int env, const double* vec, double* uv) {
   const int E = c.D.E, nt = c.D.nt;
