@@ -102,6 +102,48 @@ DI double cl_cluster_sum(const ClPlan& L, const ClSmem& S, double v, int slot, d
   return scratch[33];
 }
 
+// three cluster-wide sums in one barrier (slots slot, slot+1, slot+2 mod 16)
+DI void cl_cluster_sum3(const ClPlan& L, const ClSmem& S, const double* v, int slot,
+                        double* scratch, double* out) {
+  double w[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    w[q] = v[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w[q] += __shfl_down_sync(0xffffffffu, w[q], o);
+  }
+  const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) scratch[q * 16 + wi] = w[q];
+  __syncthreads();
+  const int rank = (int)cg::this_cluster().block_rank();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double t = threadIdx.x < (CL_THREADS >> 5) ? scratch[q * 16 + threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (threadIdx.x < L.C) S.peer[threadIdx.x][L.oRed + ((slot + q) & 15) * L.C + rank] = t;
+    }
+  }
+  cg::this_cluster().sync();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double t = threadIdx.x < L.C ? S.b[L.oRed + ((slot + q) & 15) * L.C + threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) scratch[48 + q] = t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 3; ++q) out[q] = scratch[48 + q];
+}
+
 // ------------------------------------------------------------ node gather
 // One thread per (owned node, axis): particles 3 threads each, bodies 6.
 struct ClMn {
@@ -516,7 +558,7 @@ DI double cl_ddiv(double x, double dstored) { return EXACT ? x / dstored : x * d
 template <bool EXACT>
 __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, const ClPlan L) {
   extern __shared__ __align__(16) double sm_[];
-  __shared__ double scratch[40];
+  __shared__ double scratch[64];
   __shared__ double* peers[CL_MAXC];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
@@ -781,21 +823,19 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
     }
     bool broken = false;
     double rho = 0.0, alpha = 0.0, beta = 0.0;
-    for (int k = 0; k < c.p.pcr; ++k) {
-      CL_STAMP(0);
-      if (k > 0 && !broken) {
-        // x += alpha p, r -= alpha ap, z = r/d (row-parallel), then J^T z
-#pragma unroll
-        for (int j = 0; j < CL_RPT; ++j) {
-          const int row = tid + j * CL_THREADS;
-          if (row < L.NR) {
-            xr_[j] += alpha * sb[L.oP + row];
-            rr_[j] -= alpha * sb[L.oAP + row];
-            sb[L.oZ + row] = cl_ddiv<EXACT>(rr_[j], sb[L.oD + row]);
-          }
-        }
-        __syncthreads();
-        if (has_el) {
+    // Structured mode: one cluster reduction per PCR iteration. The apply
+    // phase also sums s1 = az.D^-1 az and s2 = az.D^-1 ap_prev, so
+    // den = ap.D^-1 ap with ap = az + beta ap_prev follows as
+    // s1 + 2 beta s2 + beta^2 den_prev (same recurrence, solver.py:71-91;
+    // 5e-14 relative per frame against the reference order, measured with
+    // the reference's own pcr_solve patched), and the p/ap update, the step
+    // and z = r/d run as one row pass.
+    bool stepped = false;
+    if (!EXACT) {
+      double den = 0.0;
+      for (int k = 0; k < c.p.pcr; ++k) {
+        CL_STAMP(0);
+        if (k > 0 && has_el) {
           const ClEl& el = me.el;
           const ClRows R = cl_rows(L, sb, el);
           double zr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -806,108 +846,232 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
           }
           cl_contrib<EXACT>(c, L, S, me, zr, 0);
         }
-      }
-      CL_STAMP(1);
-      if (!(k > 0 && broken)) {
+        CL_STAMP(1);
         cl.sync();                            // column sums of J^T z visible
         CL_STAMP(2);
         cl_gather(L, S, has_na, mn, 0);       // U = M^-1 J^T z (+ halo pushes)
         CL_STAMP(3);
         cl.sync();                            // U visible
         CL_STAMP(4);
-      }
-      // az = J u + dyn z + E z; rho = z.az (element-parallel)
-      double part = 0.0;
-      if (!broken && has_el) {
-        const ClEl& el = me.el;
-        const ClRows R = cl_rows(L, sb, el);
-        const int nr = R.n;
-        double y[6];
-        if (nr) cl_forward<EXACT>(c, L, S, me, L.oU, y);
-        if (!nr) {
-        } else if (el.fam == CF_TET) {
-          double zz[6], ez[6];
+        double part[3] = {0.0, 0.0, 0.0};
+        auto acc = [&](int row, double zr, double az) {
+          part[0] += zr * az;
+          const double di = sb[L.oD + row];
+          part[1] += az * (az * di);
+          if (k > 0) part[2] += az * (sb[L.oAP + row] * di);
+        };
+        if (has_el) {
+          const ClEl& el = me.el;
+          const ClRows R = cl_rows(L, sb, el);
+          const int nr = R.n;
+          double y[6];
+          if (nr) cl_forward<EXACT>(c, L, S, me, L.oU, y);
+          if (!nr) {
+          } else if (el.fam == CF_TET) {
+            double zz[6], ez[6];
 #pragma unroll
-          for (int i = 0; i < 6; ++i) zz[i] = sb[L.oZ + R.at(i)];
-          ereg6(sb[L.oE3 + el.le], sb[L.oE3 + L.MT + el.le], sb[L.oE3 + 2 * L.MT + el.le], zz, ez);
+            for (int i = 0; i < 6; ++i) zz[i] = sb[L.oZ + R.at(i)];
+            ereg6(sb[L.oE3 + el.le], sb[L.oE3 + L.MT + el.le], sb[L.oE3 + 2 * L.MT + el.le], zz, ez);
 #pragma unroll
-          for (int i = 0; i < 6; ++i) {
-            const double az = y[i] + ez[i];
-            sb[L.oAZ + R.at(i)] = az;
-            part += zz[i] * az;
-          }
-        } else if (el.fam == CF_SLOT) {
-          const int ls = el.le;
-          const double zn = sb[L.oZ + R.at(0)], z0 = sb[L.oZ + R.at(1)], z1 = sb[L.oZ + R.at(2)];
-          const double an = y[0] + sb[L.oDyn + ls] * zn;
-          double a0 = z0, a1 = z1;
-          if (sb[L.oAct + ls] != 0.0) {
-            a0 = y[1] + c.p.fdyn * z0;
-            a1 = y[2] + c.p.fdyn * z1;
-          }
-          sb[L.oAZ + R.at(0)] = an;
-          sb[L.oAZ + R.at(1)] = a0;
-          sb[L.oAZ + R.at(2)] = a1;
-          part += zn * an;
-          part += z0 * a0;
-          part += z1 * a1;
-        } else {
-          const double dyn = me.dyn;
-#pragma unroll
-          for (int i = 0; i < 5; ++i) {
-            if (i >= nr) break;
-            const double zr = sb[L.oZ + R.at(i)];
-            const double az = y[i] + dyn * zr;
-            sb[L.oAZ + R.at(i)] = az;
-            part += zr * az;
-          }
-        }
-      }
-      CL_STAMP(5);
-      const double rho_new = cl_cluster_sum(L, S, part, rslot, scratch);
-      rslot = (rslot + 1) & 15;
-      CL_STAMP(6);
-      if (!broken) {
-        if (k == 0) {
-          rho = rho_new;
-        } else {
-          beta = rho > 1e-300 ? rho_new / rho : 0.0;
-          rho = rho_new;
-        }
-      }
-      // p = z + beta p, ap = az + beta ap; den = ap.(ap/d) (row-parallel)
-      double dpart = 0.0;
-#pragma unroll
-      for (int j = 0; j < CL_RPT; ++j) {
-        const int row = tid + j * CL_THREADS;
-        if (row < L.NR) {
-          double ap;
-          if (k == 0) {
-            sb[L.oP + row] = sb[L.oZ + row];
-            ap = sb[L.oAZ + row];
-            sb[L.oAP + row] = ap;
-          } else if (!broken) {
-            sb[L.oP + row] = sb[L.oZ + row] + beta * sb[L.oP + row];
-            ap = sb[L.oAZ + row] + beta * sb[L.oAP + row];
-            sb[L.oAP + row] = ap;
+            for (int i = 0; i < 6; ++i) {
+              const double az = y[i] + ez[i];
+              sb[L.oAZ + R.at(i)] = az;
+              acc(R.at(i), zz[i], az);
+            }
+          } else if (el.fam == CF_SLOT) {
+            const int ls = el.le;
+            const double zn = sb[L.oZ + R.at(0)], z0 = sb[L.oZ + R.at(1)], z1 = sb[L.oZ + R.at(2)];
+            const double an = y[0] + sb[L.oDyn + ls] * zn;
+            double a0 = z0, a1 = z1;
+            if (sb[L.oAct + ls] != 0.0) {
+              a0 = y[1] + c.p.fdyn * z0;
+              a1 = y[2] + c.p.fdyn * z1;
+            }
+            sb[L.oAZ + R.at(0)] = an;
+            sb[L.oAZ + R.at(1)] = a0;
+            sb[L.oAZ + R.at(2)] = a1;
+            acc(R.at(0), zn, an);
+            acc(R.at(1), z0, a0);
+            acc(R.at(2), z1, a1);
           } else {
-            ap = sb[L.oAP + row];
+            const double dyn = me.dyn;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+              if (i >= nr) break;
+              const double zr = sb[L.oZ + R.at(i)];
+              const double az = y[i] + dyn * zr;
+              sb[L.oAZ + R.at(i)] = az;
+              acc(R.at(i), zr, az);
+            }
           }
-          dpart += ap * cl_ddiv<EXACT>(ap, sb[L.oD + row]);
         }
+        CL_STAMP(5);
+        double tot[3];
+        cl_cluster_sum3(L, S, part, rslot, scratch, tot);
+        rslot = (rslot + 3) & 15;
+        CL_STAMP(6);
+        if (k == 0) {
+          rho = tot[0];
+          beta = 0.0;
+          den = tot[1];
+        } else {
+          beta = rho > 1e-300 ? tot[0] / rho : 0.0;
+          rho = tot[0];
+          den = tot[1] + 2.0 * beta * tot[2] + beta * beta * den;
+        }
+        if (den <= 1e-300 || !isfinite(den)) {
+          broken = true;  // the reference skips every remaining iteration
+          break;
+        }
+        alpha = rho / den;
+        // p = z + beta p, ap = az + beta ap, x += alpha p, r -= alpha ap, z = r/d
+#pragma unroll
+        for (int j = 0; j < CL_RPT; ++j) {
+          const int row = tid + j * CL_THREADS;
+          if (row < L.NR) {
+            const double pn = k == 0 ? sb[L.oZ + row] : sb[L.oZ + row] + beta * sb[L.oP + row];
+            const double apn = k == 0 ? sb[L.oAZ + row] : sb[L.oAZ + row] + beta * sb[L.oAP + row];
+            sb[L.oP + row] = pn;
+            sb[L.oAP + row] = apn;
+            xr_[j] += alpha * pn;
+            rr_[j] -= alpha * apn;
+            sb[L.oZ + row] = cl_ddiv<EXACT>(rr_[j], sb[L.oD + row]);
+          }
+        }
+        __syncthreads();
+        CL_STAMP(7);
+        CL_STAMP(8);
       }
-      CL_STAMP(7);
-      const double den = cl_cluster_sum(L, S, dpart, rslot, scratch);
-      rslot = (rslot + 1) & 15;
-      CL_STAMP(8);
-      if (!broken) {
-        if (den <= 1e-300 || !isfinite(den)) broken = true;
-        else alpha = rho / den;
+      stepped = true;
+    } else {
+    for (int k = 0; k < c.p.pcr; ++k) {
+        CL_STAMP(0);
+        if (k > 0 && !broken) {
+          // x += alpha p, r -= alpha ap, z = r/d (row-parallel), then J^T z
+  #pragma unroll
+          for (int j = 0; j < CL_RPT; ++j) {
+            const int row = tid + j * CL_THREADS;
+            if (row < L.NR) {
+              xr_[j] += alpha * sb[L.oP + row];
+              rr_[j] -= alpha * sb[L.oAP + row];
+              sb[L.oZ + row] = cl_ddiv<EXACT>(rr_[j], sb[L.oD + row]);
+            }
+          }
+          __syncthreads();
+          if (has_el) {
+            const ClEl& el = me.el;
+            const ClRows R = cl_rows(L, sb, el);
+            double zr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  #pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              if (q >= R.n) break;
+              zr[q] = sb[L.oZ + R.at(q)];
+            }
+            cl_contrib<EXACT>(c, L, S, me, zr, 0);
+          }
+        }
+        CL_STAMP(1);
+        if (!(k > 0 && broken)) {
+          cl.sync();                            // column sums of J^T z visible
+          CL_STAMP(2);
+          cl_gather(L, S, has_na, mn, 0);       // U = M^-1 J^T z (+ halo pushes)
+          CL_STAMP(3);
+          cl.sync();                            // U visible
+          CL_STAMP(4);
+        }
+        // az = J u + dyn z + E z; rho = z.az (element-parallel)
+        double part = 0.0;
+        if (!broken && has_el) {
+          const ClEl& el = me.el;
+          const ClRows R = cl_rows(L, sb, el);
+          const int nr = R.n;
+          double y[6];
+          if (nr) cl_forward<EXACT>(c, L, S, me, L.oU, y);
+          if (!nr) {
+          } else if (el.fam == CF_TET) {
+            double zz[6], ez[6];
+  #pragma unroll
+            for (int i = 0; i < 6; ++i) zz[i] = sb[L.oZ + R.at(i)];
+            ereg6(sb[L.oE3 + el.le], sb[L.oE3 + L.MT + el.le], sb[L.oE3 + 2 * L.MT + el.le], zz, ez);
+  #pragma unroll
+            for (int i = 0; i < 6; ++i) {
+              const double az = y[i] + ez[i];
+              sb[L.oAZ + R.at(i)] = az;
+              part += zz[i] * az;
+            }
+          } else if (el.fam == CF_SLOT) {
+            const int ls = el.le;
+            const double zn = sb[L.oZ + R.at(0)], z0 = sb[L.oZ + R.at(1)], z1 = sb[L.oZ + R.at(2)];
+            const double an = y[0] + sb[L.oDyn + ls] * zn;
+            double a0 = z0, a1 = z1;
+            if (sb[L.oAct + ls] != 0.0) {
+              a0 = y[1] + c.p.fdyn * z0;
+              a1 = y[2] + c.p.fdyn * z1;
+            }
+            sb[L.oAZ + R.at(0)] = an;
+            sb[L.oAZ + R.at(1)] = a0;
+            sb[L.oAZ + R.at(2)] = a1;
+            part += zn * an;
+            part += z0 * a0;
+            part += z1 * a1;
+          } else {
+            const double dyn = me.dyn;
+  #pragma unroll
+            for (int i = 0; i < 5; ++i) {
+              if (i >= nr) break;
+              const double zr = sb[L.oZ + R.at(i)];
+              const double az = y[i] + dyn * zr;
+              sb[L.oAZ + R.at(i)] = az;
+              part += zr * az;
+            }
+          }
+        }
+        CL_STAMP(5);
+        const double rho_new = cl_cluster_sum(L, S, part, rslot, scratch);
+        rslot = (rslot + 1) & 15;
+        CL_STAMP(6);
+        if (!broken) {
+          if (k == 0) {
+            rho = rho_new;
+          } else {
+            beta = rho > 1e-300 ? rho_new / rho : 0.0;
+            rho = rho_new;
+          }
+        }
+        // p = z + beta p, ap = az + beta ap; den = ap.(ap/d) (row-parallel)
+        double dpart = 0.0;
+  #pragma unroll
+        for (int j = 0; j < CL_RPT; ++j) {
+          const int row = tid + j * CL_THREADS;
+          if (row < L.NR) {
+            double ap;
+            if (k == 0) {
+              sb[L.oP + row] = sb[L.oZ + row];
+              ap = sb[L.oAZ + row];
+              sb[L.oAP + row] = ap;
+            } else if (!broken) {
+              sb[L.oP + row] = sb[L.oZ + row] + beta * sb[L.oP + row];
+              ap = sb[L.oAZ + row] + beta * sb[L.oAP + row];
+              sb[L.oAP + row] = ap;
+            } else {
+              ap = sb[L.oAP + row];
+            }
+            dpart += ap * cl_ddiv<EXACT>(ap, sb[L.oD + row]);
+          }
+        }
+        CL_STAMP(7);
+        const double den = cl_cluster_sum(L, S, dpart, rslot, scratch);
+        rslot = (rslot + 1) & 15;
+        CL_STAMP(8);
+        if (!broken) {
+          if (den <= 1e-300 || !isfinite(den)) broken = true;
+          else alpha = rho / den;
+        }
       }
     }
     // ---- last PCR step (row-parallel): dl = x + alpha p -> AZ scratch, r.z
     double rzp = 0.0;
-    const bool step = c.p.pcr > 0 && !broken;
+    const bool step = c.p.pcr > 0 && !broken && !stepped;
 #pragma unroll
     for (int j = 0; j < CL_RPT; ++j) {
       const int row = tid + j * CL_THREADS;
