@@ -93,8 +93,20 @@ dim3 grid_items(const Dims& D, long n, long cap_blocks) {
   if (gy > 65535) gy = 65535;
   return dim3(D.tiles, (unsigned)gy);
 }
-constexpr long kStreamBlocks = 148 * 8;  // 8 resident 256-thread CTAs per SM
-constexpr long kReduceBlocks = 148 * 8;
+// grid caps (CTAs of 256 threads); SS_STREAM_BLOCKS / SS_REDUCE_BLOCKS
+// override them at ss_create for tuning
+long env_long(const char* name, long dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atol(v) : dflt;
+}
+// Measured on the 1024-env snake (tools/grid_sweep.sh): the PCR row/element
+// kernels gain from 16 CTAs per SM-slot of grid (more independent blocks in
+// flight: k_pcr_step 49.3 -> 45.1 ms/frame), the reducing kernels from
+// exactly one resident wave (no tail wave: k_apply_rows 37.8 -> 35.5), the
+// gather and eval kernels are best at 8 per SM.
+long kStreamBlocks = 148 * 32;  // PCR step, tet J^T z, element kernels without reduction
+long kEvalBlocks = 148 * 8;     // gather, per-substep eval / integrate kernels
+long kReduceBlocks = 148 * 2;   // per-env reduction kernels: one resident wave (set at create)
 
 // kernel names for the profiler (ss_profile_frames)
 const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
@@ -141,15 +153,16 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 blk(SS_THREADS);
   int n = 0;
   const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
-  const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, kStreamBlocks);
-  const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, kStreamBlocks);
-  const dim3 g_slots = grid_items(D, D.ns, kStreamBlocks);
+  const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, kEvalBlocks);
+  const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, kEvalBlocks);
+  const dim3 g_slots = grid_items(D, D.ns, kEvalBlocks);
+  const dim3 g_eval = grid_items(D, D.nt, kEvalBlocks);
   const dim3 g_tet = grid_items(D, D.nt, kStreamBlocks);
-  const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, kStreamBlocks);
-  const dim3 g_gather = grid_items(D, D.P + D.nb, kStreamBlocks);
+  const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, kEvalBlocks);
+  const dim3 g_gather = grid_items(D, D.P + D.nb, kEvalBlocks);
   const dim3 g_el = grid_items(D, n_el, kStreamBlocks);
   const dim3 g_red(D.tiles, H->gy_red);
-  const dim3 g_int = grid_items(D, D.P + D.nb, kStreamBlocks);
+  const dim3 g_int = grid_items(D, D.P + D.nb, kEvalBlocks);
   const double* xs_lam = c.S.lam;
   const double* xc_lam = c.K.lamc;
   const double* xs_z = c.K.z;
@@ -162,7 +175,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   for (int sub = 0; sub < c.p.substeps; ++sub) {
     LAUNCH(k_pre, g_pre, c, gait && sub == 0 ? 1 : 0);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
-    if (D.nt) LAUNCH(k_eval_tet<EX>, g_tet, c);  // + tet J^T lam
+    if (D.nt) LAUNCH(k_eval_tet<EX>, g_eval, c);  // + tet J^T lam
     if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
     if (H->use_cluster) {
       // whole Newton loop, one environment per cluster (ss_cluster.cuh)
@@ -652,6 +665,16 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   if (t->n_channels % 2) return fail(SS_EINVAL, "n_channels must be even (2 per link)");
   *out = nullptr;
   CK(cudaSetDevice(device));
+  {
+    int sms = 148, occ_a = 2, occ_d = 2;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_apply_rows<false>, SS_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir, SS_THREADS, 0);
+    const long resident = (long)sms * std::max(1, std::min(occ_a, occ_d));
+    kStreamBlocks = env_long("SS_STREAM_BLOCKS", 32L * sms);
+    kEvalBlocks = env_long("SS_EVAL_BLOCKS", 8L * sms);
+    kReduceBlocks = env_long("SS_REDUCE_BLOCKS", resident);
+  }
 
   Dims D{};
   // lanes of one wave: ss_params.wave_envs, or by default at most
@@ -970,11 +993,11 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
 
   // cluster-resident Newton solver plan (ss_params.solver_mode: 0 auto, 1 streaming,
   // 2 cluster). Auto picks the cluster solver for small batches, where the streaming
-  // kernels are launch/latency-bound, and streaming from kAutoClusterMaxEnvs up
-  // (measured crossover: 1 env 483 vs 128 steps/s, 64 envs 3528 vs 2754, 128 envs
-  // 3770 vs 3750, 256 envs 3878 vs 4470; tools/solver_crossover.sh).
+  // kernels are launch/latency-bound, and streaming above kAutoClusterMaxEnvs
+  // (tools/solver_crossover.sh, v2.8 grids: 1 env 512 vs 129 steps/s, 16 envs 2862 vs
+  // 1996, 32 envs 3537 vs 2877, 48 envs 2718 vs 2898, 64 envs 3622 vs 3862).
   {
-    constexpr int kAutoClusterMaxEnvs = 128;
+    constexpr int kAutoClusterMaxEnvs = 32;
     H->keep = p->keep_matrix ? 1 : 0;
     if (H->keep && p->solver_mode == 2) {
       ss_destroy(H);
