@@ -107,6 +107,7 @@ long env_long(const char* name, long dflt) {
 long kStreamBlocks = 148 * 32;  // PCR step, tet J^T z, element kernels without reduction
 long kEvalBlocks = 148 * 8;     // gather, per-substep eval / integrate kernels
 long kReduceBlocks = 148 * 2;   // per-env reduction kernels: one resident wave (set at create)
+long kGatherBlocks = 148 * 8;   // per-DOF gather (SS_GATHER_BLOCKS; default: one resident wave)
 
 // kernel names for the profiler (ss_profile_frames)
 const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
@@ -159,7 +160,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 g_eval = grid_items(D, D.nt, kEvalBlocks);
   const dim3 g_tet = grid_items(D, D.nt, kStreamBlocks);
   const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, kEvalBlocks);
-  const dim3 g_gather = grid_items(D, D.P + D.nb, kEvalBlocks);
+  const dim3 g_gather = grid_items(D, D.P + D.nb, kGatherBlocks);
   const dim3 g_el = grid_items(D, n_el, kStreamBlocks);
   const dim3 g_red(D.tiles, H->gy_red);
   const dim3 g_int = grid_items(D, D.P + D.nb, kEvalBlocks);
@@ -674,6 +675,9 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     kStreamBlocks = env_long("SS_STREAM_BLOCKS", 32L * sms);
     kEvalBlocks = env_long("SS_EVAL_BLOCKS", 8L * sms);
     kReduceBlocks = env_long("SS_REDUCE_BLOCKS", resident);
+    int occ_g = 4;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, k_gather, SS_THREADS, 0);
+    kGatherBlocks = env_long("SS_GATHER_BLOCKS", (long)sms * std::max(1, occ_g));
   }
 
   Dims D{};

@@ -1050,7 +1050,10 @@ __global__ void k_eval_misc(const Ctx c) {
 // present contacts, friction rows regardless of the active set.
 // xs: static rows [ms][E]; xc: contact rows [3 ns][E]; tets read their
 // column sums from tC (written by the producing element kernel).
-__global__ void __launch_bounds__(SS_THREADS) k_gather(const Ctx c, int mode,
+#ifndef SS_GATHER_MINB
+#define SS_GATHER_MINB 4
+#endif
+__global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx c, int mode,
                                                        const double* __restrict__ xs,
                                                        const double* __restrict__ xc) {
   SETUP
