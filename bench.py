@@ -299,7 +299,8 @@ def main():
     nc_mean = float(np.mean([st.contact_count for st in sim.get_stats()])) / sim.config.substeps
     # one launch covers one wave: envs per launch = n / waves on average
     waves = sim.solver_info["waves"]
-    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean) * n / waves
+    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean,
+                                                   not sim.config.exact_jacobian) * n / waves
     avg_ms = prof[top][0] / prof[top][1]
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
     traffic = None

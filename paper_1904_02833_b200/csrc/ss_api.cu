@@ -216,13 +216,13 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       if (c.p.pcr > 0) {
         LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
         LAUNCH(k_apply_rows<EX>, g_red, c, 1);
-        LAUNCH(k_pcr_dir, g_red, c, 1);
+        LAUNCH(k_pcr_dir<EX>, g_red, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
-          LAUNCH(k_pcr_step, g_el, c);
+          LAUNCH(k_pcr_step<EX>, g_el, c);
           if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
           LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
           LAUNCH(k_apply_rows<EX>, g_red, c, 0);
-          LAUNCH(k_pcr_dir, g_red, c, 0);
+          LAUNCH(k_pcr_dir<EX>, g_red, c, 0);
         }
       }
       LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0);
@@ -670,7 +670,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     int sms = 148, occ_a = 2, occ_d = 2;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_apply_rows<false>, SS_THREADS, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir, SS_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir<false>, SS_THREADS, 0);
     const long resident = (long)sms * std::max(1, std::min(occ_a, occ_d));
     kStreamBlocks = env_long("SS_STREAM_BLOCKS", 32L * sms);
     kEvalBlocks = env_long("SS_EVAL_BLOCKS", 8L * sms);

@@ -1602,6 +1602,9 @@ DI bool row_live(const Ctx& c, int row, int env) {
 // p = z + beta p, ap = az + beta ap (setup: copies), then den = ap.(ap/d)
 // and alpha = rho/den with the breakdown guard (solver.py:71-81, 90-91).
 // Element-owned rows, all loads of an element issued before its stores.
+// Structured mode (!EXACT) stores apd = ap/d in the ap buffer instead of ap
+// (ap_prev = apd_prev * d when needed): the step then needs neither ap nor d.
+template <bool EXACT>
 __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) {
   SETUP
   const bool brk = c.K.broken[env] != 0;
@@ -1638,15 +1641,15 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
         if (setup) {
           P_[o] = zr[q];
           ap = azr[q];
-          AP[o] = ap;
         } else if (!brk) {
           P_[o] = zr[q] + beta * pr[q];
-          ap = azr[q] + beta * apr[q];
-          AP[o] = ap;
+          ap = azr[q] + beta * (EXACT ? apr[q] : apr[q] * dr[q]);
         } else {
-          ap = apr[q];
+          ap = EXACT ? apr[q] : apr[q] * dr[q];
         }
-        part += ap * (ap / dr[q]);
+        const double apd = ap / dr[q];
+        if (!brk || setup) AP[o] = EXACT ? ap : apd;
+        part += ap * apd;
       }
     }
   }
@@ -1660,7 +1663,12 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
 }
 
 // x += alpha p, r -= alpha ap, z = r/d (solver.py:81-84); element-owned
-// rows, loads before stores.
+// rows, loads before stores. Structured mode (!EXACT) keeps no r vector (it
+// is d z by definition) and reads apd = ap/d from k_pcr_dir: z -= alpha apd
+// carries the same recurrence one rounding apart per row, and the pass moves
+// 6 row vectors (x p z apd in, x z out) instead of 8; k_newton_final takes
+// r = d z for the residual.
+template <bool EXACT>
 __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
   SETUP
   if (c.K.broken[env]) return;  // the reference skips the whole iteration
@@ -1682,9 +1690,9 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
         const size_t o = IX(rows[q]);
         xr[q] = X_[o];
         pr[q] = P_[o];
-        rr[q] = R_[o];
+        rr[q] = EXACT ? R_[o] : Z_[o];
         apr[q] = AP[o];
-        dr[q] = Dg[o];
+        if (EXACT) dr[q] = Dg[o];
       }
     }
 #pragma unroll
@@ -1692,9 +1700,13 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
       if (q < nr) {
         const size_t o = IX(rows[q]);
         X_[o] = xr[q] + alpha * pr[q];
-        const double r = rr[q] - alpha * apr[q];
-        R_[o] = r;
-        Z_[o] = r / dr[q];
+        if (EXACT) {
+          const double r = rr[q] - alpha * apr[q];
+          R_[o] = r;
+          Z_[o] = r / dr[q];
+        } else {
+          Z_[o] = rr[q] - alpha * apr[q];
+        }
       }
     }
   }
@@ -1745,24 +1757,30 @@ __global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int la
       if (q < nr) {
         const size_t o = IX(rows[q]);
         xr[q] = c.K.x[o];
-        rr[q] = c.K.r[o];
         zr[q] = c.K.z[o];
+        if (EXACT) rr[q] = c.K.r[o];
+        if (step || !EXACT) dr[q] = c.K.d[o];
         if (step) {
           pr[q] = c.K.p[o];
           apr[q] = c.K.ap[o];
-          dr[q] = c.K.d[o];
         }
       }
     }
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       if (q < nr) {
-        double x = xr[q], r = rr[q], z = zr[q];
+        double x = xr[q], z = zr[q];
+        double r = EXACT ? rr[q] : 0.0;
         if (step) {
           x += alpha * pr[q];
-          r -= alpha * apr[q];
-          z = r / dr[q];
+          if (EXACT) {
+            r -= alpha * apr[q];
+            z = r / dr[q];
+          } else {
+            z -= alpha * apr[q];  // the ap buffer holds ap/d (k_pcr_dir)
+          }
         }
+        if (!EXACT) r = dr[q] * z;  // structured mode keeps r = d z implicit
         part += r * z;
         dl[q] = x;
       }

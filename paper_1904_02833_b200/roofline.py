@@ -26,15 +26,17 @@ def dims_of(sim) -> dict:
                 ndof=3 * P + 6 * nb)
 
 
-def bytes_per_launch_per_env(kernel: str, d: dict, nc: float) -> float:
+def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool = True) -> float:
+    """structured: the default tet-J mode, whose k_pcr_step keeps r = d z
+    implicit and reads ap/d from k_pcr_dir (6 row vectors instead of 8)."""
     rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches
     jc = F8 * 10 * d["nt"]                       # compact tet J: quat(4) S(6); R, K^-1 rebuilt
     tc = F8 * 12 * d["nt"]                       # tet column sums J^T x
     small_j = F8 * (3 * d["nd"] + 3 * d["na"] + 60 * d["nh"] + 18 * d["nw"])
     flags = 4 * d["ns"] + F8 * 2 * nc            # present flags, actf/dynn of present
     if kernel == "k_pcr_step":
-        # read x p r ap d, write x r z (rows)
-        return F8 * 8 * rows + flags
+        # read x p r|z ap|apd [d], write x [r] z (rows)
+        return F8 * (6 if structured else 8) * rows + flags
     if kernel == "k_tet_jt":
         # z of the tet rows, compact J; write tC
         return F8 * 6 * d["nt"] + jc + tc
