@@ -1068,10 +1068,14 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
         if (k == tr.x) {
           // tet run: column sums from tC, loads hoisted 4 incidences at a time
           const double* __restrict__ tC = c.K.tC;
-          for (; k + 3 < tr.y; k += 4) {
-            double a[12];
+#ifndef SS_GATHER_UNROLL
+#define SS_GATHER_UNROLL 6
+#endif
+          constexpr int GU = SS_GATHER_UNROLL;
+          for (; k + GU - 1 < tr.y; k += GU) {
+            double a[3 * GU];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < GU; ++j) {
               const int code = c.T.inc[k + j];
               const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
               a[3 * j] = tC[TCX(3 * v, e)];
@@ -1079,7 +1083,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
               a[3 * j + 2] = tC[TCX(3 * v + 2, e)];
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < GU; ++j) {
               w0 += a[3 * j];
               w1 += a[3 * j + 1];
               w2 += a[3 * j + 2];
