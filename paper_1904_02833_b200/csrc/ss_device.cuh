@@ -488,15 +488,24 @@ __global__ void k_slots(const Ctx c) {
     c.K.lamc[IX(s)] = lam_n;
     c.K.lamc[IX(ns + s)] = lam_f0;
     c.K.lamc[IX(2 * ns + s)] = lam_f1;
+    if (c.p.newton == 0 && s < nw) {
+      // store_warm after an empty Newton loop (solver.py:522, contact.py:167-180);
+      // otherwise k_newton_final's last pass stores it
+      c.S.warm_valid[IX(s)] = present ? 1 : 0;
+      c.S.warm[IX(s)] = lam_n;
+      c.S.warm[IX(nw + s)] = lam_f0;
+      c.S.warm[IX(2 * nw + s)] = lam_f1;
+    }
     if (present) atomicAdd(&c.S.nc_cnt[env], 1);
   }
 }
 
 // ------------------------------------------------------------- tetra eval
 // numba_backend.py:137-312. The Jacobian is never stored: an element keeps
-// (R, S = sym(R^T F), K^-1) — 21 doubles, S and K^-1 bitwise symmetric —
-// and tet_col() recomputes any column with the exact expressions of the
-// reference, so every use sees the same bits the eval produced.
+// S = sym(R^T F) (6 doubles) beside its persistent quaternion; R and K^-1
+// are rebuilt bitwise from them (tet_unpack), and tet_col() recomputes any
+// column with the exact expressions of the reference, so every use sees
+// the same bits the eval produced.
 
 // compact tet Jacobian of one element in registers
 struct TetC {

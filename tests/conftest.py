@@ -48,6 +48,21 @@ def assert_state_close(got: dict, want: dict, tol=None, keys=STATE_KEYS, what=""
         if k == "warm_valid":
             assert np.array_equal(np.asarray(got[k]), np.asarray(want[k])), f"{what} {k}"
             continue
+        if k == "tet_quats":
+            # q and -q are the same rotation: a tet whose polar iteration lands on
+            # the other sign (inverted or strongly sheared elements) is equal
+            a, b = np.asarray(got[k], np.float64), np.asarray(want[k], np.float64)
+            d = np.minimum(np.abs(a - b).max(axis=-1), np.abs(a + b).max(axis=-1))
+            e = float(d.max()) / max(float(np.abs(b).max()), 1e-300) if d.size else 0.0
+            assert e <= tol.get(k, 1e-8), f"{what} {k}: rel err {e:.3e} (modulo sign)"
+            continue
+        if k == "warm" and "warm_valid" in want:
+            # a wheel without contact has no entry in the reference's _warm dict
+            # (solver.py:522): its stored values are don't-cares
+            m = np.asarray(want["warm_valid"]).astype(bool)
+            e = rel_err(np.asarray(got[k])[m], np.asarray(want[k])[m]) if m.any() else 0.0
+            assert e <= tol.get(k, 1e-8), f"{what} {k}: rel err {e:.3e}"
+            continue
         e = rel_err(got[k], want[k])
         assert e <= tol.get(k, 1e-8), f"{what} {k}: rel err {e:.3e} > {tol.get(k, 1e-8):.1e}"
 

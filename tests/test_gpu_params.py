@@ -1,0 +1,124 @@
+"""Parity beyond the default SolverConfig (solver.py:95-117): non-default
+substeps / Newton / PCR budgets, latency off, friction and contact
+parameters, exact vs structured tet Jacobian, both solvers — one frame from
+the reference's own frame-19 snake state, against the oracle with the same
+config. Plus the edge cases the path has: the PCR breakdown guard (a system
+with a zero right-hand side), non-finite commands (flagged per env, never
+raised, as harness.py:196-207), and zero PCR / Newton iterations."""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+import paper_1904_02833_b200 as M
+from conftest import assert_state_close, golden_frame, load_golden, scene_parts
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {
+    "substeps1": dict(substeps=1),
+    "substeps3_newton2": dict(substeps=3, newton_iters=2),
+    "pcr7": dict(pcr_iters=7),
+    "pcr3": dict(pcr_iters=3),
+    "mu0.4_margin0.01": dict(mu=0.4, contact_margin=0.01),
+    "fb_slopes": dict(fb_slope_min=1e-3, fb_slope_max=1.5, fb_delta=1e-8),
+    "damping0.25": dict(constraint_damping=0.25),  # unstable past one frame: frame 1 only
+    "strain_rate2": dict(max_strain_rate=2.0),
+    "ground_raised": dict(ground_height=0.004),
+}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__ as g
+    g.build()
+
+
+def _one(a):
+    return {k: v[0] for k, v in a.items()}
+
+
+@pytest.mark.parametrize("solver", ["streaming", "cluster"])
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+def test_config_variant_vs_oracle(oracle_mod, name, solver):
+    g = load_golden("step_S.npz")
+    parts, cfg = scene_parts("S")
+    cfg = dataclasses.replace(cfg, **VARIANTS[name])
+    cfg.solver = solver
+    sim = M.Simulator(config=cfg, **parts)
+    f = 19
+    before = golden_frame(g, f, "before")
+    o = oracle_mod.OracleSim(config=cfg, **parts)
+    o.set_state(before)
+    sim.set_state_arrays(before, 0, 1)
+    # less damping than the default lets this state blow up in the second frame
+    # (the reference's own two backends then disagree at 1e-5): one frame only
+    lats = (True,) if name.startswith("damping") else (True, False)
+    for latency in lats:
+        st = sim.step(g[f"f{f}.commands"], latency=latency)
+        o.step(g[f"f{f}.commands"], latency)
+        assert_state_close(_one(sim.get_state_arrays(0, 1)), o.get_state(),
+                           what=f"{name}/{solver} latency={latency}")
+        ref = o.stats()
+        assert (st.newton_iterations, st.pcr_iterations, st.contact_count,
+                st.inverted_tets) == (ref.newton_iterations, ref.pcr_iterations,
+                                      ref.contact_count, ref.inverted_tets)
+
+
+@pytest.mark.parametrize("solver", ["streaming", "cluster"])
+def test_breakdown_guard_at_rest(oracle_mod, solver):
+    """Bend fixture at rest, 0 psi, no gravity: the right-hand side is at
+    rounding level, so the PCR denominators underflow toward the breakdown
+    guard (solver.py:75-78). Same result as the oracle, and the fixture
+    stays at rest."""
+    parts, cfg = scene_parts("B")
+    cfg.solver = solver
+    sim = M.Simulator(config=cfg, **parts)
+    o = oracle_mod.OracleSim(config=cfg, **parts)
+    before = _one(sim.get_state_arrays(0, 1))
+    sim.step(np.array([0.0]), latency=True)
+    o.step(np.array([0.0]), True)
+    got = _one(sim.get_state_arrays(0, 1))
+    assert_state_close(got, o.get_state(), what=f"rest/{solver}")
+    assert np.max(np.abs(got["positions"] - before["positions"])) < 1e-12
+    assert np.all(np.isfinite(got["lam_tetra"]))
+
+
+def test_nonfinite_state_flagged_not_raised():
+    """A NaN command is routed like the reference (neither > 0 nor < 0:
+    both chambers 0, pneumatics.py:75-85); a non-finite state is flagged for
+    its env only and never raised."""
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    sim = M.BatchedSimulator(3, config=cfg, **parts)
+    cmds = np.zeros((3, 4))
+    cmds[1, 2] = np.nan
+    sim.step(cmds, latency=False)
+    assert all(s.finite for s in sim.get_stats())
+    assert np.all(np.isfinite(sim.get_state_arrays()["pressures"]))
+    v = sim.get_state_arrays(1, 1)["velocities"]
+    v[0, 5, 1] = np.nan
+    sim.set_state_arrays({"velocities": v}, 1, 1)
+    sim.step(np.zeros((3, 4)), latency=False)
+    fin = [s.finite for s in sim.get_stats()]
+    assert fin[0] == 1 and fin[2] == 1 and fin[1] == 0
+    st = sim.get_state_arrays()
+    assert np.all(np.isfinite(st["positions"][0])) and np.all(np.isfinite(st["positions"][2]))
+
+
+@pytest.mark.parametrize("kw", [dict(pcr_iters=0), dict(newton_iters=0)], ids=["pcr0", "newton0"])
+def test_zero_iteration_budgets_vs_oracle(oracle_mod, kw):
+    g = load_golden("step_S.npz")
+    parts, cfg = scene_parts("S")
+    cfg = dataclasses.replace(cfg, **kw)
+    cfg.solver = "streaming"
+    sim = M.Simulator(config=cfg, **parts)
+    before = golden_frame(g, 0, "before")
+    o = oracle_mod.OracleSim(config=cfg, **parts)
+    o.set_state(before)
+    sim.set_state_arrays(before, 0, 1)
+    sim.step(g["f0.commands"], latency=True)
+    o.step(g["f0.commands"], True)
+    assert_state_close(_one(sim.get_state_arrays(0, 1)), o.get_state(), what=str(kw))
