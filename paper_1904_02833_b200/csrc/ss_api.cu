@@ -55,6 +55,12 @@ struct Arena {
 
 }  // namespace
 
+struct GridCaps {
+  long stream = 148 * 32;  // PCR step, tet J^T z, element kernels without reduction
+  long eval = 148 * 8;     // per-substep eval / integrate kernels
+  long reduce = 148 * 2;   // per-env reduction kernels: one resident wave
+  long gather = 148 * 8;   // per-DOF gather: one resident wave
+};
 struct ss_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -75,6 +81,7 @@ struct ss_handle {
   int launches = 0;
   // cluster-resident Newton solver (0 = streaming kernels)
   int use_cluster = 0;
+  GridCaps caps;
   int keep = 0;  // keep_matrix: snapshot the last Newton rhs each frame
   ClPlan plan{};
   void* plan_mem = nullptr;
@@ -104,10 +111,20 @@ long env_long(const char* name, long dflt) {
 // flight: k_pcr_step 49.3 -> 45.1 ms/frame), the reducing kernels from
 // exactly one resident wave (no tail wave: k_apply_rows 37.8 -> 35.5), the
 // gather and eval kernels are best at 8 per SM.
-long kStreamBlocks = 148 * 32;  // PCR step, tet J^T z, element kernels without reduction
-long kEvalBlocks = 148 * 8;     // gather, per-substep eval / integrate kernels
-long kReduceBlocks = 148 * 2;   // per-env reduction kernels: one resident wave (set at create)
-long kGatherBlocks = 148 * 8;   // per-DOF gather (SS_GATHER_BLOCKS; default: one resident wave)
+// occupancy-derived caps of this device; SS_*_BLOCKS override them
+GridCaps grid_caps(int device) {
+  GridCaps g;
+  int sms = 148, occ_a = 2, occ_d = 2, occ_g = 4;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_apply_rows<false>, SS_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir<false>, SS_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, k_gather, SS_THREADS, 0);
+  g.stream = env_long("SS_STREAM_BLOCKS", 32L * sms);
+  g.eval = env_long("SS_EVAL_BLOCKS", 8L * sms);
+  g.reduce = env_long("SS_REDUCE_BLOCKS", (long)sms * std::max(1, std::min(occ_a, occ_d)));
+  g.gather = env_long("SS_GATHER_BLOCKS", (long)sms * std::max(1, occ_g));
+  return g;
+}
 
 // kernel names for the profiler (ss_profile_frames)
 const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
@@ -154,16 +171,16 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 blk(SS_THREADS);
   int n = 0;
   const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
-  const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, kEvalBlocks);
-  const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, kEvalBlocks);
-  const dim3 g_slots = grid_items(D, D.ns, kEvalBlocks);
-  const dim3 g_eval = grid_items(D, D.nt, kEvalBlocks);
-  const dim3 g_tet = grid_items(D, D.nt, kStreamBlocks);
-  const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, kEvalBlocks);
-  const dim3 g_gather = grid_items(D, D.P + D.nb, kGatherBlocks);
-  const dim3 g_el = grid_items(D, n_el, kStreamBlocks);
+  const dim3 g_links = grid_items(D, D.links > 0 ? D.links : 1, H->caps.eval);
+  const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, H->caps.eval);
+  const dim3 g_slots = grid_items(D, D.ns, H->caps.eval);
+  const dim3 g_eval = grid_items(D, D.nt, H->caps.eval);
+  const dim3 g_tet = grid_items(D, D.nt, H->caps.stream);
+  const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, H->caps.eval);
+  const dim3 g_gather = grid_items(D, D.P + D.nb, H->caps.gather);
+  const dim3 g_el = grid_items(D, n_el, H->caps.stream);
   const dim3 g_red(D.tiles, H->gy_red);
-  const dim3 g_int = grid_items(D, D.P + D.nb, kEvalBlocks);
+  const dim3 g_int = grid_items(D, D.P + D.nb, H->caps.eval);
   const double* xs_lam = c.S.lam;
   const double* xc_lam = c.K.lamc;
   const double* xs_z = c.K.z;
@@ -666,19 +683,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   if (t->n_channels % 2) return fail(SS_EINVAL, "n_channels must be even (2 per link)");
   *out = nullptr;
   CK(cudaSetDevice(device));
-  {
-    int sms = 148, occ_a = 2, occ_d = 2;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_apply_rows<false>, SS_THREADS, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir<false>, SS_THREADS, 0);
-    const long resident = (long)sms * std::max(1, std::min(occ_a, occ_d));
-    kStreamBlocks = env_long("SS_STREAM_BLOCKS", 32L * sms);
-    kEvalBlocks = env_long("SS_EVAL_BLOCKS", 8L * sms);
-    kReduceBlocks = env_long("SS_REDUCE_BLOCKS", resident);
-    int occ_g = 4;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, k_gather, SS_THREADS, 0);
-    kGatherBlocks = env_long("SS_GATHER_BLOCKS", (long)sms * std::max(1, occ_g));
-  }
+  const GridCaps caps = grid_caps(device);
 
   Dims D{};
   // lanes of one wave: ss_params.wave_envs, or by default at most
@@ -901,6 +906,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
 
   // ---- allocations
   ss_handle* H = new ss_handle();
+  H->caps = caps;
   H->device = device;
   H->c.D = D;
   H->c.p = P;
@@ -1025,7 +1031,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // reduction grid (fixed: the partial-sum count per env)
   {
     const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
-    H->gy_red = (int)grid_items(D, n_el, kReduceBlocks).y;
+    H->gy_red = (int)grid_items(D, n_el, H->caps.reduce).y;
   }
 
   // state + work (lane count read at call time: the wave cap may shrink it)
@@ -1118,7 +1124,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
       while ((1 << D.lgW) < D.W) ++D.lgW;
       D.tiles = D.E / D.W;
       H->c.D = D;
-      H->gy_red = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, kReduceBlocks).y;
+      H->gy_red = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, H->caps.reduce).y;
       sa = Arena();
       wa = Arena();
       plan_state(sa);
