@@ -197,6 +197,17 @@ int ss_step_gait(ss_handle* h, int latency, int n_frames);
 
 int ss_get_stats(ss_handle* h, int env0, int n, ss_env_stats* out);
 
+/* Episode resets on the device: ss_capture_init
+ * stores env `env`'s full state (every ss_state_view field) as the reset
+ * template; ss_reset_envs writes it into envs env_ids[0..n) and restarts
+ * their gait clocks. pos_sigma / vel_sigma > 0 add deterministic N(0,
+ * sigma^2) perturbations to the live particles' positions / velocities,
+ * drawn per (seed, env id, element) so an env's draw does not depend on
+ * which other envs reset with it. */
+int ss_capture_init(ss_handle* h, int env);
+int ss_reset_envs(ss_handle* h, const int* env_ids, int n, uint64_t seed, double pos_sigma,
+                  double vel_sigma);
+
 /* The last substep's Newton system of one env (keep_matrix handles only),
  * in the reference's snapshot layout (solver.py:511-518) for
  * Simulator.last_system / export_system (solver.py:548-581): per-family

@@ -32,6 +32,8 @@ SIGNATURES = {
     "ss_step_device": (C.c_int, [_vp, _vp, _i, _i]),
     "ss_get_stats": (C.c_int, [_vp, _i, _i, C.POINTER(SsEnvStats)]),
     "ss_export_system": (C.c_int, [_vp, _i, C.POINTER(SsSystemView)]),
+    "ss_capture_init": (C.c_int, [_vp, _i]),
+    "ss_reset_envs": (C.c_int, [_vp, C.POINTER(C.c_int), _i, C.c_uint64, C.c_double, C.c_double]),
     "ss_get_com": (C.c_int, [_vp, _i, _i, _dp]),
     "ss_observe": (C.c_int, [_vp, _i, _i, _dp]),
     "ss_set_gait": (C.c_int, [_vp, _i, _i, _dp, C.POINTER(C.c_int)]),

@@ -83,6 +83,7 @@ struct ss_handle {
   int use_cluster = 0;
   GridCaps caps;
   int keep = 0;  // keep_matrix: snapshot the last Newton rhs each frame
+  char* d_init = nullptr;  // reset template: one env's state, packed per field
   ClPlan plan{};
   void* plan_mem = nullptr;
 };
@@ -1194,6 +1195,7 @@ int ss_destroy(ss_handle* H) {
   if (H->work_mem) cudaFree(H->work_mem);
   if (H->d_cmd) cudaFree(H->d_cmd);
   if (H->d_stage) cudaFree(H->d_stage);
+  if (H->d_init) cudaFree(H->d_init);
   if (H->plan_mem) cudaFree(H->plan_mem);
   if (H->plan.dbg) cudaFree(H->plan.dbg);
   if (H->stream) cudaStreamDestroy(H->stream);
@@ -1479,6 +1481,101 @@ int ss_export_system(ss_handle* H, int env, ss_system_view* v) {
   for (int k = 0; k < 6; ++k)
     if (nI[k] && hi[k]) CK(cudaMemcpyAsync(hi[k], ip[k], 4 * nI[k], cudaMemcpyDeviceToHost, H->stream));
   CK(cudaStreamSynchronize(H->stream));
+  return SS_OK;
+}
+
+// packed byte offsets of the fields of one env (state_fields order)
+static size_t init_layout(ss_handle* H, Field* f, int nf, size_t* off) {
+  size_t o = 0;
+  for (int i = 0; i < nf; ++i) {
+    off[i] = o;
+    o += (f[i].is_int ? 4 : 8) * (size_t)f[i].A * f[i].B;
+    o = (o + 7) & ~(size_t)7;
+  }
+  return o;
+}
+
+int ss_capture_init(ss_handle* H, int env) {
+  if (!H) return fail(SS_EINVAL, "null handle");
+  const Dims& D = H->c.D;
+  if (env < 0 || env >= D.n_real) return fail(SS_EINVAL, "env out of range");
+  CK(cudaSetDevice(H->device));
+  ss_state_view none{};
+  Field f[32];
+  int nf = 0;
+  const int w = env / D.E, lane = env % D.E;
+  state_fields(H, w, &none, f, &nf);
+  size_t off[32];
+  const size_t bytes = init_layout(H, f, nf, off);
+  if (!H->d_init) CK(cudaMalloc(&H->d_init, bytes));
+  for (int i = 0; i < nf; ++i) {
+    if (f[i].A * f[i].B == 0) continue;
+    if (f[i].is_int)
+      k_gather_state<int><<<64, 256, 0, H->stream>>>((int*)(H->d_init + off[i]), (const int*)f[i].dev,
+                                                     1, f[i].A, f[i].B, f[i].swap, D.E, lane);
+    else
+      k_gather_state<double><<<64, 256, 0, H->stream>>>((double*)(H->d_init + off[i]),
+                                                        (const double*)f[i].dev, 1, f[i].A, f[i].B,
+                                                        f[i].swap, D.E, lane);
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(H->stream));
+  return SS_OK;
+}
+
+int ss_reset_envs(ss_handle* H, const int* env_ids, int n, uint64_t seed, double pos_sigma,
+                  double vel_sigma) {
+  if (!H || (n > 0 && !env_ids)) return fail(SS_EINVAL, "null argument");
+  if (!H->d_init) return fail(SS_EINVAL, "no reset template (ss_capture_init)");
+  if (pos_sigma < 0.0 || vel_sigma < 0.0 || !std::isfinite(pos_sigma) || !std::isfinite(vel_sigma))
+    return fail(SS_EINVAL, "perturbation sigmas must be finite and >= 0");
+  const Dims& D = H->c.D;
+  for (int i = 0; i < n; ++i)
+    if (env_ids[i] < 0 || env_ids[i] >= D.n_real) return fail(SS_EINVAL, "env %d out of range", env_ids[i]);
+  if (n == 0) return SS_OK;
+  CK(cudaSetDevice(H->device));
+  int rc = ensure_stage(H, 8 * (size_t)n + 8);
+  if (rc) return rc;
+  ss_state_view none{};
+  for (int w = 0; w < H->n_waves; ++w) {
+    std::vector<int> lanes, envs;
+    for (int i = 0; i < n; ++i)
+      if (env_ids[i] / D.E == w) {
+        lanes.push_back(env_ids[i] % D.E);
+        envs.push_back(env_ids[i]);
+      }
+    const int nl = (int)lanes.size();
+    if (!nl) continue;
+    int* d_l = reinterpret_cast<int*>(H->d_stage);
+    int* d_e = d_l + n;
+    CK(cudaMemcpyAsync(d_l, lanes.data(), 4 * (size_t)nl, cudaMemcpyHostToDevice, H->stream));
+    CK(cudaMemcpyAsync(d_e, envs.data(), 4 * (size_t)nl, cudaMemcpyHostToDevice, H->stream));
+    Field f[32];
+    int nf = 0;
+    state_fields(H, w, &none, f, &nf);
+    size_t off[32];
+    init_layout(H, f, nf, off);
+    for (int i = 0; i < nf; ++i) {
+      if (f[i].A * f[i].B == 0) continue;
+      // fields 0/1 are particle positions / velocities (state_fields order)
+      const double sig = i == 0 ? pos_sigma : (i == 1 ? vel_sigma : 0.0);
+      if (f[i].is_int)
+        k_reset_field<int><<<64, 256, 0, H->stream>>>((int*)f[i].dev, (const int*)(H->d_init + off[i]),
+                                                      d_l, d_e, nl, f[i].A, f[i].B, f[i].swap, D.E,
+                                                      0.0, seed, i, nullptr);
+      else
+        k_reset_field<double><<<64, 256, 0, H->stream>>>(
+            (double*)f[i].dev, (const double*)(H->d_init + off[i]), d_l, d_e, nl, f[i].A, f[i].B,
+            f[i].swap, D.E, sig, seed, i, i < 2 ? H->c.T.inv_mass : nullptr);
+      CK(cudaGetLastError());
+    }
+    // the gait clock restarts with the episode
+    std::vector<int> zeros(nl, 0);
+    for (int j = 0; j < nl; ++j)
+      CK(cudaMemcpyAsync(H->wave[w].S.gait_frame + lanes[j], zeros.data(), 4, cudaMemcpyHostToDevice,
+                         H->stream));
+    CK(cudaStreamSynchronize(H->stream));
+  }
   return SS_OK;
 }
 

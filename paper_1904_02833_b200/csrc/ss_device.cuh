@@ -2132,6 +2132,44 @@ __global__ void k_export_system(const Ctx c, int env, SysOut o) {
   }
 }
 
+// Episode reset (per-env initial-state replication and
+// perturbation on the device): write the captured template env into the listed
+// lanes of one wave. noise_sigma > 0 adds a deterministic N(0, sigma^2) draw
+// per (seed, global env, element) — a counter hash, so an env's perturbation
+// does not depend on which other envs reset with it; pinned particles
+// (inv_mass 0) are never moved (mask).
+DI unsigned long long ss_mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+DI double ss_gauss(unsigned long long seed, unsigned long long env, unsigned long long k) {
+  const unsigned long long h1 = ss_mix64(seed ^ ss_mix64(env * 0x100000001B3ull + k));
+  const unsigned long long h2 = ss_mix64(h1 ^ 0xD1B54A32D192ED03ull);
+  const double u1 = ((h1 >> 11) + 1.0) * (1.0 / 9007199254740993.0);  // (0, 1]
+  const double u2 = (h2 >> 11) * (1.0 / 9007199254740992.0);          // [0, 1)
+  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+template <typename T>
+__global__ void k_reset_field(T* dst, const T* src, const int* lanes, const int* envs, int n, int A,
+                              int B, int swap, int E, double sigma, unsigned long long seed,
+                              int salt, const double* mask) {
+  const size_t K = (size_t)A * B;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < K * n;
+       g += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(g / K);
+    const size_t k = g % K;
+    const size_t a = k / B, b = k % B;
+    const size_t item = swap ? b * A + a : k;
+    T v = src[k];
+    if (sigma > 0.0 && (!mask || mask[a] > 0.0))
+      v = (T)((double)v + sigma * ss_gauss(seed, (unsigned long long)envs[j],
+                                            ((unsigned long long)salt << 40) | k));
+    dst[item * E + lanes[j]] = v;
+  }
+}
+
 // host env-major [n][A*B] <-> device [item][E] (item = swap ? b*A+a : a*B+b).
 // Scatter also replicates env 0 into the padding lanes [n_real, E).
 template <typename T>

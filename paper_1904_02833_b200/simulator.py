@@ -132,7 +132,24 @@ class BatchedSimulator:
         init = getattr(self, "_initial_override", None)
         self.set_state_arrays(init if init is not None else self._initial_state_arrays(),
                               env0=0, n=self.n_envs)
+        if init is None:
+            _native.check(L.ss_capture_init(h, 0))  # the scene's initial state as reset template
         return h
+
+    # ------------------------------------------------------------- episodes
+    def capture_initial(self, env: int = 0) -> None:
+        """Store env `env`'s current state as the template of reset_envs."""
+        _native.check(_native.lib().ss_capture_init(self._ensure(), int(env)))
+
+    def reset_envs(self, env_ids, seed: int = 0, pos_sigma: float = 0.0,
+                   vel_sigma: float = 0.0) -> None:
+        """Reset the listed envs to the template state on the device (RL
+        episode reset), with optional deterministic
+        Gaussian perturbation of particle positions / velocities."""
+        ids = np.ascontiguousarray(np.asarray(env_ids, np.int32).ravel())
+        _native.check(_native.lib().ss_reset_envs(
+            self._ensure(), ids.ctypes.data_as(C.POINTER(C.c_int)), int(ids.size),
+            int(seed) & 0xFFFFFFFFFFFFFFFF, float(pos_sigma), float(vel_sigma)))
 
     def _sync_keep(self) -> None:
         """config.keep_matrix is read per step in the reference (solver.py:
