@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--total-envs", type=int, default=0,
                     help="fixed total environments split across GPUs (strong scaling)")
     ap.add_argument("--profile-frames", type=int, default=2)
-    ap.add_argument("--cpu-frames", type=int, default=6, help="oracle frames per host core")
+    ap.add_argument("--cpu-frames", type=int, default=12,
+                    help="oracle frames per host core (cpu_baseline sample: ~15-30 core-seconds)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scene", default="S", choices=["S", "H"],
                     help="S: the snake (configs 3/4); H: the 1M-tet snake, 1 env per GPU "
