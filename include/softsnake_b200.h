@@ -177,6 +177,11 @@ int ss_num_envs(const ss_handle* h);
 
 int ss_set_state(ss_handle* h, int env0, int n, const ss_state_view* s);
 int ss_get_state(ss_handle* h, int env0, int n, ss_state_view* s);
+/* Same with DEVICE pointers in the view (same env-major [n][...] layouts,
+ * e.g. torch CUDA tensors): scattered / gathered on the device without a
+ * host round trip; returns once the copies are complete. */
+int ss_set_state_device(ss_handle* h, int env0, int n, const ss_state_view* view);
+int ss_get_state_device(ss_handle* h, int env0, int n, ss_state_view* view);
 
 /* Advance every env by n_frames frames of dt (Simulator.step, solver.py:296).
  * commands: host [n_frames, n_envs, n_channels/2] psi, or NULL (no tick,

@@ -28,6 +28,8 @@ SIGNATURES = {
     "ss_num_envs": (C.c_int, [_vp]),
     "ss_set_state": (C.c_int, [_vp, _i, _i, C.POINTER(SsStateView)]),
     "ss_get_state": (C.c_int, [_vp, _i, _i, C.POINTER(SsStateView)]),
+    "ss_get_state_device": (C.c_int, [_vp, _i, _i, C.POINTER(SsStateView)]),
+    "ss_set_state_device": (C.c_int, [_vp, _i, _i, C.POINTER(SsStateView)]),
     "ss_step": (C.c_int, [_vp, _dp, _i, _i]),
     "ss_step_device": (C.c_int, [_vp, _vp, _i, _i]),
     "ss_get_stats": (C.c_int, [_vp, _i, _i, C.POINTER(SsEnvStats)]),

@@ -1231,7 +1231,9 @@ static std::vector<WaveChunk> wave_chunks(const ss_handle* H, int env0, int n) {
   return out;
 }
 
-int ss_set_state(ss_handle* H, int env0, int n, const ss_state_view* v) {
+// state I/O of envs [env0, env0+n): host (staged) or device (direct) pointers,
+// env-major [n][A*B] on the caller's side, [item][E] per wave on the device
+static int state_io(ss_handle* H, int env0, int n, const ss_state_view* v, bool set, bool dev) {
   if (!H || !v) return fail(SS_EINVAL, "null argument");
   const Dims& D = H->c.D;
   if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
@@ -1247,57 +1249,53 @@ int ss_set_state(ss_handle* H, int env0, int n, const ss_state_view* v) {
       const size_t elem = f[i].is_int ? 4 : 8;
       const size_t K = (size_t)f[i].A * f[i].B;
       const size_t bytes = elem * K * ch.cnt;
-      int rc = ensure_stage(H, bytes);
-      if (rc) return rc;
-      CK(cudaMemcpyAsync(H->d_stage, (const char*)f[i].host + elem * K * ch.off, bytes,
-                         cudaMemcpyHostToDevice, H->stream));
-      if (f[i].is_int)
-        k_scatter<int><<<512, 256, 0, H->stream>>>((int*)f[i].dev, (const int*)H->d_stage, ch.cnt,
-                                                   f[i].A, f[i].B, f[i].swap, D.E, ch.lane0,
-                                                   n_real_w);
-      else
-        k_scatter<double><<<512, 256, 0, H->stream>>>((double*)f[i].dev, (const double*)H->d_stage,
-                                                      ch.cnt, f[i].A, f[i].B, f[i].swap, D.E,
-                                                      ch.lane0, n_real_w);
+      char* user = (char*)f[i].host + elem * K * ch.off;
+      char* buf = user;
+      if (!dev) {
+        int rc = ensure_stage(H, bytes);
+        if (rc) return rc;
+        buf = (char*)H->d_stage;
+        if (set) CK(cudaMemcpyAsync(buf, user, bytes, cudaMemcpyHostToDevice, H->stream));
+      }
+      if (set) {
+        if (f[i].is_int)
+          k_scatter<int><<<512, 256, 0, H->stream>>>((int*)f[i].dev, (const int*)buf, ch.cnt, f[i].A,
+                                                     f[i].B, f[i].swap, D.E, ch.lane0, n_real_w);
+        else
+          k_scatter<double><<<512, 256, 0, H->stream>>>((double*)f[i].dev, (const double*)buf,
+                                                        ch.cnt, f[i].A, f[i].B, f[i].swap, D.E,
+                                                        ch.lane0, n_real_w);
+      } else {
+        if (f[i].is_int)
+          k_gather_state<int><<<512, 256, 0, H->stream>>>((int*)buf, (const int*)f[i].dev, ch.cnt,
+                                                          f[i].A, f[i].B, f[i].swap, D.E, ch.lane0);
+        else
+          k_gather_state<double><<<512, 256, 0, H->stream>>>((double*)buf, (const double*)f[i].dev,
+                                                             ch.cnt, f[i].A, f[i].B, f[i].swap,
+                                                             D.E, ch.lane0);
+      }
       CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(H->stream));
+      if (!dev) {
+        if (!set) CK(cudaMemcpyAsync(user, buf, bytes, cudaMemcpyDeviceToHost, H->stream));
+        CK(cudaStreamSynchronize(H->stream));  // the staging buffer is reused per field
+      }
     }
   }
+  if (dev) CK(cudaStreamSynchronize(H->stream));
   return SS_OK;
 }
 
+int ss_set_state(ss_handle* H, int env0, int n, const ss_state_view* v) {
+  return state_io(H, env0, n, v, true, false);
+}
 int ss_get_state(ss_handle* H, int env0, int n, ss_state_view* v) {
-  if (!H || !v) return fail(SS_EINVAL, "null argument");
-  const Dims& D = H->c.D;
-  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
-  if (n == 0) return SS_OK;
-  CK(cudaSetDevice(H->device));
-  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
-    Field f[32];
-    int nf = 0;
-    state_fields(H, ch.w, v, f, &nf);
-    for (int i = 0; i < nf; ++i) {
-      if (!f[i].host || f[i].A * f[i].B == 0) continue;
-      const size_t elem = f[i].is_int ? 4 : 8;
-      const size_t K = (size_t)f[i].A * f[i].B;
-      const size_t bytes = elem * K * ch.cnt;
-      int rc = ensure_stage(H, bytes);
-      if (rc) return rc;
-      if (f[i].is_int)
-        k_gather_state<int><<<512, 256, 0, H->stream>>>((int*)H->d_stage, (const int*)f[i].dev,
-                                                        ch.cnt, f[i].A, f[i].B, f[i].swap, D.E,
-                                                        ch.lane0);
-      else
-        k_gather_state<double><<<512, 256, 0, H->stream>>>((double*)H->d_stage,
-                                                           (const double*)f[i].dev, ch.cnt, f[i].A,
-                                                           f[i].B, f[i].swap, D.E, ch.lane0);
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync((char*)f[i].host + elem * K * ch.off, H->d_stage, bytes,
-                         cudaMemcpyDeviceToHost, H->stream));
-      CK(cudaStreamSynchronize(H->stream));
-    }
-  }
-  return SS_OK;
+  return state_io(H, env0, n, v, false, false);
+}
+int ss_set_state_device(ss_handle* H, int env0, int n, const ss_state_view* v) {
+  return state_io(H, env0, n, v, true, true);
+}
+int ss_get_state_device(ss_handle* H, int env0, int n, ss_state_view* v) {
+  return state_io(H, env0, n, v, false, true);
 }
 
 // on_device: 0 host commands, 1 device commands, 2 on-device gait (cmd unused)

@@ -220,6 +220,49 @@ class BatchedSimulator:
         _native.check(_native.lib().ss_get_state(h, env0, n, C.byref(v)))
         return {k: a for k, a in buf.arrays.items() if names is None or k in names}
 
+    def get_state_tensors(self, env0: int = 0, n: int | None = None, names=None) -> dict:
+        """State fields as torch CUDA tensors [n, ...] on the handle's device,
+        gathered on the device (ss_get_state_device; no host round trip)."""
+        import torch
+        from ._abi import STATE_FIELDS, SsStateView
+        h = self._ensure()
+        n = self.n_envs - env0 if n is None else n
+        d = self._packed.dims
+        out, v = {}, SsStateView()
+        for name, shape_fn, dt in STATE_FIELDS:
+            if names is not None and name not in names:
+                continue
+            t = torch.zeros((n,) + shape_fn(d), dtype=torch.int32 if dt == np.int32 else torch.float64,
+                            device=f"cuda:{self.device}")
+            out[name] = t
+            kind = C.POINTER(C.c_int32) if dt == np.int32 else C.POINTER(C.c_double)
+            setattr(v, name, C.cast(C.c_void_p(t.data_ptr()), kind) if t.numel() else C.cast(None, kind))
+        _native.check(_native.lib().ss_get_state_device(h, env0, n, C.byref(v)))
+        return out
+
+    def set_state_tensors(self, tensors: dict, env0: int = 0, n: int | None = None) -> None:
+        """Write state fields from torch CUDA tensors [n, ...] (reference
+        shapes) on the device (ss_set_state_device); missing fields untouched."""
+        import torch
+        from ._abi import STATE_FIELDS, SsStateView
+        h = self._ensure()
+        n = self.n_envs - env0 if n is None else n
+        d = self._packed.dims
+        v, keep = SsStateView(), []
+        for name, shape_fn, dt in STATE_FIELDS:
+            if name not in tensors:
+                continue
+            want = torch.int32 if dt == np.int32 else torch.float64
+            t = tensors[name].to(device=f"cuda:{self.device}", dtype=want).contiguous()
+            if tuple(t.shape) != (n,) + shape_fn(d):
+                raise ValueError(f"{name}: expected shape {(n,) + shape_fn(d)}, got {tuple(t.shape)}")
+            keep.append(t)
+            kind = C.POINTER(C.c_int32) if dt == np.int32 else C.POINTER(C.c_double)
+            setattr(v, name, C.cast(C.c_void_p(t.data_ptr()), kind) if t.numel() else C.cast(None, kind))
+        torch.cuda.synchronize(self.device)
+        _native.check(_native.lib().ss_set_state_device(h, env0, n, C.byref(v)))
+        del keep
+
     def get_stats(self, env0: int = 0, n: int | None = None) -> list[SsEnvStats]:
         h = self._ensure()
         n = self.n_envs - env0 if n is None else n

@@ -72,3 +72,25 @@ def test_reset_perturbation_is_deterministic_per_env():
     assert 0.5e-2 < v.std() < 2e-2
     with pytest.raises(ValueError):
         a.sim.reset_envs([n])
+
+
+def test_device_state_io_matches_host_io():
+    """ss_get/set_state_device (torch CUDA tensors) == the host path."""
+    import torch
+    n = 5
+    m = _model(n, solver="streaming")
+    m.sim.set_gait(M.GaitParams(turn_bias=0.2), m.links_per_snake, t0=[0.0, 0.1, 0.2, 0.3, 0.4])
+    m.sim.step_gait(latency=True, n_frames=2)
+    host = m.sim.get_state_arrays(1, 3)
+    dev = m.sim.get_state_tensors(1, 3)
+    for k in host:
+        assert np.array_equal(host[k], dev[k].cpu().numpy()), k
+    # write env 0's state into envs 3 and 4 from the device, then compare
+    src = m.sim.get_state_tensors(0, 1)
+    rep = {k: v.repeat((2,) + (1,) * (v.dim() - 1)) for k, v in src.items()}
+    m.sim.set_state_tensors(rep, 3, 2)
+    after = m.sim.get_state_arrays()
+    for k in after:
+        assert np.array_equal(after[k][3], after[k][0]) and np.array_equal(after[k][4], after[k][0]), k
+    with pytest.raises(ValueError):
+        m.sim.set_state_tensors({"positions": torch.zeros(1, 3, device="cuda")}, 0, 1)
