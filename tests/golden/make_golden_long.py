@@ -26,14 +26,19 @@ def main(backend="numba"):
     m = R.build_snake(sc)
     sim = m.sim
     com = [center_of_mass(sim.state)]
+    curv, contacts = [], []
     for i in range(600):
-        sim.step(m.commands(i * sim.config.dt), latency=True)
+        st = sim.step(m.commands(i * sim.config.dt), latency=True)
+        curv.append([m.link_curvature(k) for k in range(m.links_per_snake)])
+        contacts.append(st.contact_count)
         if (i + 1) % 10 == 0:
             com.append(center_of_mass(sim.state))
     com = np.array(com)
     name = "long_S.npz" if backend == "numba" else f"long_S_{backend}.npz"
-    np.savez_compressed(os.path.join(OUT, name), com=com, frames=np.int64(600))
-    print(name, com[-1] - com[0])
+    np.savez_compressed(os.path.join(OUT, name), com=com, frames=np.int64(600),
+                        curvature=np.array(curv), contacts=np.array(contacts))
+    print(name, com[-1] - com[0], np.sqrt(np.mean(np.array(curv) ** 2, axis=0)),
+          np.mean(contacts), com[:, 2].mean())
 
 
 if __name__ == "__main__":
