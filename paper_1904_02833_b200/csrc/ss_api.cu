@@ -82,6 +82,11 @@ struct ss_handle {
   // cluster-resident Newton solver (0 = streaming kernels)
   int use_cluster = 0;
   GridCaps caps;
+  // concurrent lanes: waves alternate between n_lanes workspaces / streams so
+  // two waves' kernels overlap (SS_LANES=2)
+  int n_lanes = 1;
+  cudaStream_t lane_stream[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int keep = 0;  // keep_matrix: snapshot the last Newton rhs each frame
   char* d_init = nullptr;  // reset template: one env's state, packed per field
   ClPlan plan{};
@@ -694,6 +699,11 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // sweep in DESIGN.md). The memory cap is applied after the plan below.
   constexpr int kAutoWave = 4096;
   int wave_req = p->wave_envs > 0 ? std::min(p->wave_envs, n_envs) : std::min(kAutoWave, n_envs);
+  // two concurrent lanes by default from 64 envs (1024 envs: 5,913 -> 6,127 snake-steps/s:
+  // one wave's kernel tails overlap the other's; 2 sequential waves of 512: 5,756)
+  const int lanes_req = (int)std::max(1L, std::min(2L, env_long("SS_LANES", 2)));
+  if (lanes_req > 1 && p->wave_envs <= 0 && n_envs >= 64)
+    wave_req = std::min(wave_req, ((n_envs + 1) / 2 + 31) / 32 * 32);
   auto pad_lanes = [](int n) {
     int E = 1;
     if (n <= 32) {
@@ -1138,8 +1148,9 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   H->n_waves = (n_envs + D.E - 1) / D.E;
   const size_t sblock = sa.cap;
   {
+    H->n_lanes = (lanes_req > 1 && H->n_waves > 1 && !H->use_cluster) ? 2 : 1;
     cudaError_t e1 = cudaMalloc(&H->state_mem, sblock * H->n_waves);
-    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap) : e1;
+    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap * H->n_lanes) : e1;
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
       cudaGetLastError();
       ss_destroy(H);
@@ -1147,11 +1158,22 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
                   sblock, H->n_waves, wa.cap, n_envs);
     }
   }
-  wa.base = (char*)H->work_mem;
-  plan_work(wa);
-  H->bytes += sblock * H->n_waves + wa.cap;
+  Work lane_work[2];
+  for (int l = 0; l < H->n_lanes; ++l) {
+    Arena wl;
+    wl.base = (char*)H->work_mem + wa.cap * l;
+    plan_work(wl);
+    lane_work[l] = H->c.K;
+  }
+  H->bytes += sblock * H->n_waves + wa.cap * H->n_lanes;
   CK(cudaMemsetAsync(H->state_mem, 0, sblock * H->n_waves, H->stream));
-  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap, H->stream));
+  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap * H->n_lanes, H->stream));
+  H->lane_stream[0] = H->stream;
+  if (H->n_lanes > 1) {
+    CK(cudaStreamCreateWithFlags(&H->lane_stream[1], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming));
+  }
   H->wave.assign(H->n_waves, H->c);
   H->wave_graphs.assign(H->n_waves, std::vector<cudaGraphExec_t>(6, nullptr));
   for (int w = 0; w < H->n_waves; ++w) {
@@ -1159,6 +1181,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     a.base = (char*)H->state_mem + sblock * w;
     plan_state(a);  // writes H->c.S
     H->wave[w] = H->c;
+    H->wave[w].K = lane_work[w % H->n_lanes];
     H->wave[w].D.n_real = std::min(D.E, n_envs - w * D.E);
     // reference constructor defaults
     const State& S = H->wave[w].S;
@@ -1198,6 +1221,9 @@ int ss_destroy(ss_handle* H) {
   if (H->d_init) cudaFree(H->d_init);
   if (H->plan_mem) cudaFree(H->plan_mem);
   if (H->plan.dbg) cudaFree(H->plan.dbg);
+  if (H->lane_stream[1]) cudaStreamDestroy(H->lane_stream[1]);
+  if (H->ev_fork) cudaEventDestroy(H->ev_fork);
+  if (H->ev_join) cudaEventDestroy(H->ev_join);
   if (H->stream) cudaStreamDestroy(H->stream);
   delete H;
   return SS_OK;
@@ -1312,12 +1338,23 @@ static int step_impl(ss_handle* H, const double* cmd, int on_device, int latency
     if (rc) return rc;
   }
   for (int f = 0; f < n_frames; ++f) {
-    // every env of the frame, wave after wave (envs are independent)
+    // every env of the frame, wave after wave (envs are independent); with two
+    // lanes the odd waves run on the second stream, joined once per frame (the
+    // command buffer is rewritten by the next frame)
     if (has_cmd == 1)
       CK(cudaMemcpyAsync(H->d_cmd, cmd + (size_t)f * D.n_real * D.links,
                          8 * (size_t)D.n_real * D.links,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, H->stream));
-    for (int w = 0; w < H->n_waves; ++w) CK(cudaGraphLaunch(H->wave_graphs[w][key], H->stream));
+    if (H->n_lanes > 1) {
+      CK(cudaEventRecord(H->ev_fork, H->stream));
+      CK(cudaStreamWaitEvent(H->lane_stream[1], H->ev_fork, 0));
+    }
+    for (int w = 0; w < H->n_waves; ++w)
+      CK(cudaGraphLaunch(H->wave_graphs[w][key], H->lane_stream[w % H->n_lanes]));
+    if (H->n_lanes > 1) {
+      CK(cudaEventRecord(H->ev_join, H->lane_stream[1]));
+      CK(cudaStreamWaitEvent(H->stream, H->ev_join, 0));
+    }
   }
   return SS_OK;
 }

@@ -208,3 +208,36 @@ def test_waves_match_oracle_per_env(oracle_mod):
         one = M.BatchedSimulator(1, config=cfg, **parts)
         one.set_state_arrays({k: v[e] for k, v in got.items()})
         assert np.allclose(one.center_of_mass()[0], com[e], rtol=1e-14, atol=1e-15), f"env {e}"
+
+
+@pytest.mark.gpu
+def test_two_lanes_match_one_lane():
+    """From 64 envs the waves alternate between two workspaces / streams
+    (concurrent lanes). Every env equals its single-lane run up to the
+    reduction tree (which depends on the lane width)."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    n = 96
+    rng = np.random.default_rng(5)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for lanes in ("1", "2"):
+        os.environ["SS_LANES"] = lanes
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_LANES", None)
+        assert sim.solver_info["waves"] == (1 if lanes == "1" else 2)
+        for c in cmds:
+            sim.step(c, latency=True)
+        out[lanes] = sim.get_state_arrays()
+    # three frames apart in the reduction order only (STEP_TOL-scale bounds)
+    for k, tol in (("positions", 1e-9), ("velocities", 1e-7), ("lam_tetra", 1e-7),
+                   ("pressures", 0.0)):
+        a, b = out["1"][k], out["2"][k]
+        scale = max(float(np.max(np.abs(a))), 1e-30)
+        assert np.max(np.abs(a - b)) <= tol * scale, k
