@@ -85,8 +85,9 @@ struct ss_handle {
   // concurrent lanes: waves alternate between n_lanes workspaces / streams so
   // two waves' kernels overlap (SS_LANES=2)
   int n_lanes = 1;
-  cudaStream_t lane_stream[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  static constexpr int kMaxLanes = 4;
+  cudaStream_t lane_stream[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
   int keep = 0;  // keep_matrix: snapshot the last Newton rhs each frame
   char* d_init = nullptr;  // reset template: one env's state, packed per field
   ClPlan plan{};
@@ -701,9 +702,9 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   int wave_req = p->wave_envs > 0 ? std::min(p->wave_envs, n_envs) : std::min(kAutoWave, n_envs);
   // two concurrent lanes by default from 64 envs (1024 envs: 5,913 -> 6,127 snake-steps/s:
   // one wave's kernel tails overlap the other's; 2 sequential waves of 512: 5,756)
-  const int lanes_req = (int)std::max(1L, std::min(2L, env_long("SS_LANES", 2)));
-  if (lanes_req > 1 && p->wave_envs <= 0 && n_envs >= 64)
-    wave_req = std::min(wave_req, ((n_envs + 1) / 2 + 31) / 32 * 32);
+  const int lanes_req = (int)std::max(1L, std::min(4L, env_long("SS_LANES", 2)));
+  if (lanes_req > 1 && p->wave_envs <= 0 && n_envs >= 32 * lanes_req)
+    wave_req = std::min(wave_req, ((n_envs + lanes_req - 1) / lanes_req + 31) / 32 * 32);
   auto pad_lanes = [](int n) {
     int E = 1;
     if (n <= 32) {
@@ -1148,7 +1149,8 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   H->n_waves = (n_envs + D.E - 1) / D.E;
   const size_t sblock = sa.cap;
   {
-    H->n_lanes = (lanes_req > 1 && H->n_waves > 1 && !H->use_cluster) ? 2 : 1;
+    H->n_lanes = (lanes_req > 1 && H->n_waves > 1 && !H->use_cluster)
+                     ? std::min(lanes_req, H->n_waves) : 1;
     cudaError_t e1 = cudaMalloc(&H->state_mem, sblock * H->n_waves);
     cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap * H->n_lanes) : e1;
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
@@ -1158,7 +1160,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
                   sblock, H->n_waves, wa.cap, n_envs);
     }
   }
-  Work lane_work[2];
+  Work lane_work[ss_handle::kMaxLanes];
   for (int l = 0; l < H->n_lanes; ++l) {
     Arena wl;
     wl.base = (char*)H->work_mem + wa.cap * l;
@@ -1170,9 +1172,11 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   CK(cudaMemsetAsync(H->work_mem, 0, wa.cap * H->n_lanes, H->stream));
   H->lane_stream[0] = H->stream;
   if (H->n_lanes > 1) {
-    CK(cudaStreamCreateWithFlags(&H->lane_stream[1], cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming));
+    for (int l = 1; l < H->n_lanes; ++l) {
+      CK(cudaStreamCreateWithFlags(&H->lane_stream[l], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&H->ev_join[l], cudaEventDisableTiming));
+    }
   }
   H->wave.assign(H->n_waves, H->c);
   H->wave_graphs.assign(H->n_waves, std::vector<cudaGraphExec_t>(6, nullptr));
@@ -1221,9 +1225,11 @@ int ss_destroy(ss_handle* H) {
   if (H->d_init) cudaFree(H->d_init);
   if (H->plan_mem) cudaFree(H->plan_mem);
   if (H->plan.dbg) cudaFree(H->plan.dbg);
-  if (H->lane_stream[1]) cudaStreamDestroy(H->lane_stream[1]);
+  for (int l = 1; l < ss_handle::kMaxLanes; ++l) {
+    if (H->lane_stream[l]) cudaStreamDestroy(H->lane_stream[l]);
+    if (H->ev_join[l]) cudaEventDestroy(H->ev_join[l]);
+  }
   if (H->ev_fork) cudaEventDestroy(H->ev_fork);
-  if (H->ev_join) cudaEventDestroy(H->ev_join);
   if (H->stream) cudaStreamDestroy(H->stream);
   delete H;
   return SS_OK;
@@ -1347,13 +1353,13 @@ static int step_impl(ss_handle* H, const double* cmd, int on_device, int latency
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, H->stream));
     if (H->n_lanes > 1) {
       CK(cudaEventRecord(H->ev_fork, H->stream));
-      CK(cudaStreamWaitEvent(H->lane_stream[1], H->ev_fork, 0));
+      for (int l = 1; l < H->n_lanes; ++l) CK(cudaStreamWaitEvent(H->lane_stream[l], H->ev_fork, 0));
     }
     for (int w = 0; w < H->n_waves; ++w)
       CK(cudaGraphLaunch(H->wave_graphs[w][key], H->lane_stream[w % H->n_lanes]));
-    if (H->n_lanes > 1) {
-      CK(cudaEventRecord(H->ev_join, H->lane_stream[1]));
-      CK(cudaStreamWaitEvent(H->stream, H->ev_join, 0));
+    for (int l = 1; l < H->n_lanes; ++l) {
+      CK(cudaEventRecord(H->ev_join[l], H->lane_stream[l]));
+      CK(cudaStreamWaitEvent(H->stream, H->ev_join[l], 0));
     }
   }
   return SS_OK;
