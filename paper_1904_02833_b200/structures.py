@@ -12,7 +12,7 @@ the array attributes). Array dtypes and shapes follow the reference
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
