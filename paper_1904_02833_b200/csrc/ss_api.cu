@@ -1121,9 +1121,11 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     const double state_lane = (double)sa.cap / D.E;
     const double budget = 0.88 * (double)free_b;
     // work(E_w) + n_envs * state <= budget
-    const double need = (double)n_envs * state_lane + (double)D.E * (per_lane - state_lane);
+    // lanes_req workspaces of E lanes each (concurrent lanes) + every env's state
+    const double need =
+        (double)n_envs * state_lane + (double)lanes_req * D.E * (per_lane - state_lane);
     if (need > budget && D.E > 32) {
-      const double wl = (budget - n_envs * state_lane) / (per_lane - state_lane);
+      const double wl = (budget - n_envs * state_lane) / (lanes_req * (per_lane - state_lane));
       int ew = (int)(wl / 32) * 32;
       if (ew < 32) {
         ss_destroy(H);
