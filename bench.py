@@ -303,6 +303,9 @@ def main():
     per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean,
                                                    not sim.config.exact_jacobian) * n / waves
     avg_ms = prof[top][0] / prof[top][1]
+    # algorithmic bytes of one frame of every env of this rank (all modelled kernels)
+    step_bytes = sum(roofline.bytes_per_launch_per_env(k, d, nc_mean, not sim.config.exact_jacobian)
+                     * (v[1] / args.profile_frames) * n / waves for k, v in prof.items())
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -343,6 +346,11 @@ def main():
                      "mean_contacts_per_substep": nc_mean,
                      "share_of_step": prof[top][0] / sum(v[0] for v in prof.values()),
                      "traffic": traffic},
+        # whole step: every kernel's algorithmic bytes per frame over the graph-timed
+        # frame (concurrent lanes overlap kernels, so this exceeds per-kernel rates)
+        "step_bandwidth": {"achieved": step_bytes * (K / (ms * 1e-3)) / 1e9, "peak": peak,
+                           "unit": "GB/s", "frac": step_bytes * (K / (ms * 1e-3)) / 1e9 / peak,
+                           "bytes_per_step": step_bytes},
         "kernels_ms_per_frame": {k: round(v[0] / args.profile_frames, 4) for k, v in prof.items()},
         "profiled_ms_per_frame": step_ms_prof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": n * 4 * 8,
