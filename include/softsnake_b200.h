@@ -110,14 +110,15 @@ typedef struct ss_params {
    * chain-rule application of the same operator, ~5x fewer FP64 ops,
    * rounding-level (1e-16) differences. */
   int32_t exact_jacobian;
-  /* Newton-loop solver: 0 auto (= streaming), 1 streaming batched kernels,
-   * 2 cluster-resident: one env per <=16-CTA cluster, PCR state in shared
+  /* Newton-loop solver: 0 auto (cluster-resident up to 32 envs when the
+   * scene fits, else streaming), 1 streaming batched kernels, 2
+   * cluster-resident: one env per <=16-CTA cluster, PCR state in shared
    * memory (error if the scene does not fit). */
   int32_t solver_mode;
-  /* envs per wave (0 = auto: min(n_envs, 4096), lowered further if the
-   * workspace plus all env state would not fit in device memory). Persistent
-   * state is kept for every env; waves share one workspace and run back to
-   * back inside each frame. */
+  /* envs per wave (0 = auto: min(n_envs, 4096), split over two concurrent
+   * lanes from 64 envs, lowered further if the workspaces plus all env state
+   * would not fit in device memory). Persistent state is kept for every env;
+   * waves alternate between the lanes' workspaces and streams. */
   int32_t wave_envs;
   /* SolverConfig.keep_matrix (solver.py:113, 511-518): keep the last
    * substep's Newton system readable through ss_export_system (forces the
@@ -166,7 +167,8 @@ int ss_abi_version(void);
 const char* ss_last_error(void);
 int ss_device_count(int* n);
 
-/* Upload topology, allocate state for n_envs copies on `device`. The
+/* Simulator.__init__ (solver.py:157-265) for n_envs independent copies:
+ * upload topology, allocate state for n_envs copies on `device`. The
  * initial state of every env is zero except quaternions (identity), dirs
  * (1,0,0), scale 1, strains 1 — the reference constructor defaults
  * (constraints.py:80-82,156-158; solver.py:247-255). Call ss_set_state. */
@@ -175,6 +177,11 @@ int ss_create(const ss_topology* topo, const ss_params* params, int n_envs,
 int ss_destroy(ss_handle* h);
 int ss_num_envs(const ss_handle* h);
 
+/* Write / read the persistent state of envs [env0, env0+n) — what the
+ * reference keeps in sim.state, the lam_* arrays, tetras.quats,
+ * distances.dirs/scale, the strain trackers, channels.pressures and _warm
+ * (state.py:59-109, solver.py:247-255, constraints.py:69-70,146,
+ * pneumatics.py:92). Host pointers, env-major; NULL fields are skipped. */
 int ss_set_state(ss_handle* h, int env0, int n, const ss_state_view* s);
 int ss_get_state(ss_handle* h, int env0, int n, ss_state_view* s);
 /* Same with DEVICE pointers in the view (same env-major [n][...] layouts,
