@@ -612,6 +612,13 @@ DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, i
     o2 *= s;
     const double wn = sqrt(o0 * o0 + o1 * o1 + o2 * o2);
     if (wn < tol) break;
+    if (wn != wn) {
+      // non-finite element (a diverged env): the reference keeps iterating to
+      // maxiter and ends with a NaN quaternion; end there at once
+      qw = qx = qy = qz = __longlong_as_double(0x7ff8000000000000ll);
+      it = maxiter;
+      break;
+    }
     const double half = 0.5 * wn;
     double sh, cw;
     sincos(half, &sh, &cw);  // one shared argument reduction
