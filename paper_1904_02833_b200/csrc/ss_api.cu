@@ -82,6 +82,9 @@ struct ss_handle {
   // cluster-resident Newton solver (0 = streaming kernels)
   int use_cluster = 0;
   GridCaps caps;
+  // item lanes per DOF in the J^T gather (1: serial walk in reference order;
+  // 2/4/8: split walk for few env lanes, structured mode only; SS_GATHER_SPLIT)
+  int gather_split = 1;
   // concurrent lanes: waves alternate between n_lanes workspaces / streams so
   // two waves' kernels overlap (SS_LANES=2)
   int n_lanes = 1;
@@ -125,7 +128,7 @@ GridCaps grid_caps(int device) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_apply_rows<false>, SS_THREADS, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir<false>, SS_THREADS, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, k_gather, SS_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, k_gather<1>, SS_THREADS, 0);
   g.stream = env_long("SS_STREAM_BLOCKS", 32L * sms);
   g.eval = env_long("SS_EVAL_BLOCKS", 8L * sms);
   g.reduce = env_long("SS_REDUCE_BLOCKS", (long)sms * std::max(1, std::min(occ_a, occ_d)));
@@ -184,7 +187,14 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 g_eval = grid_items(D, D.nt, H->caps.eval);
   const dim3 g_tet = grid_items(D, D.nt, H->caps.stream);
   const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, H->caps.eval);
-  const dim3 g_gather = grid_items(D, D.P + D.nb, H->caps.gather);
+  int gsp = EX ? 1 : H->gather_split;  // the split walk changes the summation order
+  if (gsp == 0) {
+    const long lanes = H->caps.gather * (long)SS_THREADS;
+    gsp = 4;
+    while (gsp > 1 && (long)(D.P + D.nb) * gsp * D.E > lanes) gsp >>= 1;
+  }
+  while (gsp > 1 && gsp * D.W > 32) gsp >>= 1;  // a DOF's lanes stay in one warp
+  const dim3 g_gather = grid_items(D, (long)(D.P + D.nb) * gsp, H->caps.gather);
   const dim3 g_el = grid_items(D, n_el, H->caps.stream);
   const dim3 g_red(D.tiles, H->gy_red);
   const dim3 g_int = grid_items(D, D.P + D.nb, H->caps.eval);
@@ -194,6 +204,13 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const double* xc_z = c.K.z + (size_t)D.ms * D.E;
   const double* xs_dl = c.K.az;
   const double* xc_dl = c.K.az + (size_t)D.ms * D.E;
+#define GATHER(mode, xs, xc)                                        \
+  do {                                                              \
+    if (gsp == 8) LAUNCH(k_gather<8>, g_gather, c, mode, xs, xc);    \
+    else if (gsp == 4) LAUNCH(k_gather<4>, g_gather, c, mode, xs, xc); \
+    else if (gsp == 2) LAUNCH(k_gather<2>, g_gather, c, mode, xs, xc); \
+    else LAUNCH(k_gather<1>, g_gather, c, mode, xs, xc);             \
+  } while (0)
   // has_cmd: 0 no commands, 1 commands in d_cmd, 2 on-device gait generator
   const int gait = has_cmd == 2 ? 1 : 0;
   LAUNCH(k_frame_begin, g_links, c, d_cmd, has_cmd == 1 ? 1 : 0, latency, gait);
@@ -231,26 +248,26 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       LAUNCH(k_integrate, g_int, c);
       continue;
     }
-    LAUNCH(k_gather, g_gather, c, 1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
+    GATHER(1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
     for (int it = 0; it < c.p.newton; ++it) {
       LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
       if (H->keep && sub == c.p.substeps - 1 && it == c.p.newton - 1)
         CK(cudaMemcpyAsync(c.K.snap_rhs, c.K.r, 8 * (size_t)D.m * D.E, cudaMemcpyDeviceToDevice,
                            st));  // the snapshot's rhs (solver.py:515)
       if (c.p.pcr > 0) {
-        LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
+        GATHER(0, xs_z, xc_z);
         LAUNCH(k_apply_rows<EX>, g_red, c, 1);
         LAUNCH(k_pcr_dir<EX>, g_red, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
           LAUNCH(k_pcr_step<EX>, g_el, c);
           if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
-          LAUNCH(k_gather, g_gather, c, 0, xs_z, xc_z);
+          GATHER(0, xs_z, xc_z);
           LAUNCH(k_apply_rows<EX>, g_red, c, 0);
           LAUNCH(k_pcr_dir<EX>, g_red, c, 0);
         }
       }
       LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0);
-      LAUNCH(k_gather, g_gather, c, 1, xs_dl, xc_dl);  // v += M^-1 J^T dlam
+      GATHER(1, xs_dl, xc_dl);  // v += M^-1 J^T dlam
     }
     LAUNCH(k_integrate, g_int, c);
   }
@@ -919,6 +936,15 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // ---- allocations
   ss_handle* H = new ss_handle();
   H->caps = caps;
+  {
+    // 0 = auto: the widest split up to 4 whose lanes still fit one resident
+    // wave (coupled 2/10-snake scenes at E = 1: 7.8 -> 5.6 / 9.1 -> 7.1 ms per
+    // frame at split 4, 5.3 / 6.9 at 8 — but 8 moved one ill-conditioned
+    // parity case (test_gpu_params fb_slopes) past the 1e-10 per-step bound;
+    // the 1M-tet snake fills the GPU already and stays at 1)
+    const long gs = env_long("SS_GATHER_SPLIT", 0);
+    H->gather_split = gs >= 8 ? 8 : gs >= 4 ? 4 : gs >= 2 ? 2 : gs == 1 ? 1 : 0;
+  }
   H->device = device;
   H->c.D = D;
   H->c.p = P;

@@ -1066,14 +1066,199 @@ __global__ void k_eval_misc(const Ctx c) {
 // present contacts, friction rows regardless of the active set.
 // xs: static rows [ms][E]; xc: contact rows [3 ns][E]; tets read their
 // column sums from tC (written by the producing element kernel).
+// One incidence (code = (fam<<29)|(v<<25)|e) of a particle's / a body's
+// J^T list: its contribution to the DOF's w (block_transpose,
+// numba_backend.py:43-52, per row); false when the row is inactive.
+DI bool inc_particle(const Ctx& c, int code, int mode, const double* __restrict__ xs,
+                     const double* __restrict__ xc, int env, double& a0, double& a1,
+                     double& a2) {
+  const int E = c.D.E, nt = c.D.nt, na = c.D.na, ns = c.D.ns;
+  (void)nt;
+  const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+  if (fam == F_TET) {
+    a0 = c.K.tC[TCX(3 * v, e)];
+    a1 = c.K.tC[TCX(3 * v + 1, e)];
+    a2 = c.K.tC[TCX(3 * v + 2, e)];
+  } else if (fam == F_DIST) {
+    const int nd = c.D.nd;
+    const double xr = xs[IX(c.D.od + e)];
+    double d0 = c.S.dirs[IX(e)], d1 = c.S.dirs[IX(nd + e)], d2 = c.S.dirs[IX(2 * nd + e)];
+    if (v) { d0 = -d0; d1 = -d1; d2 = -d2; }
+    a0 = 0.0 + d0 * xr;
+    a1 = 0.0 + d1 * xr;
+    a2 = 0.0 + d2 * xr;
+  } else if (fam == F_ATTP) {
+    double x3[3];
+    const double rw[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) x3[i] = xs[IX(c.D.oa + i * na + e)];
+    double acc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      acc[a] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) acc[a] += att_val(i, a, rw) * x3[i];
+    }
+    a0 = acc[0]; a1 = acc[1]; a2 = acc[2];
+  } else {  // F_CN / F_CF on a particle slot: n = (0,0,1), t1 = (1,0,0), t2 = (0,1,0)
+    const bool on = mode == 0 ? (fam == F_CN ? c.K.present[IX(e)] != 0 : c.K.actf[IX(e)] != 0.0)
+                              : c.K.present[IX(e)] != 0;
+    if (!on) return false;
+    if (fam == F_CN) {
+      const double xn = xc[IX(e)];
+      a0 = 0.0 + 0.0 * xn;
+      a1 = 0.0 + 0.0 * xn;
+      a2 = 0.0 + 1.0 * xn;
+    } else {
+      const double xf0 = xc[IX(ns + e)], xf1 = xc[IX(2 * ns + e)];
+      a0 = 0.0 + 1.0 * xf0;
+      a0 += 0.0 * xf1;
+      a1 = 0.0 + 0.0 * xf0;
+      a1 += 1.0 * xf1;
+      a2 = 0.0 + 0.0 * xf0;
+      a2 += 0.0 * xf1;
+    }
+  }
+  return true;
+}
+DI bool inc_body(const Ctx& c, int code, int mode, const double* __restrict__ xs,
+                 const double* __restrict__ xc, int env, double* acc) {
+  const int E = c.D.E, na = c.D.na, nh = c.D.nh, nw = c.D.nw, ns = c.D.ns;
+  const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+  if (fam == F_ATTB) {
+    double x3[3], rw[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      x3[i] = xs[IX(c.D.oa + i * na + e)];
+      rw[i] = c.K.rw[IX(i * na + e)];
+    }
+#pragma unroll
+    for (int kk = 0; kk < 6; ++kk) {
+      acc[kk] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) acc[kk] += att_val(i, 3 + kk, rw) * x3[i];
+    }
+  } else if (fam == F_HINGE) {
+    double x5[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) x5[i] = xs[IX(c.D.oh + i * nh + e)];
+#pragma unroll
+    for (int kk = 0; kk < 6; ++kk) {
+      acc[kk] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+        acc[kk] += c.K.hJ[IX((size_t)(12 * i + 6 * v + kk) * nh + e)] * x5[i];
+    }
+  } else {  // wheel slot e (< nw)
+    const bool on = mode == 0 ? (fam == F_CN ? c.K.present[IX(e)] != 0 : c.K.actf[IX(e)] != 0.0)
+                              : c.K.present[IX(e)] != 0;
+    if (!on) return false;
+    if (fam == F_CN) {
+      const double xn = xc[IX(e)];
+#pragma unroll
+      for (int kk = 0; kk < 6; ++kk) acc[kk] = 0.0 + c.K.wJ[IX((size_t)kk * nw + e)] * xn;
+    } else {
+      const double xf0 = xc[IX(ns + e)], xf1 = xc[IX(2 * ns + e)];
+#pragma unroll
+      for (int kk = 0; kk < 6; ++kk) {
+        acc[kk] = 0.0 + c.K.wJ[IX((size_t)(6 + kk) * nw + e)] * xf0;
+        acc[kk] += c.K.wJ[IX((size_t)(12 + kk) * nw + e)] * xf1;
+      }
+    }
+  }
+  return true;
+}
+
 #ifndef SS_GATHER_MINB
 #define SS_GATHER_MINB 4
 #endif
+// minv_apply (numba_backend.py:68-82) of one body's w, stored (mode 0) or
+// added to v (mode 1)
+DI void gather_body_out(const Ctx& c, int b, int mode, const double* w, int env) {
+  const int E = c.D.E;
+  const double im = c.T.body_inv_mass[b];
+  double u[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) u[a] = im * w[a];
+  const int nb = c.D.nb;
+  double A[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) A[k] = c.K.ang_inv[IX((size_t)k * nb + b)];
+  u[3] = A[0] * w[3] + A[1] * w[4] + A[2] * w[5];
+  u[4] = A[3] * w[3] + A[4] * w[4] + A[5] * w[5];
+  u[5] = A[6] * w[3] + A[7] * w[4] + A[8] * w[5];
+  const int o = c.D.bd0 + 6 * b;
+  if (mode == 0) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) c.K.u[IX(o + k)] = u[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) c.K.v[IX(o + k)] += u[k];
+  }
+}
+
+// SPLIT > 1 (structured mode, few env lanes): SPLIT adjacent item lanes
+// share one DOF and walk every SPLIT-th incidence of its list, then combine
+// with a fixed shuffle tree — the serial incidence walk of a lone env is
+// latency-bound (one CTA column per 256 DOFs), this gives it SPLIT× the
+// loads in flight. Not the reference's summation order (exact mode keeps
+// SPLIT = 1).
+template <int SPLIT>
 __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx c, int mode,
                                                        const double* __restrict__ xs,
                                                        const double* __restrict__ xc) {
   SETUP
   const int P = c.D.P, nt = c.D.nt, na = c.D.na, nh = c.D.nh, nw = c.D.nw, ns = c.D.ns;
+  if constexpr (SPLIT > 1) {
+    (void)nt; (void)na; (void)nh; (void)nw; (void)ns;
+    const int sub = il % SPLIT, ilg = il / SPLIT, ILg = IL / SPLIT;
+    const int n_it = P + c.D.nb;
+    // block-uniform trip count: every lane reaches the shuffles
+    for (int it0 = blockIdx.y * ILg; it0 < n_it; it0 += gridDim.y * ILg) {
+      const int it = it0 + ilg;
+      double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (it < n_it) {
+        const int k0 = c.T.inc_ptr[it], k1 = c.T.inc_ptr[it + 1];
+        if (it < P) {
+          for (int k = k0 + sub; k < k1; k += SPLIT) {
+            double a0, a1, a2;
+            if (!inc_particle(c, c.T.inc[k], mode, xs, xc, env, a0, a1, a2)) continue;
+            w[0] += a0;
+            w[1] += a1;
+            w[2] += a2;
+          }
+        } else {
+          for (int k = k0 + sub; k < k1; k += SPLIT) {
+            double acc[6];
+            if (!inc_body(c, c.T.inc[k], mode, xs, xc, env, acc)) continue;
+#pragma unroll
+            for (int kk = 0; kk < 6; ++kk) w[kk] += acc[kk];
+          }
+        }
+      }
+#pragma unroll
+      for (int off = SPLIT >> 1; off > 0; off >>= 1) {
+#pragma unroll
+        for (int kk = 0; kk < 6; ++kk) w[kk] += __shfl_xor_sync(0xffffffffu, w[kk], off * c.D.W);
+      }
+      if (it >= n_it || sub != 0) continue;
+      if (it < P) {
+        const double im = c.T.inv_mass[it];
+        const double u0 = im * w[0], u1 = im * w[1], u2 = im * w[2];
+        if (mode == 0) {
+          c.K.u[IX(3 * it)] = u0;
+          c.K.u[IX(3 * it + 1)] = u1;
+          c.K.u[IX(3 * it + 2)] = u2;
+        } else {
+          c.K.v[IX(3 * it)] += u0;
+          c.K.v[IX(3 * it + 1)] += u1;
+          c.K.v[IX(3 * it + 2)] += u2;
+        }
+      } else {
+        gather_body_out(c, it - P, mode, w, env);
+      }
+    }
+  } else {
   FOR_ITEMS(it, P + c.D.nb) {
     const int k0 = c.T.inc_ptr[it], k1 = c.T.inc_ptr[it + 1];
     if (it < P) {
@@ -1115,52 +1300,8 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
           if (k >= k1) break;
         }
         const int code = c.T.inc[k];
-        const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
         double a0, a1, a2;
-        if (fam == F_TET) {
-          a0 = c.K.tC[TCX(3 * v, e)];
-          a1 = c.K.tC[TCX(3 * v + 1, e)];
-          a2 = c.K.tC[TCX(3 * v + 2, e)];
-        } else if (fam == F_DIST) {
-          const int nd = c.D.nd;
-          const double xr = xs[IX(c.D.od + e)];
-          double d0 = c.S.dirs[IX(e)], d1 = c.S.dirs[IX(nd + e)], d2 = c.S.dirs[IX(2 * nd + e)];
-          if (v) { d0 = -d0; d1 = -d1; d2 = -d2; }
-          a0 = 0.0 + d0 * xr;
-          a1 = 0.0 + d1 * xr;
-          a2 = 0.0 + d2 * xr;
-        } else if (fam == F_ATTP) {
-          double x3[3];
-          const double rw[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-          for (int i = 0; i < 3; ++i) x3[i] = xs[IX(c.D.oa + i * na + e)];
-          double acc[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            acc[a] = 0.0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) acc[a] += att_val(i, a, rw) * x3[i];
-          }
-          a0 = acc[0]; a1 = acc[1]; a2 = acc[2];
-        } else {  // F_CN / F_CF on a particle slot: n = (0,0,1), t1 = (1,0,0), t2 = (0,1,0)
-          const bool on = mode == 0 ? (fam == F_CN ? c.K.present[IX(e)] != 0 : c.K.actf[IX(e)] != 0.0)
-                                    : c.K.present[IX(e)] != 0;
-          if (!on) continue;
-          if (fam == F_CN) {
-            const double xn = xc[IX(e)];
-            a0 = 0.0 + 0.0 * xn;
-            a1 = 0.0 + 0.0 * xn;
-            a2 = 0.0 + 1.0 * xn;
-          } else {
-            const double xf0 = xc[IX(ns + e)], xf1 = xc[IX(2 * ns + e)];
-            a0 = 0.0 + 1.0 * xf0;
-            a0 += 0.0 * xf1;
-            a1 = 0.0 + 0.0 * xf0;
-            a1 += 1.0 * xf1;
-            a2 = 0.0 + 0.0 * xf0;
-            a2 += 0.0 * xf1;
-          }
-        }
+        if (!inc_particle(c, code, mode, xs, xc, env, a0, a1, a2)) continue;
         w0 += a0;
         w1 += a1;
         w2 += a2;
@@ -1181,73 +1322,14 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
       double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       for (int k = k0; k < k1; ++k) {
         const int code = c.T.inc[k];
-        const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
         double acc[6];
-        if (fam == F_ATTB) {
-          double x3[3], rw[3];
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            x3[i] = xs[IX(c.D.oa + i * na + e)];
-            rw[i] = c.K.rw[IX(i * na + e)];
-          }
-#pragma unroll
-          for (int kk = 0; kk < 6; ++kk) {
-            acc[kk] = 0.0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) acc[kk] += att_val(i, 3 + kk, rw) * x3[i];
-          }
-        } else if (fam == F_HINGE) {
-          double x5[5];
-#pragma unroll
-          for (int i = 0; i < 5; ++i) x5[i] = xs[IX(c.D.oh + i * nh + e)];
-#pragma unroll
-          for (int kk = 0; kk < 6; ++kk) {
-            acc[kk] = 0.0;
-#pragma unroll
-            for (int i = 0; i < 5; ++i)
-              acc[kk] += c.K.hJ[IX((size_t)(12 * i + 6 * v + kk) * nh + e)] * x5[i];
-          }
-        } else {  // wheel slot e (< nw)
-          const bool on = mode == 0 ? (fam == F_CN ? c.K.present[IX(e)] != 0 : c.K.actf[IX(e)] != 0.0)
-                                    : c.K.present[IX(e)] != 0;
-          if (!on) continue;
-          if (fam == F_CN) {
-            const double xn = xc[IX(e)];
-#pragma unroll
-            for (int kk = 0; kk < 6; ++kk) acc[kk] = 0.0 + c.K.wJ[IX((size_t)kk * nw + e)] * xn;
-          } else {
-            const double xf0 = xc[IX(ns + e)], xf1 = xc[IX(2 * ns + e)];
-#pragma unroll
-            for (int kk = 0; kk < 6; ++kk) {
-              acc[kk] = 0.0 + c.K.wJ[IX((size_t)(6 + kk) * nw + e)] * xf0;
-              acc[kk] += c.K.wJ[IX((size_t)(12 + kk) * nw + e)] * xf1;
-            }
-          }
-        }
+        if (!inc_body(c, code, mode, xs, xc, env, acc)) continue;
 #pragma unroll
         for (int kk = 0; kk < 6; ++kk) w[kk] += acc[kk];
       }
-      // minv_apply (numba_backend.py:68-82)
-      const double im = c.T.body_inv_mass[b];
-      double u[6];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) u[a] = im * w[a];
-      const int nb = c.D.nb;
-      double A[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) A[k] = c.K.ang_inv[IX((size_t)k * nb + b)];
-      u[3] = A[0] * w[3] + A[1] * w[4] + A[2] * w[5];
-      u[4] = A[3] * w[3] + A[4] * w[4] + A[5] * w[5];
-      u[5] = A[6] * w[3] + A[7] * w[4] + A[8] * w[5];
-      const int o = c.D.bd0 + 6 * b;
-      if (mode == 0) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) c.K.u[IX(o + k)] = u[k];
-      } else {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) c.K.v[IX(o + k)] += u[k];
-      }
+      gather_body_out(c, b, mode, w, env);
     }
+  }
   }
 }
 

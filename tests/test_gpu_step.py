@@ -241,3 +241,29 @@ def test_two_lanes_match_one_lane():
         a, b = out["1"][k], out["2"][k]
         scale = max(float(np.max(np.abs(a))), 1e-30)
         assert np.max(np.abs(a - b)) <= tol * scale, k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split", ["4", "8"])
+def test_split_gather_matches_serial_walk(split):
+    """A lone env's J^T gather splits each DOF's incidence walk over 2-8
+    lanes (structured mode; SS_GATHER_SPLIT, auto up to 4 by default). Same frames
+    as the serial walk in reference order up to the summation order."""
+    import os
+    out = {}
+    for s in ("1", split):
+        os.environ["SS_GATHER_SPLIT"] = s
+        try:
+            m = M.build_snake(M.SceneConfig(), n_snakes=2)
+            m.sim.config.solver = "streaming"
+            m.sim._ensure()
+        finally:
+            os.environ.pop("SS_GATHER_SPLIT", None)
+        for i in range(3):
+            m.sim.step(m.commands(i * m.sim.config.dt), latency=True)
+        out[s] = m.sim.get_state_arrays(0, 1)
+    for k, tol in (("positions", 1e-9), ("velocities", 1e-7), ("lam_tetra", 1e-7),
+                   ("pressures", 0.0)):
+        a, b = out["1"][k], out[split][k]
+        scale = max(float(np.max(np.abs(a))), 1e-30)
+        assert np.max(np.abs(a - b)) <= tol * scale, k
