@@ -1592,6 +1592,10 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY_MINB) k_apply_rows(const 
   const double* u = c.K.u;
   const double* z = c.K.z;
   double part = 0.0;
+  // structured mode: the next tet item's node ids are fetched one item ahead,
+  // so its gathered u loads issue with the quaternion / S / z loads instead of
+  // after a dependent index load
+  int pf_t = -1, pf_n0 = 0, pf_n1 = 0, pf_n2 = 0, pf_n3 = 0;
   FOR_ITEMS(it, nd + nt + na + nh + ns) {
     if (it < nd) {
       const int row = c.D.od + it;
@@ -1613,14 +1617,32 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY_MINB) k_apply_rows(const 
         // every load of the tet issued before any arithmetic (one memory
         // round trip per item instead of three)
         double q[4], sv[6], uv[12];
+        int nid[4];
+        if (pf_t == t) {
+          nid[0] = pf_n0; nid[1] = pf_n1; nid[2] = pf_n2; nid[3] = pf_n3;
+        } else {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + t];
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) uv[3 * v + a] = u[IX(3 * nid[v] + a)];
 #pragma unroll
         for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
 #pragma unroll
         for (int k = 0; k < 6; ++k) sv[k] = c.K.tS[IX(k * nt + t)];
-        tet_node_vals(c, t, env, u, uv);
 #pragma unroll
         for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
         tet_rinv(c, t, Ri);
+        const int tn = t + gridDim.y * IL;
+        if (tn < nt) {
+          pf_t = tn;
+          pf_n0 = c.T.t_idx[tn];
+          pf_n1 = c.T.t_idx[nt + tn];
+          pf_n2 = c.T.t_idx[2 * nt + tn];
+          pf_n3 = c.T.t_idx[3 * nt + tn];
+        }
         tet_unpack(q, sv, T);
         tet_forward_uv(T, Ri, uv, y);
       }
