@@ -300,11 +300,12 @@ def main():
     nc_mean = float(np.mean([st.contact_count for st in sim.get_stats()])) / sim.config.substeps
     # one launch covers one wave: envs per launch = n / waves on average
     waves = sim.solver_info["waves"]
-    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean,
-                                                   not sim.config.exact_jacobian) * n / waves
+    structured = not sim.config.exact_jacobian
+    pcr = sim.config.pcr_iters
+    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean, structured, pcr) * n / waves
     avg_ms = prof[top][0] / prof[top][1]
     # algorithmic bytes of one frame of every env of this rank (all modelled kernels)
-    step_bytes = sum(roofline.bytes_per_launch_per_env(k, d, nc_mean, not sim.config.exact_jacobian)
+    step_bytes = sum(roofline.bytes_per_launch_per_env(k, d, nc_mean, structured, pcr)
                      * (v[1] / args.profile_frames) * n / waves for k, v in prof.items())
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
     traffic = None

@@ -60,6 +60,7 @@ struct GridCaps {
   long eval = 148 * 8;     // per-substep eval / integrate kernels
   long reduce = 148 * 2;   // per-env reduction kernels: one resident wave
   long gather = 148 * 8;   // per-DOF gather: one resident wave
+  long dir = 148 * 2;      // k_pcr_dir: its own resident wave (lighter than apply)
 };
 struct ss_handle {
   int device = 0;
@@ -70,7 +71,8 @@ struct ss_handle {
   int n_waves = 1;
   std::vector<Ctx> wave;   // per-wave contexts (State pointers, real lanes)
   std::vector<std::vector<cudaGraphExec_t>> wave_graphs;  // [wave][key]
-  int gy_red = 1;
+  int gy_red = 1;   // apply / final grid rows (partials per env)
+  int gy_dir = 1;   // k_pcr_dir grid rows
   void* topo_mem = nullptr;
   void* state_mem = nullptr;
   void* work_mem = nullptr;
@@ -131,8 +133,9 @@ GridCaps grid_caps(int device) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, k_gather<1>, SS_THREADS, 0);
   g.stream = env_long("SS_STREAM_BLOCKS", 32L * sms);
   g.eval = env_long("SS_EVAL_BLOCKS", 8L * sms);
-  g.reduce = env_long("SS_REDUCE_BLOCKS", (long)sms * std::max(1, std::min(occ_a, occ_d)));
+  g.reduce = env_long("SS_REDUCE_BLOCKS", (long)sms * std::max(1, occ_a));
   g.gather = env_long("SS_GATHER_BLOCKS", (long)sms * std::max(1, occ_g));
+  g.dir = env_long("SS_DIR_BLOCKS", (long)sms * std::max(1, occ_d));
   return g;
 }
 
@@ -197,6 +200,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 g_gather = grid_items(D, (long)(D.P + D.nb) * gsp, H->caps.gather);
   const dim3 g_el = grid_items(D, n_el, H->caps.stream);
   const dim3 g_red(D.tiles, H->gy_red);
+  const dim3 g_dir(D.tiles, H->gy_dir);
   const dim3 g_int = grid_items(D, D.P + D.nb, H->caps.eval);
   const double* xs_lam = c.S.lam;
   const double* xc_lam = c.K.lamc;
@@ -257,16 +261,17 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       if (c.p.pcr > 0) {
         GATHER(0, xs_z, xc_z);
         LAUNCH(k_apply_rows<EX>, g_red, c, 1);
-        LAUNCH(k_pcr_dir<EX>, g_red, c, 1);
+        LAUNCH(k_pcr_dir<EX>, g_dir, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
-          LAUNCH(k_pcr_step<EX>, g_el, c);
+          LAUNCH(k_pcr_step<EX>, g_el, c, k == 0 ? 1 : 0);
           if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
           GATHER(0, xs_z, xc_z);
           LAUNCH(k_apply_rows<EX>, g_red, c, 0);
-          LAUNCH(k_pcr_dir<EX>, g_red, c, 0);
+          LAUNCH(k_pcr_dir<EX>, g_dir, c, 0);
         }
       }
-      LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0);
+      LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
+             c.p.pcr == 1 ? 1 : 0);
       GATHER(1, xs_dl, xc_dl);  // v += M^-1 J^T dlam
     }
     LAUNCH(k_integrate, g_int, c);
@@ -1070,6 +1075,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   {
     const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
     H->gy_red = (int)grid_items(D, n_el, H->caps.reduce).y;
+    H->gy_dir = (int)grid_items(D, n_el, H->caps.dir).y;
   }
 
   // state + work (lane count read at call time: the wave cap may shrink it)
@@ -1101,7 +1107,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   };
   auto plan_work = [&](Arena& A) {
     const size_t Es = H->c.D.E;
-    const int gy_max = H->gy_red;
+    const int gy_max = std::max(H->gy_red, H->gy_dir);
     Work& K = H->c.K;
     K.v = A.take<double>((size_t)D.ndof * Es);
     K.u = A.take<double>((size_t)D.ndof * Es);
@@ -1165,6 +1171,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
       D.tiles = D.E / D.W;
       H->c.D = D;
       H->gy_red = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, H->caps.reduce).y;
+      H->gy_dir = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, H->caps.dir).y;
       sa = Arena();
       wa = Arena();
       plan_state(sa);

@@ -1748,11 +1748,11 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
     for (int q = 0; q < 6; ++q) {
       if (q < nr) {
         const size_t o = IX(rows[q]);
-        zr[q] = Z[o];
+        if (EXACT) zr[q] = Z[o];
         azr[q] = AZ[o];
         dr[q] = Dg[o];
         if (!setup) {
-          pr[q] = P_[o];
+          if (EXACT) pr[q] = P_[o];
           apr[q] = AP[o];
         }
       }
@@ -1763,10 +1763,10 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
         const size_t o = IX(rows[q]);
         double ap;
         if (setup) {
-          P_[o] = zr[q];
+          if (EXACT) P_[o] = zr[q];
           ap = azr[q];
         } else if (!brk) {
-          P_[o] = zr[q] + beta * pr[q];
+          if (EXACT) P_[o] = zr[q] + beta * pr[q];
           ap = azr[q] + beta * (EXACT ? apr[q] : apr[q] * dr[q]);
         } else {
           ap = EXACT ? apr[q] : apr[q] * dr[q];
@@ -1792,16 +1792,21 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
 // carries the same recurrence one rounding apart per row, and the pass moves
 // 6 row vectors (x p z apd in, x z out) instead of 8; k_newton_final takes
 // r = d z for the residual.
+// Structured mode also forms the search direction here, p = z + beta p
+// (p = z on the first iteration; solver.py:90-91), from the z it already
+// reads, instead of in k_pcr_dir: the same value bitwise, two row vectors
+// fewer per iteration (k_pcr_dir no longer reads z, p or writes p).
 template <bool EXACT>
-__global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
+__global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c, int first) {
   SETUP
   if (c.K.broken[env]) return;  // the reference skips the whole iteration
   const double alpha = c.K.alpha[env];
+  const double beta = c.K.beta[env];
   const int n_el = c.D.nd + c.D.nt + c.D.na + c.D.nh + c.D.ns;
   double* __restrict__ X_ = c.K.x;
   double* __restrict__ R_ = c.K.r;
   double* __restrict__ Z_ = c.K.z;
-  const double* __restrict__ P_ = c.K.p;
+  double* __restrict__ P_ = c.K.p;
   const double* __restrict__ AP = c.K.ap;
   const double* __restrict__ Dg = c.K.d;
   FOR_ITEMS(it, n_el) {
@@ -1813,7 +1818,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
       if (q < nr) {
         const size_t o = IX(rows[q]);
         xr[q] = X_[o];
-        pr[q] = P_[o];
+        if (EXACT || !first) pr[q] = P_[o];
         rr[q] = EXACT ? R_[o] : Z_[o];
         apr[q] = AP[o];
         if (EXACT) dr[q] = Dg[o];
@@ -1823,6 +1828,10 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c) {
     for (int q = 0; q < 6; ++q) {
       if (q < nr) {
         const size_t o = IX(rows[q]);
+        if (!EXACT) {
+          pr[q] = first ? rr[q] : rr[q] + beta * pr[q];  // rr holds z here
+          P_[o] = pr[q];
+        }
         X_[o] = xr[q] + alpha * pr[q];
         if (EXACT) {
           const double r = rr[q] - alpha * apr[q];
@@ -1865,10 +1874,12 @@ template <bool EXACT>
 #define SS_FINAL_MINB 2
 #endif
 #define SS_FINAL_MINB_LB __launch_bounds__(SS_THREADS, SS_FINAL_MINB)
-__global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int last) {
+__global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int last,
+                                                 int first) {
   SETUP
   const bool step = do_step && !c.K.broken[env];
   const double alpha = c.K.alpha[env];
+  const double beta = c.K.beta[env];
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns, nw = c.D.nw;
   const int n_el = nd + nt + na + nh + ns;
   double part = 0.0;
@@ -1885,7 +1896,12 @@ __global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int la
         if (EXACT) rr[q] = c.K.r[o];
         if (step || !EXACT) dr[q] = c.K.d[o];
         if (step) {
-          pr[q] = c.K.p[o];
+          if (EXACT) {
+            pr[q] = c.K.p[o];
+          } else {
+            // the search direction as k_pcr_step forms it
+            pr[q] = first ? zr[q] : zr[q] + beta * c.K.p[o];
+          }
           apr[q] = c.K.ap[o];
         }
       }

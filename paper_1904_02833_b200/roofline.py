@@ -26,21 +26,32 @@ def dims_of(sim) -> dict:
                 ndof=3 * P + 6 * nb)
 
 
-def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool = True) -> float:
-    """structured: the default tet-J mode, whose k_pcr_step keeps r = d z
-    implicit and reads ap/d from k_pcr_dir (6 row vectors instead of 8)."""
+def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool = True,
+                             pcr: int = 20) -> float:
+    """structured: the default tet-J mode. Its k_pcr_step keeps r = d z
+    implicit, reads ap/d from k_pcr_dir and forms p = z + beta p itself, so
+    k_pcr_dir moves 4 row vectors (3 on the setup launch) instead of 7 and
+    k_pcr_step 7 (6 on the first launch of a solve) instead of 8. pcr: the
+    PCR budget, for the per-launch average over one solve (pcr k_pcr_dir
+    launches, pcr - 1 k_pcr_step launches)."""
     rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches
     jc = F8 * 10 * d["nt"]                       # compact tet J: quat(4) S(6); R, K^-1 rebuilt
     tc = F8 * 12 * d["nt"]                       # tet column sums J^T x
     small_j = F8 * (3 * d["nd"] + 3 * d["na"] + 60 * d["nh"] + 18 * d["nw"])
     flags = 4 * d["ns"] + F8 * 2 * nc            # present flags, actf/dynn of present
     if kernel == "k_pcr_step":
-        # read x p r|z ap|apd [d], write x [r] z (rows)
-        return F8 * (6 if structured else 8) * rows + flags
+        if structured:
+            # read x p z apd, write x z p (the first launch of a solve reads no p)
+            return F8 * (7 - 1.0 / max(pcr - 1, 1)) * rows + flags
+        # read x p r ap d, write x r z
+        return F8 * 8 * rows + flags
     if kernel == "k_tet_jt":
         # z of the tet rows, compact J; write tC
         return F8 * 6 * d["nt"] + jc + tc
     if kernel == "k_pcr_dir":
+        if structured:
+            # read az apd d, write apd (the setup launch reads no apd)
+            return F8 * (4 - 1.0 / max(pcr, 1)) * rows + flags
         # read z az p ap d, write p ap
         return F8 * 7 * rows + flags
     if kernel == "k_apply_rows":
