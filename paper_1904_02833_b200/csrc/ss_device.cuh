@@ -1886,41 +1886,31 @@ __global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int la
   FOR_ITEMS(it, n_el) {
     int rows[6];
     const int nr = item_rows(c, it, env, rows);
-    double dl[6], xr[6], rr[6], zr[6], pr[6], apr[6], dr[6];
+    // one pass per row: only dl survives into the multiplier update (the
+    // two-pass load-all-then-compute form spilled the loaded rows at 128
+    // registers, and each spill store waited on its load)
+    double dl[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       if (q < nr) {
         const size_t o = IX(rows[q]);
-        xr[q] = c.K.x[o];
-        zr[q] = c.K.z[o];
-        if (EXACT) rr[q] = c.K.r[o];
-        if (step || !EXACT) dr[q] = c.K.d[o];
+        double x = c.K.x[o], z = c.K.z[o];
+        double r = EXACT ? c.K.r[o] : 0.0;
+        const double dq = (step || !EXACT) ? c.K.d[o] : 1.0;
         if (step) {
+          double pq;
+          if (EXACT) pq = c.K.p[o];
+          else pq = first ? z : z + beta * c.K.p[o];  // the direction as k_pcr_step forms it
+          const double apq = c.K.ap[o];
+          x += alpha * pq;
           if (EXACT) {
-            pr[q] = c.K.p[o];
+            r -= alpha * apq;
+            z = r / dq;
           } else {
-            // the search direction as k_pcr_step forms it
-            pr[q] = first ? zr[q] : zr[q] + beta * c.K.p[o];
-          }
-          apr[q] = c.K.ap[o];
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      if (q < nr) {
-        double x = xr[q], z = zr[q];
-        double r = EXACT ? rr[q] : 0.0;
-        if (step) {
-          x += alpha * pr[q];
-          if (EXACT) {
-            r -= alpha * apr[q];
-            z = r / dr[q];
-          } else {
-            z -= alpha * apr[q];  // the ap buffer holds ap/d (k_pcr_dir)
+            z -= alpha * apq;  // the ap buffer holds ap/d (k_pcr_dir)
           }
         }
-        if (!EXACT) r = dr[q] * z;  // structured mode keeps r = d z implicit
+        if (!EXACT) r = dq * z;  // structured mode keeps r = d z implicit
         part += r * z;
         dl[q] = x;
       }
