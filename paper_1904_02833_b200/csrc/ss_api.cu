@@ -263,7 +263,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
         LAUNCH(k_apply_rows<EX>, g_red, c, 1);
         LAUNCH(k_pcr_dir<EX>, g_dir, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
-          LAUNCH(k_pcr_step<EX>, g_el, c, k == 0 ? 1 : 0);
+          LAUNCH(k_pcr_step<EX>, g_el, c, k);
           if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
           GATHER(0, xs_z, xc_z);
           LAUNCH(k_apply_rows<EX>, g_red, c, 0);
@@ -1136,6 +1136,8 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.rho = A.take<double>(Es);
     K.alpha = A.take<double>(Es);
     K.beta = A.take<double>(Es);
+    K.alpha_prev = A.take<double>(Es);
+    K.last_step = A.take<int>(Es);
     K.broken = A.take<int>(Es);
     K.snap_rhs = p->keep_matrix ? A.take<double>((size_t)D.m * Es) : nullptr;
   };

@@ -97,6 +97,8 @@ struct Work {
   double* part;             // [gy_red][E]
   int* cnt;                 // [tiles]
   double *rho, *alpha, *beta;  // [E]
+  double* alpha_prev;           // [E] alpha of the previous PCR iteration (deferred x update)
+  int* last_step;               // [E] index of the last executed k_pcr_step (-1: none)
   int* broken;                  // [E]
   double* snap_rhs;             // [m] rhs of the last Newton pass (keep_matrix only)
 };
@@ -1492,6 +1494,7 @@ __global__ void SS_RHS_MINB_LB k_newton_rhs(const Ctx c) {
     if (it == 0) {
       c.K.broken[env] = 0;
       c.K.beta[env] = 0.0;
+      c.K.last_step[env] = -1;
     }
     if (it < nd) {
       const int row = c.D.od + it;
@@ -1780,8 +1783,12 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
   double den;
   if (reduce_env(c, part, &den)) {
     if (!c.K.broken[env]) {
-      if (den <= 1e-300 || !isfinite(den)) c.K.broken[env] = 1;
-      else c.K.alpha[env] = c.K.rho[env] / den;
+      if (den <= 1e-300 || !isfinite(den)) {
+        c.K.broken[env] = 1;
+      } else {
+        c.K.alpha_prev[env] = c.K.alpha[env];
+        c.K.alpha[env] = c.K.rho[env] / den;
+      }
     }
   }
 }
@@ -1797,11 +1804,20 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) 
 // reads, instead of in k_pcr_dir: the same value bitwise, two row vectors
 // fewer per iteration (k_pcr_dir no longer reads z, p or writes p).
 template <bool EXACT>
-__global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c, int first) {
+__global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c, int k) {
   SETUP
   if (c.K.broken[env]) return;  // the reference skips the whole iteration
+  const bool first = k == 0;
+  // structured mode defers x: an even iteration leaves x alone, the next
+  // (odd) one applies both, x = (x + alpha_prev p_old) + alpha p_new — the
+  // reference's two updates in the reference's order (bitwise the same x),
+  // with one x read/write per two iterations; k_newton_final applies a
+  // pending even update (last_step)
+  const bool upd_x = EXACT || (k & 1);
   const double alpha = c.K.alpha[env];
   const double beta = c.K.beta[env];
+  const double alpha_prev = EXACT ? 0.0 : c.K.alpha_prev[env];
+  if (!EXACT && blockIdx.y == 0 && il == 0) c.K.last_step[env] = k;
   const int n_el = c.D.nd + c.D.nt + c.D.na + c.D.nh + c.D.ns;
   double* __restrict__ X_ = c.K.x;
   double* __restrict__ R_ = c.K.r;
@@ -1817,7 +1833,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c, int first)
     for (int q = 0; q < 6; ++q) {
       if (q < nr) {
         const size_t o = IX(rows[q]);
-        xr[q] = X_[o];
+        if (upd_x) xr[q] = X_[o];
         if (EXACT || !first) pr[q] = P_[o];
         rr[q] = EXACT ? R_[o] : Z_[o];
         apr[q] = AP[o];
@@ -1828,16 +1844,15 @@ __global__ void __launch_bounds__(SS_THREADS) k_pcr_step(const Ctx c, int first)
     for (int q = 0; q < 6; ++q) {
       if (q < nr) {
         const size_t o = IX(rows[q]);
-        if (!EXACT) {
-          pr[q] = first ? rr[q] : rr[q] + beta * pr[q];  // rr holds z here
-          P_[o] = pr[q];
-        }
-        X_[o] = xr[q] + alpha * pr[q];
         if (EXACT) {
+          X_[o] = xr[q] + alpha * pr[q];
           const double r = rr[q] - alpha * apr[q];
           R_[o] = r;
           Z_[o] = r / dr[q];
         } else {
+          const double pn = first ? rr[q] : rr[q] + beta * pr[q];  // rr holds z here
+          P_[o] = pn;
+          if (upd_x) X_[o] = (xr[q] + alpha_prev * pr[q]) + alpha * pn;
           Z_[o] = rr[q] - alpha * apr[q];
         }
       }
@@ -1880,6 +1895,11 @@ __global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int la
   const bool step = do_step && !c.K.broken[env];
   const double alpha = c.K.alpha[env];
   const double beta = c.K.beta[env];
+  // a deferred x update of the last executed (even) k_pcr_step: its alpha is
+  // alpha_prev after a further k_pcr_dir, alpha after a breakdown
+  const int ls = EXACT ? -1 : c.K.last_step[env];
+  const bool pend = ls >= 0 && !(ls & 1);
+  const double alpha_pend = pend ? (step ? c.K.alpha_prev[env] : alpha) : 0.0;
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns, nw = c.D.nw;
   const int n_el = nd + nt + na + nh + ns;
   double part = 0.0;
@@ -1897,10 +1917,12 @@ __global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int la
         double x = c.K.x[o], z = c.K.z[o];
         double r = EXACT ? c.K.r[o] : 0.0;
         const double dq = (step || !EXACT) ? c.K.d[o] : 1.0;
+        const double po = (!EXACT && (pend || (step && !first))) ? c.K.p[o] : 0.0;
+        if (pend) x += alpha_pend * po;
         if (step) {
           double pq;
           if (EXACT) pq = c.K.p[o];
-          else pq = first ? z : z + beta * c.K.p[o];  // the direction as k_pcr_step forms it
+          else pq = first ? z : z + beta * po;  // the direction as k_pcr_step forms it
           const double apq = c.K.ap[o];
           x += alpha * pq;
           if (EXACT) {

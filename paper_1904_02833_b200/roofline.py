@@ -30,8 +30,9 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
                              pcr: int = 20) -> float:
     """structured: the default tet-J mode. Its k_pcr_step keeps r = d z
     implicit, reads ap/d from k_pcr_dir and forms p = z + beta p itself, so
-    k_pcr_dir moves 4 row vectors (3 on the setup launch) instead of 7 and
-    k_pcr_step 7 (6 on the first launch of a solve) instead of 8. pcr: the
+    k_pcr_dir moves 4 row vectors (3 on the setup launch) instead of 7, and
+    k_pcr_step 7 on odd launches, 5 on even ones (x deferred to the next
+    launch; 4 on the first launch of a solve) instead of 8. pcr: the
     PCR budget, for the per-launch average over one solve (pcr k_pcr_dir
     launches, pcr - 1 k_pcr_step launches)."""
     rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches
@@ -41,8 +42,11 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
     flags = 4 * d["ns"] + F8 * 2 * nc            # present flags, actf/dynn of present
     if kernel == "k_pcr_step":
         if structured:
-            # read x p z apd, write x z p (the first launch of a solve reads no p)
-            return F8 * (7 - 1.0 / max(pcr - 1, 1)) * rows + flags
+            # odd launches: read x p z apd, write x z p; even launches defer x
+            # (read p z apd, write z p); the first launch of a solve reads no p
+            n = max(pcr - 1, 1)
+            even, odd = (n + 1) // 2, n // 2
+            return F8 * ((5 * even + 7 * odd - 1) / n) * rows + flags
         # read x p r ap d, write x r z
         return F8 * 8 * rows + flags
     if kernel == "k_tet_jt":

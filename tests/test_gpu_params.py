@@ -21,7 +21,9 @@ VARIANTS = {
     "substeps1": dict(substeps=1),
     "substeps3_newton2": dict(substeps=3, newton_iters=2),
     "pcr7": dict(pcr_iters=7),
+    "pcr4": dict(pcr_iters=4),  # last PCR step even: a deferred x update for the final pass
     "pcr3": dict(pcr_iters=3),
+    "pcr2": dict(pcr_iters=2),
     "mu0.4_margin0.01": dict(mu=0.4, contact_margin=0.01),
     "fb_slopes": dict(fb_slope_min=1e-3, fb_slope_max=1.5, fb_delta=1e-8),
     "damping0.25": dict(constraint_damping=0.25),  # unstable past one frame: frame 1 only
@@ -67,13 +69,15 @@ def test_config_variant_vs_oracle(oracle_mod, name, solver):
                                       ref.contact_count, ref.inverted_tets)
 
 
+@pytest.mark.parametrize("pcr", [20, 5, 6])
 @pytest.mark.parametrize("solver", ["streaming", "cluster"])
-def test_breakdown_guard_at_rest(oracle_mod, solver):
+def test_breakdown_guard_at_rest(oracle_mod, solver, pcr):
     """Bend fixture at rest, 0 psi, no gravity: the right-hand side is at
     rounding level, so the PCR denominators underflow toward the breakdown
     guard (solver.py:75-78). Same result as the oracle, and the fixture
     stays at rest."""
     parts, cfg = scene_parts("B")
+    cfg = dataclasses.replace(cfg, pcr_iters=pcr)
     cfg.solver = solver
     sim = M.Simulator(config=cfg, **parts)
     o = oracle_mod.OracleSim(config=cfg, **parts)
