@@ -1732,7 +1732,9 @@ DI bool row_live(const Ctx& c, int row, int env) {
 // Structured mode (!EXACT) stores apd = ap/d in the ap buffer instead of ap
 // (ap_prev = apd_prev * d when needed): the step then needs neither ap nor d.
 template <bool EXACT>
-__global__ void __launch_bounds__(SS_THREADS) k_pcr_dir(const Ctx c, int setup) {
+// structured mode pinned to 3 CTAs/SM (<= 85 registers; at 85 registers and 2
+// CTAs/SM the kernel takes 33.5 instead of 28.9 ms/frame)
+__global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : 3) k_pcr_dir(const Ctx c, int setup) {
   SETUP
   const bool brk = c.K.broken[env] != 0;
   const double beta = c.K.beta[env];
