@@ -1806,7 +1806,10 @@ __global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : 3) k_pcr_dir(const Ctx
 // reads, instead of in k_pcr_dir: the same value bitwise, two row vectors
 // fewer per iteration (k_pcr_dir no longer reads z, p or writes p).
 template <bool EXACT>
-__global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : 3) k_pcr_step(const Ctx c, int k) {
+#ifndef SS_STEP_MINB
+#define SS_STEP_MINB 3
+#endif
+__global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : SS_STEP_MINB) k_pcr_step(const Ctx c, int k) {
   SETUP
   if (c.K.broken[env]) return;  // the reference skips the whole iteration
   const bool first = k == 0;
@@ -1864,7 +1867,10 @@ __global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : 3) k_pcr_step(const Ct
 
 // tet column sums of J^T z for the next apply (after k_pcr_step)
 template <bool EXACT>
-__global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : 3) k_tet_jt(const Ctx c) {
+#ifndef SS_TETJT_MINB
+#define SS_TETJT_MINB 3
+#endif
+__global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : SS_TETJT_MINB) k_tet_jt(const Ctx c) {
   SETUP
   if (c.K.broken[env]) return;  // z unchanged: tC from the previous pass is still valid
   const int nt = c.D.nt;
