@@ -164,6 +164,9 @@ typedef struct ss_env_stats {
 typedef struct ss_handle ss_handle;
 
 int ss_abi_version(void);
+/* sha256 (hex) of the CUDA sources and this header the library was built
+ * from; __graft_entry__.build() rebuilds when it differs from the tree. */
+const char* ss_build_id(void);
 const char* ss_last_error(void);
 int ss_device_count(int* n);
 
@@ -206,6 +209,14 @@ int ss_step_device(ss_handle* h, const double* d_commands, int latency, int n_fr
  * computed inside the frame graph (no host commands), f += 1 per frame. */
 int ss_set_gait(ss_handle* h, int env0, int n, const double* params, const int* frame0);
 int ss_step_gait(ss_handle* h, int latency, int n_frames);
+/* Simulator.set_channel_targets (solver.py:274-277): one pneumatic tick of
+ * every env toward commands[n_envs][links] psi (ChannelBank.tick,
+ * pneumatics.py:102-116) without stepping; the strain target follows at the
+ * next ss_step (solver.py:299-301). */
+int ss_set_channel_targets(ss_handle* h, const double* commands, int latency);
+/* Read back the gait parameters (same layout as ss_set_gait) and each env's
+ * current gait frame counter (frames stepped since its clock started). */
+int ss_get_gait(ss_handle* h, int env0, int n, double* params, int* frame);
 
 int ss_get_stats(ss_handle* h, int env0, int n, ss_env_stats* out);
 

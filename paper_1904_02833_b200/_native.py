@@ -22,6 +22,7 @@ _vp, _dp, _ip, _i = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c
 SIGNATURES = {
     "ss_abi_version": (C.c_int, []),
     "ss_last_error": (C.c_char_p, []),
+    "ss_build_id": (C.c_char_p, []),
     "ss_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "ss_create": (C.c_int, [C.POINTER(SsTopology), C.POINTER(SsParams), _i, _i, C.POINTER(_vp)]),
     "ss_destroy": (C.c_int, [_vp]),
@@ -40,6 +41,8 @@ SIGNATURES = {
     "ss_observe": (C.c_int, [_vp, _i, _i, _dp]),
     "ss_set_gait": (C.c_int, [_vp, _i, _i, _dp, C.POINTER(C.c_int)]),
     "ss_step_gait": (C.c_int, [_vp, _i, _i]),
+    "ss_set_channel_targets": (C.c_int, [_vp, _dp, _i]),
+    "ss_get_gait": (C.c_int, [_vp, _i, _i, _dp, C.POINTER(C.c_int)]),
     "ss_synchronize": (C.c_int, [_vp]),
     "ss_stream": (_vp, [_vp]),
     "ss_launches_per_frame": (C.c_int, [_vp]),
@@ -63,6 +66,53 @@ SIGNATURES = {
 }
 
 
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+# nvcc flags of the library build (part of the build id)
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+              "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              "-diag-suppress", "177"]
+ROOT_DIR = os.path.dirname(PKG_DIR)
+
+
+def source_files() -> list[str]:
+    """The files the library is compiled from (the build id covers them)."""
+    csrc = os.path.join(PKG_DIR, "csrc")
+    if not os.path.isdir(csrc):
+        return []
+    return [os.path.join(csrc, f) for f in sorted(os.listdir(csrc))
+            if f.endswith((".cu", ".cuh", ".h"))] + \
+        [os.path.join(ROOT_DIR, "include", "softsnake_b200.h")]
+
+
+def source_hash(extra: str | None = None) -> str | None:
+    """sha256 over the source files' names and bytes (None without sources)."""
+    import hashlib
+    files = source_files()
+    if not files or not all(os.path.exists(f) for f in files):
+        return None
+    h = hashlib.sha256()
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update((" ".join(NVCC_FLAGS) if extra is None else extra).encode())
+    return h.hexdigest()
+
+
+def embedded_build_id(path: str = LIB_PATH) -> str | None:
+    """The build id stored in a library file, read without loading it."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        return None
+    k = data.find(b"ss-build-id:")
+    if k < 0:
+        return None
+    end = data.find(b"\0", k)
+    return data[k + 12:end].decode(errors="replace")
+
+
 def lib():
     """The loaded library; raises RuntimeError if it was not built."""
     global _lib
@@ -76,6 +126,11 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        want = source_hash()
+        got = L.ss_build_id().decode()
+        if want is not None and got != want and not os.environ.get("SS_LIB_OVERRIDE"):
+            raise RuntimeError(f"{LIB_PATH} was built from other sources (build id {got[:12]}, "
+                               f"tree {want[:12]}): rerun __graft_entry__.build()")
         _lib = L
     return _lib
 

@@ -5,6 +5,8 @@
 // per-frame launch sequence captured once into a CUDA graph, state I/O.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
@@ -90,6 +92,7 @@ struct ss_handle {
   // concurrent lanes: waves alternate between n_lanes workspaces / streams so
   // two waves' kernels overlap (SS_LANES=2)
   int n_lanes = 1;
+  int n_work = 1;  // workspace blocks: n_lanes, or one per wave with keep_matrix
   static constexpr int kMaxLanes = 4;
   cudaStream_t lane_stream[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {nullptr, nullptr, nullptr, nullptr};
@@ -695,6 +698,13 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
 extern "C" {
 
 int ss_abi_version(void) { return SS_ABI_VERSION; }
+#ifndef SS_BUILD_ID
+#define SS_BUILD_ID "unversioned"
+#endif
+// sha256 of the sources this library was compiled from (__graft_entry__.
+// source_hash); the marker makes it findable in the file without loading it
+extern "C" __attribute__((used)) const char ss_build_id_marker[] = "ss-build-id:" SS_BUILD_ID;
+const char* ss_build_id(void) { return ss_build_id_marker + 12; }
 const char* ss_last_error(void) { return g_err.c_str(); }
 
 int ss_device_count(int* n) {
@@ -1188,25 +1198,30 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   {
     H->n_lanes = (lanes_req > 1 && H->n_waves > 1 && !H->use_cluster)
                      ? std::min(lanes_req, H->n_waves) : 1;
+    // keep_matrix: the system snapshot (rhs, Jacobian blocks, M^-1) lives in
+    // the workspace, so every wave gets its own workspace block — a wave
+    // sharing a lane's block would overwrite an earlier wave's snapshot
+    H->n_work = H->keep ? H->n_waves : H->n_lanes;
     cudaError_t e1 = cudaMalloc(&H->state_mem, sblock * H->n_waves);
-    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap * H->n_lanes) : e1;
+    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&H->work_mem, wa.cap * H->n_work) : e1;
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
       cudaGetLastError();
       ss_destroy(H);
-      return fail(SS_ENOMEM, "cudaMalloc state/work (%zu x %d + %zu bytes) for %d envs failed",
-                  sblock, H->n_waves, wa.cap, n_envs);
+      return fail(SS_ENOMEM, "cudaMalloc state/work (%zu x %d + %zu x %d bytes) for %d envs failed%s",
+                  sblock, H->n_waves, wa.cap, H->n_work, n_envs,
+                  H->keep ? " (keep_matrix needs one workspace per wave)" : "");
     }
   }
-  Work lane_work[ss_handle::kMaxLanes];
-  for (int l = 0; l < H->n_lanes; ++l) {
+  std::vector<Work> blk_work(H->n_work);
+  for (int l = 0; l < H->n_work; ++l) {
     Arena wl;
     wl.base = (char*)H->work_mem + wa.cap * l;
     plan_work(wl);
-    lane_work[l] = H->c.K;
+    blk_work[l] = H->c.K;
   }
-  H->bytes += sblock * H->n_waves + wa.cap * H->n_lanes;
+  H->bytes += sblock * H->n_waves + wa.cap * H->n_work;
   CK(cudaMemsetAsync(H->state_mem, 0, sblock * H->n_waves, H->stream));
-  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap * H->n_lanes, H->stream));
+  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap * H->n_work, H->stream));
   H->lane_stream[0] = H->stream;
   if (H->n_lanes > 1) {
     CK(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
@@ -1222,7 +1237,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     a.base = (char*)H->state_mem + sblock * w;
     plan_state(a);  // writes H->c.S
     H->wave[w] = H->c;
-    H->wave[w].K = lane_work[w % H->n_lanes];
+    H->wave[w].K = blk_work[H->keep ? w : w % H->n_lanes];
     H->wave[w].D.n_real = std::min(D.E, n_envs - w * D.E);
     // reference constructor defaults
     const State& S = H->wave[w].S;
@@ -1412,6 +1427,25 @@ int ss_step_gait(ss_handle* H, int latency, int n_frames) {
   return step_impl(H, nullptr, 2, latency, n_frames);
 }
 
+int ss_set_channel_targets(ss_handle* H, const double* commands, int latency) {
+  if (!H) return fail(SS_EINVAL, "null handle");
+  const Dims& D = H->c.D;
+  if (D.nch == 0 || D.links == 0) return SS_OK;  // no channels: nothing to tick
+  if (!commands) return fail(SS_EINVAL, "null commands");
+  CK(cudaSetDevice(H->device));
+  CK(cudaMemcpyAsync(H->d_cmd, commands, 8 * (size_t)D.n_real * D.links, cudaMemcpyHostToDevice,
+                     H->stream));
+  for (int w = 0; w < H->n_waves; ++w) {
+    const Ctx& c = H->wave[w];
+    const double* d_cmd = H->d_cmd + (size_t)w * D.E * D.links;
+    k_tick<<<grid_items(c.D, D.links, H->caps.eval), SS_THREADS, 0, H->stream>>>(c, d_cmd,
+                                                                                 latency ? 1 : 0);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(H->stream));  // the caller's host buffer may go away
+  return SS_OK;
+}
+
 int ss_set_gait(ss_handle* H, int env0, int n, const double* params, const int* frame0) {
   if (!H || (!params && n > 0)) return fail(SS_EINVAL, "null argument");
   const Dims& D = H->c.D;
@@ -1442,6 +1476,26 @@ int ss_set_gait(ss_handle* H, int env0, int n, const double* params, const int* 
     CK(cudaMemcpyAsync(S.gait_frame + ch.lane0, fr.data(), 4 * (size_t)ch.cnt,
                        cudaMemcpyHostToDevice, H->stream));
     CK(cudaStreamSynchronize(H->stream));  // host staging vectors go out of scope
+  }
+  return SS_OK;
+}
+
+int ss_get_gait(ss_handle* H, int env0, int n, double* params, int* frame) {
+  if (!H || (n > 0 && (!params || !frame))) return fail(SS_EINVAL, "null argument");
+  const Dims& D = H->c.D;
+  if (env0 < 0 || n < 0 || env0 + n > D.n_real) return fail(SS_EINVAL, "env range out of bounds");
+  CK(cudaSetDevice(H->device));
+  CK(cudaStreamSynchronize(H->stream));
+  for (const WaveChunk& ch : wave_chunks(H, env0, n)) {
+    const State& S = H->wave[ch.w].S;
+    std::vector<double> rows(6 * (size_t)ch.cnt);
+    for (int k = 0; k < 6; ++k)
+      CK(cudaMemcpy(rows.data() + (size_t)k * ch.cnt, S.gait + (size_t)k * D.E + ch.lane0,
+                    8 * (size_t)ch.cnt, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 6; ++k)
+      for (int i = 0; i < ch.cnt; ++i) params[6 * (size_t)(ch.off + i) + k] = rows[(size_t)k * ch.cnt + i];
+    CK(cudaMemcpy(frame + ch.off, S.gait_frame + ch.lane0, 4 * (size_t)ch.cnt,
+                  cudaMemcpyDeviceToHost));
   }
   return SS_OK;
 }
@@ -1747,8 +1801,33 @@ int ssk_block_forward(const int32_t* dof_idx, const double* vals, int n, int r, 
 }
 int ssk_block_transpose(const int32_t* dof_idx, const double* vals, int n, int r, int k,
                         const double* x_rows, double* y, int ndof, void* stream) {
-  if (ndof > 0) kk_block_transpose<<<KBLK(ndof)>>>(dof_idx, vals, n, r, k, x_rows, y, ndof);
-  CK(cudaGetLastError());
+  const long nk = (long)n * k;
+  if (ndof <= 0) return SS_OK;
+  if (nk <= 0) return SS_OK;  // y += 0
+  if (nk > 0x7fffffffL) return fail(SS_EINVAL, "block_transpose: n*k exceeds int32");
+  // CSR transpose: stable radix sort of (dof, e*k+j) pairs by dof
+  int *keys_out = nullptr, *vals_in = nullptr, *vals_out = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dof_idx, keys_out, vals_in, vals_out, (int)nk,
+                                  0, 32, KSTREAM);
+  CK(cudaMalloc(&keys_out, 4 * nk));
+  CK(cudaMalloc(&vals_in, 4 * nk));
+  CK(cudaMalloc(&vals_out, 4 * nk));
+  CK(cudaMalloc(&tmp, tmp_bytes));
+  kk_iota<<<256, 256, 0, KSTREAM>>>(vals_in, nk);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dof_idx, keys_out, vals_in,
+                                                  vals_out, (int)nk, 0, 32, KSTREAM);
+  if (e == cudaSuccess) {
+    kk_block_transpose<<<KBLK(ndof)>>>(keys_out, vals_out, nk, vals, r, k, x_rows, y, ndof);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(KSTREAM);
+  cudaFree(keys_out);
+  cudaFree(vals_in);
+  cudaFree(vals_out);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return fail(SS_ECUDA, "block_transpose: %s", cudaGetErrorString(e));
   return SS_OK;
 }
 int ssk_block_rowdiag(const int32_t* dof_idx, const double* vals, int n, int r, int k,

@@ -335,6 +335,29 @@ __global__ void k_frame_begin(const Ctx c, const double* __restrict__ cmd, int h
   }
 }
 
+// Simulator.set_channel_targets (solver.py:274-277): the pneumatic tick
+// alone (ChannelBank.tick, pneumatics.py:102-116), without the strain
+// target update that step() does after it (_update_actuation)
+__global__ void k_tick(const Ctx c, const double* __restrict__ cmd, int latency) {
+  SETUP
+  FOR_ITEMS(i, c.D.links) {
+    const int ce = env < c.D.n_real ? env : 0;
+    const double a = cmd[(size_t)ce * c.D.links + i];
+    double left = 0.0, right = 0.0;
+    if (a > 0.0) right = a;
+    else if (a < 0.0) left = -a;
+    double* pl = &c.S.press[IX(2 * i)];
+    double* pr = &c.S.press[IX(2 * i + 1)];
+    if (latency) {
+      *pl = update_pressure(*pl, left, c.p);
+      *pr = update_pressure(*pr, right, c.p);
+    } else {
+      *pl = left;
+      *pr = right;
+    }
+  }
+}
+
 // =============================================================== substep
 // _slew_actuation (solver.py:284-292), build_mass_inverse (state.py:246-268)
 // and _predict_velocities (solver.py:316-332). Items: P particles, nb

@@ -16,21 +16,38 @@ __global__ void kk_block_forward(const int* idx, const double* vals, int n, int 
   out[g] = acc;
 }
 
-// numba_backend.py:43-52 — scatter-free: one thread per DOF scans the
-// (element, column) pairs in the reference order and accumulates the ones
-// that target it, so the summation order is exactly the serial scatter's.
-__global__ void kk_block_transpose(const int* idx, const double* vals, int n, int r, int k,
-                                   const double* x, double* y, int ndof) {
+// numba_backend.py:43-52 — scatter-free: the (element, column) pairs are
+// stably sorted by target DOF (ssk_block_transpose: CSR transpose, keys =
+// dof_idx, values = e*k + j ascending), so one thread per DOF walks exactly
+// its own entries in the serial scatter's order: bitwise the reference sum
+// at O(n k) work instead of a full scan per DOF.
+__device__ __forceinline__ long kk_lower_bound(const int* a, long n, int key) {
+  long lo = 0, hi = n;
+  while (lo < hi) {
+    const long mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void kk_iota(int* v, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    v[i] = (int)i;
+}
+__global__ void kk_block_transpose(const int* skey, const int* sval, long nk, const double* vals,
+                                   int r, int k, const double* x, double* y, int ndof) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= ndof) return;
+  const long b = kk_lower_bound(skey, nk, d), e_ = kk_lower_bound(skey, nk, d + 1);
   double acc_y = y[d];
-  for (long e = 0; e < n; ++e)
-    for (int j = 0; j < k; ++j) {
-      if (idx[e * k + j] != d) continue;
-      double acc = 0.0;
-      for (int i = 0; i < r; ++i) acc += vals[(e * r + i) * k + j] * x[e * r + i];
-      acc_y += acc;
-    }
+  for (long s = b; s < e_; ++s) {
+    const long ej = sval[s];
+    const long e = ej / k;
+    const int j = (int)(ej % k);
+    double acc = 0.0;
+    for (int i = 0; i < r; ++i) acc += vals[(e * r + i) * k + j] * x[e * r + i];
+    acc_y += acc;
+  }
   y[d] = acc_y;
 }
 

@@ -130,16 +130,24 @@ class BatchedSimulator:
         self._keep_built = bool(self.config.keep_matrix)
         self._snap_ready = False
         init = getattr(self, "_initial_override", None)
-        self.set_state_arrays(init if init is not None else self._initial_state_arrays(),
-                              env0=0, n=self.n_envs)
         if init is None:
-            _native.check(L.ss_capture_init(h, 0))  # the scene's initial state as reset template
+            self._template = self._initial_state_arrays()  # the reset template (env 0)
+            self.set_state_arrays(self._template, env0=0, n=self.n_envs)
+        else:
+            # handle rebuilt (keep_matrix toggle): the template is restored
+            # through env 0, then every env's carried-over state is written
+            self.set_state_arrays(self._template, env0=0, n=1)
+        _native.check(L.ss_capture_init(h, 0))
+        if init is not None:
+            self.set_state_arrays(init, env0=0, n=self.n_envs)
         return h
 
     # ------------------------------------------------------------- episodes
     def capture_initial(self, env: int = 0) -> None:
         """Store env `env`'s current state as the template of reset_envs."""
         _native.check(_native.lib().ss_capture_init(self._ensure(), int(env)))
+        # host copy, so a handle rebuild (keep_matrix toggle) can restore it
+        self._template = {k: v[0] for k, v in self.get_state_arrays(int(env), 1).items()}
 
     def reset_envs(self, env_ids, seed: int = 0, pos_sigma: float = 0.0,
                    vel_sigma: float = 0.0) -> None:
@@ -158,12 +166,41 @@ class BatchedSimulator:
         if self._h is None or bool(self.config.keep_matrix) == self._keep_built:
             return
         st = self.get_state_arrays()
+        gait = self.get_gait()
         self.close()
         self._initial_override = st
         try:
             self._ensure()
         finally:
             self._initial_override = None
+        # the on-device gait generator's parameters and frame counters
+        prm, fr = gait
+        armed = prm[:, 5] >= 1.0  # links_per_snake is 0 where no gait was set
+        i = 0
+        while i < self.n_envs:
+            if not armed[i]:
+                i += 1
+                continue
+            j = i
+            while j < self.n_envs and armed[j]:
+                j += 1
+            p_run = np.ascontiguousarray(prm[i:j])
+            f_run = np.ascontiguousarray(fr[i:j])
+            _native.check(_native.lib().ss_set_gait(
+                self._h, i, j - i, p_run.ctypes.data_as(C.POINTER(C.c_double)),
+                f_run.ctypes.data_as(C.POINTER(C.c_int))))
+            i = j
+
+    def get_gait(self, env0: int = 0, n: int | None = None):
+        """(params [n, 6], frame [n]) of the on-device gait generator
+        (ss_set_gait layout; all-zero params when no gait is armed)."""
+        n = self.n_envs - env0 if n is None else n
+        prm = np.zeros((n, 6))
+        fr = np.zeros(n, np.int32)
+        _native.check(_native.lib().ss_get_gait(
+            self._ensure(), env0, n, prm.ctypes.data_as(C.POINTER(C.c_double)),
+            fr.ctypes.data_as(C.POINTER(C.c_int))))
+        return prm, fr
 
     def close(self):
         if self._h is not None:
@@ -232,11 +269,14 @@ class BatchedSimulator:
         for name, shape_fn, dt in STATE_FIELDS:
             if names is not None and name not in names:
                 continue
-            t = torch.zeros((n,) + shape_fn(d), dtype=torch.int32 if dt == np.int32 else torch.float64,
+            t = torch.empty((n,) + shape_fn(d), dtype=torch.int32 if dt == np.int32 else torch.float64,
                             device=f"cuda:{self.device}")
             out[name] = t
             kind = C.POINTER(C.c_int32) if dt == np.int32 else C.POINTER(C.c_double)
             setattr(v, name, C.cast(C.c_void_p(t.data_ptr()), kind) if t.numel() else C.cast(None, kind))
+        # the handle's stream is not ordered after torch's: finish torch's
+        # pending work on these allocations before the device gather writes them
+        torch.cuda.current_stream(self.device).synchronize()
         _native.check(_native.lib().ss_get_state_device(h, env0, n, C.byref(v)))
         return out
 
@@ -333,6 +373,20 @@ class BatchedSimulator:
         self.frames += n_frames
         self._snap_ready = self._keep_built
 
+    def set_channel_targets(self, commands, latency: bool = True) -> None:
+        """One pneumatic tick of every env toward commands [n_envs, links]
+        psi (ChannelBank.tick via solver.py:274-277), without stepping."""
+        h = self._ensure()
+        if self.channels is None:
+            return
+        cmd = np.ascontiguousarray(np.asarray(commands, np.float64))
+        if cmd.size == self.n_links and self.n_envs > 1:
+            cmd = np.ascontiguousarray(np.broadcast_to(cmd, (self.n_envs, self.n_links)))
+        if cmd.size != self.n_envs * self.n_links:
+            raise ValueError(f"commands must hold {self.n_envs * self.n_links} values, got {cmd.size}")
+        _native.check(_native.lib().ss_set_channel_targets(
+            h, cmd.ctypes.data_as(C.POINTER(C.c_double)), 1 if latency else 0))
+
     def step_device(self, d_commands_ptr: int, latency: bool = True, n_frames: int = 1) -> None:
         self._sync_keep()
         h = self._ensure()
@@ -421,9 +475,10 @@ class Simulator(BatchedSimulator):
 
     # reference surface ------------------------------------------------
     def set_channel_targets(self, commands, latency: bool = True) -> None:
-        """Tick the channels without stepping is not separable on the device;
-        the reference only calls this from step()."""
-        raise NotImplementedError("use step(commands, latency)")
+        """Advance the pneumatic channels one tick toward the commands
+        (solver.py:274-277) on the device, without stepping."""
+        super().set_channel_targets(np.asarray(commands, np.float64).reshape(1, -1), latency)
+        self._refresh_host()
 
     def step(self, commands=None, latency: bool = True) -> StepStats:  # noqa: D401
         t0 = _time.perf_counter()

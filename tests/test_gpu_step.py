@@ -267,3 +267,30 @@ def test_split_gather_matches_serial_walk(split):
         a, b = out["1"][k], out[split][k]
         scale = max(float(np.max(np.abs(a))), 1e-30)
         assert np.max(np.abs(a - b)) <= tol * scale, k
+
+
+def test_set_channel_targets_then_step_none():
+    """Simulator.set_channel_targets (solver.py:274-277) ticks the channels
+    on the device without stepping; step(None) afterwards equals
+    step(commands) (step() = set_channel_targets + the frame)."""
+    from paper_1904_02833_b200.structures import ChannelBank
+    a, _, cfg = _sim("S")
+    b, _, _ = _sim("S")
+    host = ChannelBank.create(4)
+    for i in range(3):
+        cmd = M.gait_commands(M.GaitParams(turn_bias=0.2), i * cfg.dt, 4, 4)
+        a.set_channel_targets(cmd, latency=True)
+        host.tick(cmd, latency=True)
+        assert np.array_equal(a.channels.pressures, host.pressures), i
+        st = a.get_state_arrays(0, 1)
+        assert np.array_equal(st["pressures"][0], host.pressures)
+        a.step(None)
+        b.step(cmd, latency=True)
+    ga, gb = a.get_state_arrays(0, 1), b.get_state_arrays(0, 1)
+    for k in ga:
+        assert np.array_equal(ga[k], gb[k]), k
+    # latency off snaps; a batched handle takes one row per env
+    bs, _, _ = _sim("S", 3)
+    bs.set_channel_targets(np.array([[8.0, -4.0, 0.0, 1.0]] * 3), latency=False)
+    p = bs.get_state_arrays()["pressures"]
+    assert np.array_equal(p[2], [0.0, 8.0, 4.0, 0.0, 0.0, 0.0, 0.0, 1.0])
