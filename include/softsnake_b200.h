@@ -274,7 +274,9 @@ int ss_launches_per_frame(ss_handle* h);
 int64_t ss_device_bytes(ss_handle* h);
 /* info[0] 1 if the cluster-resident solver is used, info[1] CTAs per
  * cluster, info[2] shared bytes per CTA, info[3] env lanes per wave,
- * info[4] number of waves. info must hold 5 ints. */
+ * info[4] number of waves, info[5] 1 if the PCR loop's J^T z gather is
+ * fused (k_gather_fused), info[6] its particle blocks, info[7] its chunks
+ * over all blocks. info must hold 8 ints. */
 int ss_solver_info(ss_handle* h, int* info);
 /* Debug: clock64 phase stamps of one PCR iteration of the cluster solver
  * (handle created with SS_CLUSTER_STAMPS set); out[16]. */

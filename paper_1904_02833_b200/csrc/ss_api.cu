@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/softsnake_b200.h"
@@ -100,6 +101,12 @@ struct ss_handle {
   char* d_init = nullptr;  // reset template: one env's state, packed per field
   ClPlan plan{};
   void* plan_mem = nullptr;
+  // fused J^T z gather of the PCR loop (k_gather_fused; structured mode)
+  int fused = 0;
+  FusedPlan fplan{};
+  void* fplan_mem = nullptr;
+  size_t fused_smem = 0;
+  int fused_chunks = 0;
 };
 
 namespace {
@@ -146,8 +153,8 @@ GridCaps grid_caps(int device) {
 const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
                                     "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_apply_rows",
                                     "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
-                                    "k_tet_jt",      "k_newton_cluster"};
-constexpr int kNumKernels = 14;
+                                    "k_tet_jt",      "k_newton_cluster", "k_gather_fused"};
+constexpr int kNumKernels = 15;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -159,7 +166,8 @@ int kid(const char* name) {
   return -1;
 }
 
-#define LAUNCH(kern, grid, ...)                                          \
+#define LAUNCH(kern, grid, ...) LAUNCH_SM(kern, grid, 0, __VA_ARGS__)
+#define LAUNCH_SM(kern, grid, smem, ...)                                 \
   do {                                                                   \
     cudaEvent_t e0_ = nullptr, e1_ = nullptr;                            \
     if (prof) {                                                          \
@@ -167,7 +175,7 @@ int kid(const char* name) {
       cudaEventCreate(&e1_);                                             \
       cudaEventRecord(e0_, st);                                          \
     }                                                                    \
-    kern<<<grid, blk, 0, st>>>(__VA_ARGS__);                             \
+    kern<<<grid, blk, smem, st>>>(__VA_ARGS__);                          \
     if (prof) {                                                          \
       cudaEventRecord(e1_, st);                                          \
       prof->ev.push_back({kid(#kern), {e0_, e1_}});                      \
@@ -267,8 +275,19 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
         LAUNCH(k_pcr_dir<EX>, g_dir, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
           LAUNCH(k_pcr_step<EX>, g_el, c, k);
-          if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
-          GATHER(0, xs_z, xc_z);
+          if (!EX && H->fused) {
+            const dim3 g_fu(D.E / H->fplan.FW, H->fplan.n_blocks + 1);
+            const size_t sm = H->fused_smem;
+            switch (H->fplan.FW) {
+              case 1: LAUNCH_SM(k_gather_fused<1>, g_fu, sm, c, H->fplan); break;
+              case 2: LAUNCH_SM(k_gather_fused<2>, g_fu, sm, c, H->fplan); break;
+              case 4: LAUNCH_SM(k_gather_fused<4>, g_fu, sm, c, H->fplan); break;
+              default: LAUNCH_SM(k_gather_fused<8>, g_fu, sm, c, H->fplan); break;
+            }
+          } else {
+            if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
+            GATHER(0, xs_z, xc_z);
+          }
           LAUNCH(k_apply_rows<EX>, g_red, c, 0);
           LAUNCH(k_pcr_dir<EX>, g_dir, c, 0);
         }
@@ -284,6 +303,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   return SS_OK;
 }
 #undef LAUNCH
+#undef LAUNCH_SM
 
 int enqueue_frame(ss_handle* H, int w, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
   const Ctx& c = H->wave[w];
@@ -357,6 +377,210 @@ __global__ void k_fill(double* p, size_t n, double val) {
 }
 
 }  // namespace
+
+// ------------------------------------------------------ fused gather plan
+// Particle blocks for k_gather_fused: runs of consecutive particles of one
+// tet-connected component (a snake link), split evenly when a run exceeds
+// the shared-memory budget or when too few CTAs would run. Per block, the
+// elements touching it are packed greedily (ascending id) into chunks of at
+// most FIL elements with no particle of the block twice in a chunk, family
+// by family in the reference's accumulation order (solver.py:354-367).
+static int plan_fused(ss_handle* H, const Dims& D, const int* tets, const std::vector<int>& d_i,
+                      const std::vector<int>& d_j, const std::vector<int>& a_p,
+                      const std::vector<int>& slot_part) {
+  const long mode = env_long("SS_FUSED", -1);  // -1 auto, 0 off, 1 on
+  H->fused = 0;
+  if (mode == 0 || D.nt == 0 || H->c.p.exact_j || H->use_cluster) return SS_OK;
+  const int FW = (int)std::min<long>(env_long("SS_FUSED_W", 8), D.E);
+  if (FW != 1 && FW != 2 && FW != 4 && FW != 8) return fail(SS_EINVAL, "SS_FUSED_W must be 1/2/4/8");
+  if (mode < 0 && D.E < 8) return SS_OK;  // few env lanes: the split gather / cluster plans
+  const int FIL = SS_THREADS / FW;
+  const int tiles_f = D.E / FW;
+  const long smem_cap = env_long("SS_FUSED_SMEM", 72 * 1024);
+  const int nb_cap = (int)(smem_cap / 8 / FW / 3);
+  if (nb_cap < 16) return SS_OK;
+  // components of the tet graph (union-find)
+  std::vector<int> par(D.P);
+  for (int i = 0; i < D.P; ++i) par[i] = i;
+  auto root = [&](int x) {
+    while (par[x] != x) x = par[x] = par[par[x]];
+    return x;
+  };
+  for (int t = 0; t < D.nt; ++t)
+    for (int v = 1; v < 4; ++v) {
+      const int ra = root(tets[4 * (size_t)t]), rb = root(tets[4 * (size_t)t + v]);
+      if (ra != rb) par[std::max(ra, rb)] = std::min(ra, rb);
+    }
+  const int want_blocks = (148 + tiles_f - 1) / tiles_f;
+  const int nb_target = std::max(16, (D.P + want_blocks - 1) / want_blocks);
+  std::vector<int> bp0, bnp;
+  for (int p = 0; p < D.P;) {
+    int q = p + 1;
+    const int r = root(p);
+    while (q < D.P && root(q) == r) ++q;
+    const int len = q - p;
+    const int lim = std::min(nb_cap, std::max(nb_target, std::min(len, nb_cap)));
+    const int parts = (len + lim - 1) / lim;
+    for (int k = 0; k < parts; ++k) {
+      const int x0 = p + (int)((long)len * k / parts), x1 = p + (int)((long)len * (k + 1) / parts);
+      bp0.push_back(x0);
+      bnp.push_back(x1 - x0);
+    }
+    p = q;
+  }
+  const int nbk = (int)bp0.size();
+  int nb_max = 0;
+  for (int x : bnp) nb_max = std::max(nb_max, x);
+  std::vector<int> blk_of(D.P);
+  for (int b = 0; b < nbk; ++b)
+    for (int n = 0; n < bnp[b]; ++n) blk_of[bp0[b] + n] = b;
+  // per block, per family: the elements touching it (ascending) and their particles
+  struct Elem { int e; int nodes[4]; };
+  std::vector<std::vector<Elem>> fam_el[4];  // dist, tet, attach, contact slot
+  for (auto& f : fam_el) f.assign(nbk, {});
+  auto add = [&](int f, int e, std::initializer_list<int> nodes) {
+    Elem el{e, {-1, -1, -1, -1}};
+    int k = 0;
+    for (int n : nodes) el.nodes[k++] = n;
+    int seen[4] = {-1, -1, -1, -1}, ns_ = 0;
+    for (int n : nodes) {
+      const int b = blk_of[n];
+      bool dup = false;
+      for (int j = 0; j < ns_; ++j) dup |= seen[j] == b;
+      if (dup) continue;
+      seen[ns_++] = b;
+      fam_el[f][b].push_back(el);
+    }
+  };
+  for (int e = 0; e < D.nd; ++e) add(0, e, {d_i[e], d_j[e]});
+  for (int e = 0; e < D.nt; ++e)
+    add(1, e, {tets[4 * (size_t)e], tets[4 * (size_t)e + 1], tets[4 * (size_t)e + 2], tets[4 * (size_t)e + 3]});
+  for (int e = 0; e < D.na; ++e) add(2, e, {a_p[e]});
+  // a particle contact slot adds its normal row, then its friction rows
+  // (one element: the reference's CN-before-CF order per particle)
+  for (int s = D.nw; s < D.ns; ++s) add(3, s, {slot_part[s - D.nw]});
+  const int fam_code[4] = {F_DIST, F_TET, F_ATTP, F_CN};
+  std::vector<int> cptr(1, 0), hdr, start, elist;
+  std::vector<int2> enode;
+  int sched_max = 0;
+  std::vector<int> deg(D.P, 0);
+  for (int b = 0; b < nbk; ++b) {
+    const int el_b0 = (int)elist.size();
+    for (int f = 0; f < 4; ++f) {
+      // conflict-free packing into as few, as even chunks as possible: the
+      // elements on the most-shared particles first, each into the smallest
+      // open chunk it does not conflict with (at least max-degree chunks)
+      const auto& els = fam_el[f][b];
+      for (const Elem& el : els)
+        for (int n : el.nodes)
+          if (n >= 0) ++deg[n];
+      int kmin = (int)((els.size() + FIL - 1) / FIL);
+      for (const Elem& el : els)
+        for (int n : el.nodes)
+          if (n >= 0 && blk_of[n] == b) kmin = std::max(kmin, deg[n]);
+      std::vector<int> order(els.size());
+      std::vector<long> key(els.size(), 0);
+      for (size_t i = 0; i < els.size(); ++i) {
+        order[i] = (int)i;
+        for (int n : els[i].nodes)
+          if (n >= 0 && blk_of[n] == b) key[i] += deg[n];
+      }
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key[x] > key[y]; });
+      std::vector<std::vector<int>> chunks(kmin);
+      std::vector<std::vector<char>> used(kmin, std::vector<char>(bnp[b], 0));
+      for (int i : order) {
+        const Elem& el = els[i];
+        int best = -1;
+        for (size_t k = 0; k < chunks.size(); ++k) {
+          if ((int)chunks[k].size() >= FIL) continue;
+          bool ok = true;
+          for (int n : el.nodes)
+            if (n >= 0 && blk_of[n] == b && used[k][n - bp0[b]]) ok = false;
+          if (ok && (best < 0 || chunks[k].size() < chunks[best].size())) best = (int)k;
+        }
+        if (best < 0) {
+          best = (int)chunks.size();
+          chunks.emplace_back();
+          used.emplace_back(bnp[b], 0);
+        }
+        chunks[best].push_back(i);
+        for (int n : el.nodes)
+          if (n >= 0 && blk_of[n] == b) used[best][n - bp0[b]] = 1;
+      }
+      for (const Elem& el : els)
+        for (int n : el.nodes)
+          if (n >= 0) deg[n] = 0;
+      for (auto& ck : chunks) std::sort(ck.begin(), ck.end());
+      for (auto& ck : chunks) {
+        if (ck.empty()) continue;
+        hdr.push_back((fam_code[f] << 24) | (int)ck.size());
+        start.push_back((int)elist.size());
+        for (int i : ck) {
+          // the element's particles in this block, block-local (0xFFFF: outside)
+          const Elem* el = &els[i];
+          const int e = el->e;
+          unsigned q[4];
+          for (int j = 0; j < 4; ++j) {
+            const int n = el->nodes[j];
+            q[j] = (n >= 0 && blk_of[n] == b) ? (unsigned)(n - bp0[b]) : 0xFFFFu;
+          }
+          elist.push_back(e);
+          enode.push_back(make_int2((int)(q[0] | (q[1] << 16)), (int)(q[2] | (q[3] << 16))));
+        }
+      }
+    }
+    cptr.push_back((int)hdr.size());
+    sched_max = std::max(sched_max, 2 * (cptr[b + 1] - cptr[b]) + 3 * ((int)elist.size() - el_b0));
+  }
+  start.push_back((int)elist.size());  // [n_chunks + 1] starts
+  std::vector<int> chk(hdr);
+  chk.insert(chk.end(), start.begin(), start.end());
+  // device copy
+  std::vector<int> enode_i(2 * enode.size());
+  for (size_t i = 0; i < enode.size(); ++i) {
+    enode_i[2 * i] = enode[i].x;
+    enode_i[2 * i + 1] = enode[i].y;
+  }
+  std::vector<int>* arrs[] = {&bp0, &bnp, &cptr, &chk, &elist, &enode_i};
+  size_t bytes = 0;
+  for (auto* x : arrs) bytes += ((4 * std::max<size_t>(x->size(), 1) + 255) / 256) * 256;
+  CK(cudaMalloc(&H->fplan_mem, bytes));
+  const int* dp[6];
+  {
+    char* q = (char*)H->fplan_mem;
+    for (int i = 0; i < 6; ++i) {
+      dp[i] = (const int*)q;
+      if (!arrs[i]->empty())
+        CK(cudaMemcpy(q, arrs[i]->data(), 4 * arrs[i]->size(), cudaMemcpyHostToDevice));
+      q += ((4 * std::max<size_t>(arrs[i]->size(), 1) + 255) / 256) * 256;
+    }
+  }
+  FusedPlan& F = H->fplan;
+  F.n_blocks = nbk;
+  F.FW = FW;
+  F.FIL = FIL;
+  F.nb_max = nb_max;
+  F.blk_p0 = dp[0];
+  F.blk_np = dp[1];
+  F.blk_cptr = dp[2];
+  F.chk = dp[3];
+  F.elist = dp[4];
+  F.enode = reinterpret_cast<const int2*>(dp[5]);
+  F.sched_max = sched_max;
+  H->fused_smem = 8 * (size_t)nb_max * 3 * FW + 4 * (size_t)sched_max;
+  if (H->fused_smem > 200 * 1024) return SS_OK;  // schedule too large for shared memory: unfused
+  H->fused_chunks = (int)hdr.size();
+  cudaError_t e = cudaSuccess;
+  switch (FW) {
+    case 1: e = cudaFuncSetAttribute(k_gather_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->fused_smem); break;
+    case 2: e = cudaFuncSetAttribute(k_gather_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->fused_smem); break;
+    case 4: e = cudaFuncSetAttribute(k_gather_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->fused_smem); break;
+    default: e = cudaFuncSetAttribute(k_gather_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H->fused_smem); break;
+  }
+  if (e != cudaSuccess) return fail(SS_ECUDA, "fused gather smem attribute: %s", cudaGetErrorString(e));
+  H->fused = 1;
+  return SS_OK;
+}
 
 // ------------------------------------------------------ cluster plan
 // Partition of one environment over the C CTAs of a cluster (contiguous tet
@@ -1258,6 +1482,13 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     CK(cudaMalloc(&H->d_cmd, 8 * cmd_n));
     CK(cudaMemsetAsync(H->d_cmd, 0, 8 * cmd_n, H->stream));
   }
+  {
+    int frc = plan_fused(H, H->c.D, t->tets, d_i, d_j, a_p, slot_part);
+    if (frc) {
+      ss_destroy(H);
+      return frc;
+    }
+  }
   CK(cudaStreamSynchronize(H->stream));
   *out = H;
   return SS_OK;
@@ -1276,6 +1507,7 @@ int ss_destroy(ss_handle* H) {
   if (H->d_stage) cudaFree(H->d_stage);
   if (H->d_init) cudaFree(H->d_init);
   if (H->plan_mem) cudaFree(H->plan_mem);
+  if (H->fplan_mem) cudaFree(H->fplan_mem);
   if (H->plan.dbg) cudaFree(H->plan.dbg);
   for (int l = 1; l < ss_handle::kMaxLanes; ++l) {
     if (H->lane_stream[l]) cudaStreamDestroy(H->lane_stream[l]);
@@ -1745,6 +1977,9 @@ int ss_solver_info(ss_handle* H, int* info) {
   info[2] = H->use_cluster ? 8 * H->plan.smem_doubles : 0;
   info[3] = H->c.D.E;
   info[4] = H->n_waves;
+  info[5] = H->fused;
+  info[6] = H->fused ? H->fplan.n_blocks : 0;
+  info[7] = H->fused ? H->fused_chunks : 0;
   return SS_OK;
 }
 

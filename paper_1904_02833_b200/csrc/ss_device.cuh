@@ -1358,6 +1358,225 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
   }
 }
 
+// ------------------------------------------------ fused J^T z gather
+// The PCR operator's J^T z -> u = M^-1 J^T z without the tet column sums in
+// HBM (structured mode). Particles are partitioned into blocks (the snake:
+// one block per link, no element spans two links); a CTA owns one block for
+// FW env-lanes and accumulates the block's node sums in shared memory. Every
+// element touching the block is scattered into them in a static schedule of
+// conflict-free chunks (no two elements of a chunk share a node of the
+// block; a barrier between chunks), families in the reference's order —
+// distance rows, tets, attachments, contact normals, contact friction —
+// so every node's sum is a fixed-order, deterministic sum of the same terms
+// k_gather adds (per-term values bitwise equal; the order within a family
+// is the chunk order instead of ascending element id). The tet terms are
+// computed from z, the quaternion and S (tet_jt_cols) on the fly: 24 fewer
+// doubles of HBM traffic per tet and PCR iteration than k_tet_jt writing tC
+// and k_gather reading it back, and one launch fewer.
+struct FusedPlan {
+  int n_blocks;      // particle blocks (the body CTAs follow: blockIdx.y == n_blocks)
+  int FW, FIL;       // env lanes x item lanes per CTA (FW * FIL = SS_THREADS); chunk <= FIL
+  int nb_max;        // particles of the largest block (shared accumulator rows)
+  const int* blk_p0;    // [n_blocks] first particle
+  const int* blk_np;    // [n_blocks] particle count
+  const int* blk_cptr;  // [n_blocks + 1] chunks of each block
+  const int* chk;       // [n_chunks] family << 24 | element count; [n_chunks + 1] starts follow
+  const int* elist;     // element ids (family-local), chunk after chunk
+  const int2* enode;    // per elist entry: its 4 block-local particles, 16 bits each (0xFFFF: none)
+  int sched_max;        // ints of the largest block's schedule (shared copy)
+};
+
+// raw loads of one element of a chunk (issued one chunk ahead)
+struct FLoad {
+  double x[16];
+  int idx[4];
+  int fam;
+  int e;  // -1: no element for this thread
+};
+
+// sched (shared): [nch] headers, [nch] starts (block-relative), then per
+// element its id and its packed particles (2 ints)
+template <int FW>
+DI void fused_load(const Ctx& c, const int* sched, int nch, int k, int il, int env, FLoad& L) {
+  const int E = c.D.E, nt = c.D.nt, nd = c.D.nd, na = c.D.na, ns = c.D.ns;
+  const int hdr = sched[k];
+  L.fam = hdr >> 24;
+  const int cnt = hdr & 0xFFFFFF;
+  L.e = -1;
+  if (il >= cnt) return;
+  const int* el = sched + 2 * nch + 3 * (sched[nch + k] + il);
+  const int e = el[0];
+  const unsigned pk0 = (unsigned)el[1], pk1 = (unsigned)el[2];
+  L.e = e;
+  L.idx[0] = (int)(pk0 & 0xFFFF);
+  L.idx[1] = (int)(pk0 >> 16);
+  L.idx[2] = (int)(pk1 & 0xFFFF);
+  L.idx[3] = (int)(pk1 >> 16);
+  const double* __restrict__ xs = c.K.z;
+  const double* __restrict__ xc = c.K.z + (size_t)c.D.ms * E;
+  if (L.fam == F_TET) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) L.x[i] = xs[IX(c.D.ot + i * nt + e)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) L.x[6 + q] = c.S.quat[IX(q * nt + e)];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) L.x[10 + q] = c.K.tS[IX(q * nt + e)];
+  } else if (L.fam == F_DIST) {
+    L.x[0] = xs[IX(c.D.od + e)];
+    L.x[1] = c.S.dirs[IX(e)];
+    L.x[2] = c.S.dirs[IX(nd + e)];
+    L.x[3] = c.S.dirs[IX(2 * nd + e)];
+  } else if (L.fam == F_ATTP) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) L.x[i] = xs[IX(c.D.oa + i * na + e)];
+  } else {  // particle contact slot e
+    L.x[0] = c.K.present[IX(e)] != 0 ? 1.0 : 0.0;
+    L.x[1] = xc[IX(e)];
+    L.x[2] = c.K.actf[IX(e)];
+    L.x[3] = xc[IX(ns + e)];
+    L.x[4] = xc[IX(2 * ns + e)];
+  }
+}
+
+// one element's contribution to up to 4 particles (block-local; -1: none),
+// per-term values exactly those of inc_particle
+DI void fused_contrib(const Ctx& c, const FLoad& L, int* node, double* v) {
+  node[0] = node[1] = node[2] = node[3] = 0xFFFF;
+  if (L.e < 0) return;
+  if (L.fam == F_TET) {
+    TetC T;
+    double Ri[9];
+    tet_unpack(L.x + 6, L.x + 10, T);
+    tet_rinv(c, L.e, Ri);
+    tet_jt_cols(T, Ri, L.x, v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) node[k] = L.idx[k];
+  } else if (L.fam == F_DIST) {
+    const double xr = L.x[0], d0 = L.x[1], d1 = L.x[2], d2 = L.x[3];
+    node[0] = L.idx[0];
+    node[1] = L.idx[1];
+    v[0] = 0.0 + d0 * xr;
+    v[1] = 0.0 + d1 * xr;
+    v[2] = 0.0 + d2 * xr;
+    v[3] = 0.0 + (-d0) * xr;
+    v[4] = 0.0 + (-d1) * xr;
+    v[5] = 0.0 + (-d2) * xr;
+  } else if (L.fam == F_ATTP) {
+    const double rw[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_ += att_val(i, a, rw) * L.x[i];
+      v[a] = s_;
+    }
+    node[0] = L.idx[0];
+  } else {
+    // contact slot: normal row (if present), then friction rows (if active);
+    // as two terms added in that order (slot 0 and slot 1 of the same node)
+    const double xn = L.x[1], xf0 = L.x[3], xf1 = L.x[4];
+    if (L.x[0] != 0.0) {
+      v[0] = 0.0 + 0.0 * xn;
+      v[1] = 0.0 + 0.0 * xn;
+      v[2] = 0.0 + 1.0 * xn;
+      node[0] = L.idx[0];
+    }
+    if (L.x[2] != 0.0) {
+      double a0 = 0.0 + 1.0 * xf0;
+      a0 += 0.0 * xf1;
+      double a1 = 0.0 + 0.0 * xf0;
+      a1 += 1.0 * xf1;
+      double a2 = 0.0 + 0.0 * xf0;
+      a2 += 0.0 * xf1;
+      v[3] = a0;
+      v[4] = a1;
+      v[5] = a2;
+      node[1] = L.idx[0];
+    }
+  }
+}
+
+#ifndef SS_FUSED_MINB
+#define SS_FUSED_MINB 2
+#endif
+template <int FW>
+__global__ void __launch_bounds__(SS_THREADS, SS_FUSED_MINB) k_gather_fused(const Ctx c, const FusedPlan fp) {
+  extern __shared__ double fsm[];
+  constexpr int FIL = SS_THREADS / FW;
+  const int E = c.D.E;
+  const int lane = threadIdx.x % FW, il = threadIdx.x / FW;
+  const int env = blockIdx.x * FW + lane;
+  const int P = c.D.P;
+  if ((int)blockIdx.y >= fp.n_blocks) {
+    // bodies (k_gather<1> body branch)
+    const double* __restrict__ xs = c.K.z;
+    const double* __restrict__ xc = c.K.z + (size_t)c.D.ms * E;
+    for (int b = il; b < c.D.nb; b += FIL) {
+      const int it = P + b;
+      const int k0 = c.T.inc_ptr[it], k1 = c.T.inc_ptr[it + 1];
+      double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int k = k0; k < k1; ++k) {
+        double acc[6];
+        if (!inc_body(c, c.T.inc[k], 0, xs, xc, env, acc)) continue;
+#pragma unroll
+        for (int kk = 0; kk < 6; ++kk) w[kk] += acc[kk];
+      }
+      gather_body_out(c, b, 0, w, env);
+    }
+    return;
+  }
+  const int blk = blockIdx.y;
+  const int p0 = fp.blk_p0[blk], np = fp.blk_np[blk];
+  double* acc = fsm;  // [np * 3][FW]
+  int* sched = reinterpret_cast<int*>(fsm + (size_t)fp.nb_max * 3 * FW);
+  for (int k = threadIdx.x; k < np * 3 * FW; k += SS_THREADS) acc[k] = 0.0;
+  const int c0 = fp.blk_cptr[blk], c1 = fp.blk_cptr[blk + 1], nch = c1 - c0;
+  {
+    // this block's schedule into shared memory (headers, starts, elements)
+    const int n_all = fp.blk_cptr[fp.n_blocks];
+    const int s_0 = fp.chk[n_all + c0];
+    const int s_1 = fp.chk[n_all + c1];
+    for (int k = threadIdx.x; k < nch; k += SS_THREADS) {
+      sched[k] = fp.chk[c0 + k];
+      sched[nch + k] = fp.chk[n_all + c0 + k] - s_0;
+    }
+    int* el = sched + 2 * nch;
+    for (int k = threadIdx.x; k < s_1 - s_0; k += SS_THREADS) {
+      const int2 pk = fp.enode[s_0 + k];
+      el[3 * k] = fp.elist[s_0 + k];
+      el[3 * k + 1] = pk.x;
+      el[3 * k + 2] = pk.y;
+    }
+  }
+  __syncthreads();
+  FLoad L;
+  if (nch > 0) fused_load<FW>(c, sched, nch, 0, il, env, L);
+  for (int k = 0; k < nch; ++k) {
+    int node[4];
+    double v[12];
+    fused_contrib(c, L, node, v);
+    if (k + 1 < nch) fused_load<FW>(c, sched, nch, k + 1, il, env, L);  // in flight over the adds
+    __syncthreads();  // the previous chunk's adds are done
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int n = node[k];
+      if (n >= np) continue;  // 0xFFFF: no particle of this block
+      double* a = acc + (size_t)(3 * n) * FW + lane;
+      a[0] += v[3 * k];
+      a[FW] += v[3 * k + 1];
+      a[2 * FW] += v[3 * k + 2];
+    }
+  }
+  __syncthreads();
+  for (int n = il; n < np; n += FIL) {
+    const int it = p0 + n;
+    const double im = c.T.inv_mass[it];
+    c.K.u[IX(3 * it)] = im * acc[(3 * n) * FW + lane];
+    c.K.u[IX(3 * it + 1)] = im * acc[(3 * n + 1) * FW + lane];
+    c.K.u[IX(3 * it + 2)] = im * acc[(3 * n + 2) * FW + lane];
+  }
+}
+
 // --------------------------------------------------------------- J rows
 // block_forward of each family on a DOF vector vec ([ndof][E]);
 // numba_backend.py:31-40 order (j ascending from acc = 0).

@@ -294,3 +294,46 @@ def test_set_channel_targets_then_step_none():
     bs.set_channel_targets(np.array([[8.0, -4.0, 0.0, 1.0]] * 3), latency=False)
     p = bs.get_state_arrays()["pressures"]
     assert np.array_equal(p[2], [0.0, 8.0, 4.0, 0.0, 0.0, 0.0, 0.0, 1.0])
+
+
+@pytest.mark.parametrize("n,fw,smem", [(40, "8", None), (40, "4", None), (40, "8", "20000"),
+                                        (3, "1", None)])
+def test_fused_gather_matches_gather(n, fw, smem):
+    """k_gather_fused (J^T z of the PCR loop scattered through shared
+    memory, no tet column sums in HBM) against k_tet_jt + k_gather (serial
+    walk): the same terms in another fixed order. A small shared budget
+    splits each link into blocks (elements spanning two blocks)."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(3)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        env = {"SS_FUSED": mode, "SS_FUSED_W": fw, "SS_GATHER_SPLIT": "1"}
+        if smem:
+            env["SS_FUSED_SMEM"] = smem
+        os.environ.update(env)
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+        info = sim.solver_info
+        assert info["fused_gather"] == (mode == "1")
+        if mode == "1":
+            assert info["fused_blocks"] == (4 if not smem else 16), info
+        names = sim.profile_frames(cmds[0], True, 1)
+        assert (names["k_gather_fused"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k, tol in (("positions", 1e-9), ("velocities", 1e-7), ("lam_tetra", 1e-7),
+                   ("pressures", 0.0), ("tet_quats", 1e-9)):
+        a, b = out["0"][k], out["1"][k]
+        scale = max(float(np.max(np.abs(a))), 1e-30)
+        assert np.max(np.abs(a - b)) <= tol * scale, k
