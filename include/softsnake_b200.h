@@ -170,6 +170,44 @@ const char* ss_build_id(void);
 const char* ss_last_error(void);
 int ss_device_count(int* n);
 
+/* ---- device-side scene construction ----
+ * The link meshes of build_snake (snake.py:97-189): particle grid,
+ * five-tet cells with TetraElement.from_positions (constraints.py:128-137)
+ * and tetra_compliance (constraints.py:26-40), lumped masses, the cable
+ * network and the frame mounts, for every link of every snake, built on the
+ * device and copied into caller-owned host arrays (links concatenated in
+ * the reference order; particle base = link * particles_per_link). Every
+ * value is bitwise the reference's numpy result (ss_build.cuh). The rigid
+ * bodies, hinges, wheels and attachment anchors (O(links)) stay on the host.
+ */
+typedef struct ss_link_mesh_params {
+  int32_t sections, width_nodes, height_nodes;  /* S, W, H (scene.py:20-22) */
+  int32_t n_links;                              /* all snakes' links       */
+  double dx, dy, dz;          /* link_length/(S-1), link_width/(W-1), link_height/(H-1) */
+  double half_width;          /* 0.5 * link_width                          */
+  double youngs_modulus, poisson, density;
+  double actuation_compliance, inextensible_compliance, structural_compliance;
+  const double* origins;      /* [n_links, 3] (snake.py:314-316)          */
+  const int32_t* channels;    /* [n_links, 2] left, right channel         */
+} ss_link_mesh_params;
+/* per-link counts: counts[0] particles, [1] tets, [2] cables, [3] mounts per face */
+int ss_link_mesh_counts(const ss_link_mesh_params* p, int32_t* counts);
+typedef struct ss_link_mesh_out {  /* host arrays, n_links x the per-link counts */
+  double* positions;        /* [P, 3]   */
+  double* masses;           /* [P]      */
+  int32_t* tets;            /* [T, 4]   */
+  double* rest_inv;         /* [T, 3, 3] */
+  double* rest_volume;      /* [T]      */
+  double* compliance;       /* [T, 6, 6] */
+  int32_t* pairs;           /* [C, 2]   */
+  double* rest;             /* [C]      */
+  double* cable_compliance; /* [C]      */
+  int32_t* kind;            /* [C]      */
+  int32_t* channel;         /* [C]      */
+  int32_t* mounts;          /* [n_links, 2, 6] start face, end face */
+} ss_link_mesh_out;
+int ss_build_link_meshes(const ss_link_mesh_params* p, int device, ss_link_mesh_out* out);
+
 /* Simulator.__init__ (solver.py:157-265) for n_envs independent copies:
  * upload topology, allocate state for n_envs copies on `device`. The
  * initial state of every env is zero except quaternions (identity), dirs

@@ -97,6 +97,26 @@ class SsSystemView(C.Structure):
         ("ang_inv", "d"))]
 
 
+class SsLinkMeshParams(C.Structure):
+    """ss_link_mesh_params (include/softsnake_b200.h)."""
+    _fields_ = [
+        ("sections", C.c_int32), ("width_nodes", C.c_int32), ("height_nodes", C.c_int32),
+        ("n_links", C.c_int32), ("dx", C.c_double), ("dy", C.c_double), ("dz", C.c_double),
+        ("half_width", C.c_double), ("youngs_modulus", C.c_double), ("poisson", C.c_double),
+        ("density", C.c_double), ("actuation_compliance", C.c_double),
+        ("inextensible_compliance", C.c_double), ("structural_compliance", C.c_double),
+        ("origins", _dp), ("channels", _ip),
+    ]
+
+
+class SsLinkMeshOut(C.Structure):
+    """ss_link_mesh_out (include/softsnake_b200.h)."""
+    _fields_ = [(n, C.POINTER(C.c_double) if t == "d" else C.POINTER(C.c_int32)) for n, t in (
+        ("positions", "d"), ("masses", "d"), ("tets", "i"), ("rest_inv", "d"),
+        ("rest_volume", "d"), ("compliance", "d"), ("pairs", "i"), ("rest", "d"),
+        ("cable_compliance", "d"), ("kind", "i"), ("channel", "i"), ("mounts", "i"))]
+
+
 def _ptr(a: np.ndarray | None, kind):
     if a is None or a.size == 0:
         return C.cast(None, kind)

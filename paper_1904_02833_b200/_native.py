@@ -8,7 +8,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from ._abi import SsEnvStats, SsParams, SsStateView, SsSystemView, SsTopology
+from ._abi import (SsEnvStats, SsLinkMeshOut, SsLinkMeshParams, SsParams, SsStateView,
+                   SsSystemView, SsTopology)
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.environ.get("SS_LIB_OVERRIDE") or os.path.join(LIB_DIR, "libsoftsnake_b200.so")
@@ -51,6 +52,8 @@ SIGNATURES = {
     "ss_solver_info": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "ss_cluster_stamps": (C.c_int, [_vp, C.POINTER(C.c_longlong)]),
     "ss_profile_frames": (C.c_int, [_vp, _dp, _i, _i, _dp, C.POINTER(C.c_int)]),
+    "ss_link_mesh_counts": (C.c_int, [C.POINTER(SsLinkMeshParams), _ip]),
+    "ss_build_link_meshes": (C.c_int, [C.POINTER(SsLinkMeshParams), _i, C.POINTER(SsLinkMeshOut)]),
     "ssk_block_forward": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "ssk_block_transpose": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp]),
     "ssk_block_rowdiag": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),

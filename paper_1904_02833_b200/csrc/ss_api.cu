@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/softsnake_b200.h"
+#include "ss_build.cuh"
 #include "ss_cluster.cuh"
 #include "ss_device.cuh"
 #include "ss_kabi.cuh"
@@ -2021,6 +2022,98 @@ int ss_profile_frames(ss_handle* H, const double* commands, int latency, int n_f
       cudaEventDestroy(e.second.second);
     }
   }
+  return SS_OK;
+}
+
+// ------------------------------------------------ device scene builder
+static int link_counts(const ss_link_mesh_params* p, int32_t* c) {
+  const int S = p->sections, W = p->width_nodes, H = p->height_nodes;
+  if (W < 5 || H < 2 || S < 2) return fail(SS_EINVAL, "link grid needs at least 5x2 nodes and 2 sections");
+  if (p->n_links < 0) return fail(SS_EINVAL, "n_links must be >= 0");
+  const int n_ring = S - S / 3 - (S % 3 >= 2 ? 1 : 0);
+  c[0] = S * W * H;
+  c[1] = 5 * (S - 1) * (W - 1) * (H - 1);
+  c[2] = 2 * H + H * (S - 1) + n_ring * (2 * (W - 1) + 2 * (H - 1)) + 4 * S;
+  c[3] = 6;
+  return SS_OK;
+}
+
+int ss_link_mesh_counts(const ss_link_mesh_params* p, int32_t* counts) {
+  if (!p || !counts) return fail(SS_EINVAL, "null argument");
+  return link_counts(p, counts);
+}
+
+int ss_build_link_meshes(const ss_link_mesh_params* p, int device, ss_link_mesh_out* o) {
+  if (!p || !o) return fail(SS_EINVAL, "null argument");
+  int32_t cnt[4];
+  int rc = link_counts(p, cnt);
+  if (rc) return rc;
+  const long L = p->n_links;
+  if (L == 0) return SS_OK;
+  if (!p->origins || !p->channels) return fail(SS_EINVAL, "null origins / channels");
+  CK(cudaSetDevice(device));
+  const size_t nP = (size_t)L * cnt[0], nT = (size_t)L * cnt[1], nC = (size_t)L * cnt[2];
+  // one device block: doubles, then ints
+  const size_t nd = 3 * L + 3 * nP + nP + 9 * nT + nT + 36 * nT + 2 * nC;
+  const size_t ni = 2 * L + 4 * nT + 2 * nC + 2 * nC + 12 * L + 1;
+  char* mem = nullptr;
+  CK(cudaMalloc(&mem, 8 * nd + 4 * ni));
+  double* dd = (double*)mem;
+  double* d_orig = dd; dd += 3 * L;
+  double* d_pos = dd; dd += 3 * nP;
+  double* d_mass = dd; dd += nP;
+  double* d_rinv = dd; dd += 9 * nT;
+  double* d_vol = dd; dd += nT;
+  double* d_comp = dd; dd += 36 * nT;
+  double* d_rest = dd; dd += nC;
+  double* d_ccomp = dd; dd += nC;
+  int* di = (int*)dd;
+  int* d_chan = di; di += 2 * L;
+  int* d_tets = di; di += 4 * nT;
+  int* d_pairs = di; di += 2 * nC;
+  int* d_kind = di; di += nC;
+  int* d_cch = di; di += nC;
+  int* d_mounts = di; di += 12 * L;
+  int* d_bad = di;
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+  ok(cudaMemcpy(d_orig, p->origins, 24 * L, cudaMemcpyHostToDevice));
+  ok(cudaMemcpy(d_chan, p->channels, 8 * L, cudaMemcpyHostToDevice));
+  ok(cudaMemset(d_bad, 0, 4));
+  SsbLink g;
+  g.S = p->sections; g.W = p->width_nodes; g.H = p->height_nodes; g.L = (int)L;
+  g.dx = p->dx; g.dy = p->dy; g.dz = p->dz; g.hw = p->half_width;
+  g.E = p->youngs_modulus; g.nu = p->poisson; g.rho = p->density;
+  g.c_act = p->actuation_compliance; g.c_inext = p->inextensible_compliance;
+  g.c_struct = p->structural_compliance;
+  g.origin = d_orig; g.chan = d_chan;
+  g.NP = cnt[0]; g.NT = cnt[1]; g.NC = cnt[2];
+  auto blocks = [](size_t n) { return (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16); };
+  if (e == cudaSuccess) {
+    ssb_k_particles<<<blocks(nP), 256>>>(g, d_pos);
+    ssb_k_tets<<<blocks(nT), 256>>>(g, d_tets, d_rinv, d_vol, d_comp, d_bad);
+    ssb_k_masses<<<blocks(nP), 256>>>(g, d_vol, d_mass);
+    ssb_k_cables<<<blocks(nC), 256>>>(g, d_pairs, d_rest, d_ccomp, d_kind, d_cch, d_mounts);
+    e = cudaGetLastError();
+  }
+  int bad = 0;
+  ok(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost));
+  auto down = [&](void* h, const void* d, size_t bytes) { if (h && bytes) ok(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost)); };
+  down(o->positions, d_pos, 24 * nP);
+  down(o->masses, d_mass, 8 * nP);
+  down(o->tets, d_tets, 16 * nT);
+  down(o->rest_inv, d_rinv, 72 * nT);
+  down(o->rest_volume, d_vol, 8 * nT);
+  down(o->compliance, d_comp, 288 * nT);
+  down(o->pairs, d_pairs, 8 * nC);
+  down(o->rest, d_rest, 8 * nC);
+  down(o->cable_compliance, d_ccomp, 8 * nC);
+  down(o->kind, d_kind, 4 * nC);
+  down(o->channel, d_cch, 4 * nC);
+  down(o->mounts, d_mounts, 48 * L);
+  cudaFree(mem);
+  if (e != cudaSuccess) return fail(SS_ECUDA, "scene builder: %s", cudaGetErrorString(e));
+  if (bad) return fail(SS_EINVAL, "degenerate rest tetrahedron (%d tets)", bad);
   return SS_OK;
 }
 

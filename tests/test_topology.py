@@ -1,6 +1,8 @@
 """The builder reproduces the reference topology bit for bit (digests of
 every array the reference builder produced, tests/golden/topology_digest.npz,
-made by tests/golden/make_goldens.py from /root/reference)."""
+made by tests/golden/make_goldens.py from /root/reference). Both builders:
+the host one (numpy, CPU) and the device one (ss_build_link_meshes, the
+link meshes built on the GPU)."""
 import hashlib
 
 import numpy as np
@@ -37,11 +39,16 @@ def _arrays(model):
     return out
 
 
+BUILDERS = [pytest.param("host"), pytest.param("device", marks=pytest.mark.gpu)]
+
+
+@pytest.mark.parametrize("builder", BUILDERS)
 @pytest.mark.parametrize("tag", ["S", "B"])
-def test_topology_bit_identical(tag):
+def test_topology_bit_identical(tag, builder):
     g = load_golden("topology_digest.npz")
     sc = M.SceneConfig()
-    model = M.build_snake(sc) if tag == "S" else M.build_bend_fixture(sc)
+    model = (M.build_snake(sc, builder=builder) if tag == "S"
+             else M.build_bend_fixture(sc, builder=builder))
     arrays = _arrays(model)
     keys = sorted(k.split(":", 1)[1] for k in g.files if k.startswith(tag + ":"))
     assert keys == sorted(arrays), "array set differs from the reference builder"
@@ -50,19 +57,21 @@ def test_topology_bit_identical(tag):
 
 
 def test_snake_counts_match_survey():
-    sim = M.build_snake(M.SceneConfig()).sim
+    sim = M.build_snake(M.SceneConfig(), builder="host").sim
     assert sim.state.num_particles == 1456 and sim.state.num_bodies == 15
     assert sim.distances.count == 1080 and sim.tetras.count == 4320
     assert sim.attachments.count == 48 and sim.hinges.count == 10 and len(sim.wheels) == 10
     assert sim.static_rows == 27194
 
 
-def test_degenerate_grid_rejected():
+@pytest.mark.parametrize("builder", BUILDERS)
+def test_degenerate_grid_rejected(builder):
     with pytest.raises(ValueError):
-        M.build_snake(M.SceneConfig(width_nodes=4))
+        M.build_snake(M.SceneConfig(width_nodes=4), builder=builder)
 
 
-def test_hires_topology_bit_identical():
+@pytest.mark.parametrize("builder", BUILDERS)
+def test_hires_topology_bit_identical(builder):
     """Config 5 (1,000,000 tets): every topology array equals the reference
     builder's (digests in tests/golden/step_H.npz)."""
     import os
@@ -70,8 +79,14 @@ def test_hires_topology_bit_identical():
     if not os.path.exists(path):
         pytest.skip("step_H.npz not generated")
     g = np.load(path)
-    model = M.build_snake(M.SceneConfig(sections=101, width_nodes=26, height_nodes=21))
+    import time
+    t0 = time.perf_counter()
+    model = M.build_snake(M.SceneConfig(sections=101, width_nodes=26, height_nodes=21),
+                          builder=builder)
+    secs = time.perf_counter() - t0
     assert model.sim.tetras.count == 1_000_000
+    if builder == "device":
+        assert secs < 5.0, f"device build of the 1M-tet scene took {secs:.1f} s"
     arrays = _arrays(model)
     keys = sorted(k.split(":", 1)[1] for k in g.files if k.startswith("topo:"))
     assert keys == sorted(arrays)
@@ -79,7 +94,8 @@ def test_hires_topology_bit_identical():
         assert _digest(arrays[k]) == str(g[f"topo:{k}"]), f"H {k} differs from reference"
 
 
-def test_two_snake_topology_bit_identical():
+@pytest.mark.parametrize("builder", BUILDERS)
+def test_two_snake_topology_bit_identical(builder):
     """build_snake(n_snakes=2) (the coupled scene) equals the reference
     builder's arrays (digests in tests/golden/step_S2.npz)."""
     import os
@@ -87,7 +103,7 @@ def test_two_snake_topology_bit_identical():
     if not os.path.exists(path):
         pytest.skip("step_S2.npz not generated")
     g = np.load(path)
-    arrays = _arrays(M.build_snake(M.SceneConfig(), n_snakes=2))
+    arrays = _arrays(M.build_snake(M.SceneConfig(), n_snakes=2, builder=builder))
     keys = sorted(k.split(":", 1)[1] for k in g.files if k.startswith("topo:"))
     assert keys == sorted(arrays)
     for k in keys:
