@@ -82,34 +82,56 @@ def env_commands(n_envs: int, frames: int, first_frame: int, env0: int = 0,
 # ----------------------------------------------------------------- CPU leg
 class CpuArm:
     """The reference algorithm (oracle C port) on host cores: one snake per
-    core, stepped in threads (ctypes releases the GIL)."""
+    core, one dedicated worker thread per snake pinned to its own core (the
+    survey's taskset protocol); ctypes releases the GIL."""
 
     def __init__(self, cores: int | None = None, frames: int = 64):
-        from concurrent.futures import ThreadPoolExecutor
+        import queue
         from oracle.oracle import OracleSim
         import paper_1904_02833_b200 as M
         from paper_1904_02833_b200.model import build_scene_parts
-        self.cores = cores or len(os.sched_getaffinity(0))
+        cpus = sorted(os.sched_getaffinity(0))
+        self.cores = cores or len(cpus)
+        self.cpus = [cpus[i % len(cpus)] for i in range(self.cores)]
         sc = M.SceneConfig()
         parts, *_ = build_scene_parts(sc)
         cfg = sc.solver_config()
         self.sims = [OracleSim(config=cfg, **parts) for _ in range(self.cores)]
         self.cmds = env_commands(self.cores, frames, 0)
         self.frame = 0
-        self.ex = ThreadPoolExecutor(self.cores)
+        self.todo = [queue.Queue() for _ in range(self.cores)]
+        self.done = queue.Queue()
+        self.threads = [threading.Thread(target=self._worker, args=(e,), daemon=True)
+                        for e in range(self.cores)]
+        for t in self.threads:
+            t.start()
 
-    def step(self, frames: int = 1):
-        f0 = self.frame
-
-        def run(e):
+    def _worker(self, e):
+        try:
+            os.sched_setaffinity(0, {self.cpus[e]})  # this thread only
+        except OSError:
+            pass
+        while True:
+            job = self.todo[e].get()
+            if job is None:
+                return
+            f0, frames = job
             for f in range(frames):
                 self.sims[e].step(self.cmds[(f0 + f) % len(self.cmds), e], True)
+            self.done.put(e)
 
-        list(self.ex.map(run, range(self.cores)))
+    def step(self, frames: int = 1):
+        for q in self.todo:
+            q.put((self.frame, frames))
+        for _ in range(self.cores):
+            self.done.get()
         self.frame += frames
 
     def close(self):
-        self.ex.shutdown()
+        for q in self.todo:
+            q.put(None)
+        for t in self.threads:
+            t.join()
 
 
 def cpu_oracle_rate(frames_per_core: int, cores: int | None = None):
@@ -121,6 +143,20 @@ def cpu_oracle_rate(frames_per_core: int, cores: int | None = None):
     dt = time.perf_counter() - t
     arm.close()
     return arm.cores * frames_per_core / dt, arm.cores, dt
+
+
+def numba_calibration(port_rate: float) -> dict:
+    """The reference's own numba path cannot run on the GPU box (it is not
+    installed there); profiles/cpu_calibration.json holds both measured on
+    one host (tools/cpu_calibration.py). Scale the port's rate by it."""
+    path = os.path.join(ROOT, "profiles", "cpu_calibration.json")
+    if not os.path.exists(path):
+        return {}
+    cal = json.load(open(path))
+    r = float(cal["port_over_numba_aggregate"])
+    return {"numba_equivalent_value": port_rate / r, "port_over_numba": r,
+            "calibration": "profiles/cpu_calibration.json (numba reference vs this port, "
+                           f"{cal['host_cores']} pinned processes on one host)"}
 
 
 def run_reference(args):
@@ -146,7 +182,8 @@ def run_reference(args):
         "config": {"workload": WORKLOAD, "sample": f"{cores} snakes x 1 frame per step"},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"oracle/softsnake_oracle.c (C restatement of the reference "
-                                   f"step), 1 snake per core, {args.steps} frames"},
+                                   f"step), 1 snake per core (pinned thread), {args.steps} frames",
+                         **numba_calibration(rate)},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -308,6 +345,21 @@ def main():
     step_bytes = sum(roofline.bytes_per_launch_per_env(k, d, nc_mean, structured, pcr)
                      * (v[1] / args.profile_frames) * n / waves for k, v in prof.items())
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
+    # per-kernel table (live CUDA events): algorithmic bytes per launch, mean
+    # launch time, achieved GB/s and the fraction of the HBM peak
+    per_kernel = {}
+    for k, (kms, kl) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+        if kl == 0:
+            continue
+        kb = roofline.bytes_per_launch_per_env(k, d, nc_mean, structured, pcr) * n / waves
+        kus = 1e3 * kms / kl
+        per_kernel[k] = {"ms_per_frame": round(kms / args.profile_frames, 4),
+                         "launches_per_frame": kl // args.profile_frames,
+                         "bytes_per_launch": kb, "avg_launch_us": round(kus, 3),
+                         "gbps": round(kb / (kus * 1e-6) / 1e9, 1) if kb else None,
+                         "frac": round(kb / (kus * 1e-6) / 1e9 / peak, 4) if kb else None}
+    # the reference-layout byte model beside this build's own
+    survey = roofline.survey_model(d, nc_mean, sim.config.substeps, sim.config.newton_iters, pcr)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and not hires:  # traffic.json holds the S-scene capture
@@ -346,12 +398,25 @@ def main():
                      "bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
                      "mean_contacts_per_substep": nc_mean,
                      "share_of_step": prof[top][0] / sum(v[0] for v in prof.values()),
-                     "traffic": traffic},
+                     "traffic": traffic,
+                     "traffic_over_model": traffic / per_launch if traffic else None},
         # whole step: every kernel's algorithmic bytes per frame over the graph-timed
         # frame (concurrent lanes overlap kernels, so this exceeds per-kernel rates)
         "step_bandwidth": {"achieved": step_bytes * (K / (ms * 1e-3)) / 1e9, "peak": peak,
                            "unit": "GB/s", "frac": step_bytes * (K / (ms * 1e-3)) / 1e9 / peak,
                            "bytes_per_step": step_bytes},
+        # SURVEY.md §8(d) model (reference layout: stored 6x12 tet J read twice per
+        # apply, 6x6 E_tet) vs this build's own bytes (compact J, structured apply)
+        "byte_models": {
+            "survey_8d_bytes_per_snake_step": survey["total"],
+            "survey_8d_env_private_bytes_per_snake_step": survey["env_private"],
+            "implementation_bytes_per_snake_step": step_bytes / n,
+            "ratio_survey_env_private_over_implementation": survey["env_private"] / (step_bytes / n),
+            "effective_frac_on_survey_env_private": survey["env_private"] * (total * K / (ms * 1e-3))
+            / world / 1e9 / peak,
+            "note": "effective_frac > 1 means the build moves fewer bytes than the reference "
+                    "layout needs; step_bandwidth.frac is the fraction on the build's own bytes"},
+        "per_kernel": per_kernel,
         "kernels_ms_per_frame": {k: round(v[0] / args.profile_frames, 4) for k, v in prof.items()},
         "profiled_ms_per_frame": step_ms_prof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": n * 4 * 8,
@@ -377,7 +442,9 @@ def main():
         rate, cores, secs = cpu_oracle_rate(args.cpu_frames)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"oracle C port, {cores} snakes x {args.cpu_frames} "
-                                          f"frames ({secs:.1f} s wall)"}
+                                          f"frames ({secs:.1f} s wall), one pinned thread "
+                                          f"per core"}
+        line["cpu_baseline"].update(numba_calibration(rate))
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -316,6 +316,10 @@ int64_t ss_device_bytes(ss_handle* h);
  * fused (k_gather_fused), info[6] its particle blocks, info[7] its chunks
  * over all blocks. info must hold 8 ints. */
 int ss_solver_info(ss_handle* h, int* info);
+/* Debug: with SS_GUARD=1 set at ss_create every device array is followed by
+ * a 0xA5 guard band; *bad_bytes = guard bytes changed since (an out-of-
+ * bounds write), or -1 when the handle has no guards. */
+int ss_check_guards(ss_handle* h, int64_t* bad_bytes);
 /* Debug: clock64 phase stamps of one PCR iteration of the cluster solver
  * (handle created with SS_CLUSTER_STAMPS set); out[16]. */
 int ss_cluster_stamps(ss_handle* h, long long* out);

@@ -50,6 +50,7 @@ SIGNATURES = {
     "ss_device_bytes": (C.c_int64, [_vp]),
     "ss_kernel_names": (C.c_int, [C.POINTER(C.c_char_p), _i]),
     "ss_solver_info": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "ss_check_guards": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "ss_cluster_stamps": (C.c_int, [_vp, C.POINTER(C.c_longlong)]),
     "ss_profile_frames": (C.c_int, [_vp, _dp, _i, _i, _dp, C.POINTER(C.c_int)]),
     "ss_link_mesh_counts": (C.c_int, [C.POINTER(SsLinkMeshParams), _ip]),

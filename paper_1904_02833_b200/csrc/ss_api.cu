@@ -4,6 +4,7 @@
 // reference accumulation order, compliance pattern), device memory, the
 // per-frame launch sequence captured once into a CUDA graph, state I/O.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -26,6 +27,18 @@ namespace {
 
 thread_local std::string g_err;
 
+// NVTX range for the duration of a scope (frames, waves, builder phases;
+// inside a graph replay the kernels themselves carry no host ranges)
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name, bool on_ = true) : on(on_) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -43,15 +56,27 @@ int fail(int code, const char* fmt, ...) {
       return fail(SS_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));        \
   } while (0)
 
+// Debug (SS_GUARD=1): every array is followed by a guard band filled with
+// 0xA5 at creation; ss_check_guards reports bytes that changed (an
+// out-of-bounds write past some array). compute-sanitizer is not available
+// on the GPU pool, so this and SS_POISON (workspace filled with NaN bytes
+// instead of zeros: a read-before-write shows up as a changed result) are
+// the memcheck / initcheck stand-ins (tests/test_gpu_guard.py).
+thread_local size_t g_guard = 0;
+thread_local std::vector<std::pair<char*, size_t>>* g_spans = nullptr;
+
 // bump allocator over one cudaMalloc
 struct Arena {
   char* base = nullptr;
   size_t cap = 0, off = 0;
   template <typename T>
   T* take(size_t n) {
-    size_t bytes = ((n * sizeof(T) + 255) / 256) * 256;
+    const size_t data = n * sizeof(T);
+    size_t bytes = ((data + 255) / 256) * 256;
     if (bytes == 0) bytes = 256;
+    bytes += g_guard;
     T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    if (base && g_guard && g_spans) g_spans->push_back({base + off + data, bytes - data});
     off += bytes;
     return p;
   }
@@ -108,6 +133,11 @@ struct ss_handle {
   void* fplan_mem = nullptr;
   size_t fused_smem = 0;
   int fused_chunks = 0;
+  int apply_async = 0;       // k_apply_rows_async (cp.async-staged tet operands)
+  int jtg_grid = 0;          // k_jtg persistent grid (resident CTAs)
+  JtgPlan jplan{};           // k_jtg plan (fixed at ss_create)
+  size_t apply_async_smem = 0;
+  std::vector<std::pair<char*, size_t>> guards;  // SS_GUARD spans
 };
 
 namespace {
@@ -154,8 +184,9 @@ GridCaps grid_caps(int device) {
 const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots",    "k_eval_tet",
                                     "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_apply_rows",
                                     "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
-                                    "k_tet_jt",      "k_newton_cluster", "k_gather_fused"};
-constexpr int kNumKernels = 15;
+                                    "k_tet_jt",      "k_newton_cluster", "k_gather_fused",
+                                    "k_apply_rows_async", "k_jtg"};
+constexpr int kNumKernels = 17;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -183,6 +214,26 @@ int kid(const char* name) {
     }                                                                    \
     ++n;                                                                 \
   } while (0)
+
+// ------------------------------------------------------ k_jtg plan
+static int jtg_ring_slots() { return (int)std::max(2L, env_long("SS_JTG_RING", 3)); }
+static int jtg_lag() { return (int)std::max(1L, env_long("SS_JTG_LAG", 2)); }
+static bool jtg_wanted(const ss_handle* H, const Dims& D) {
+  // opt-in (SS_JTG=1): starved of ready work items at L2-sized rings — 1024 envs:
+  // 76-171 ms/frame against 46.5 for k_tet_jt + k_gather (profiles/r2_summary.md)
+  return env_long("SS_JTG", 0) && !H->c.p.exact_j && !H->use_cluster && D.nt > 0 &&
+         D.E >= 64 && D.E % 32 == 0;
+}
+static JtgPlan jtg_plan(const Dims& D) {
+  JtgPlan jp;
+  jp.tiles = D.E / 32;
+  jp.n1 = (D.nt + JTG_TETS - 1) / JTG_TETS;
+  jp.n2 = (D.P + D.nb + JTG_NODES - 1) / JTG_NODES;
+  jp.lag = std::min(jtg_lag(), jp.tiles);
+  jp.ring = std::max(jtg_ring_slots(), jp.lag + 1);
+  jp.n_items = jp.tiles * (jp.n1 + jp.n2);
+  return jp;
+}
 
 // Enqueue one frame (Simulator.step, solver.py:296-314) on the stream.
 // With prof, every launch is bracketed by CUDA events (eager, not graphed).
@@ -231,6 +282,9 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const int gait = has_cmd == 2 ? 1 : 0;
   LAUNCH(k_frame_begin, g_links, c, d_cmd, has_cmd == 1 ? 1 : 0, latency, gait);
   for (int sub = 0; sub < c.p.substeps; ++sub) {
+    // NVTX groups (eager profiled frames): substep > assembly / newton > pcr
+    NvtxRange nv_sub("substep", prof != nullptr);
+    NvtxRange* nv_asm = new NvtxRange("assembly: pre, contacts, eval", prof != nullptr);
     LAUNCH(k_pre, g_pre, c, gait && sub == 0 ? 1 : 0);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
     if (D.nt) LAUNCH(k_eval_tet<EX>, g_eval, c);  // + tet J^T lam
@@ -262,17 +316,29 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       }
       ++n;
       LAUNCH(k_integrate, g_int, c);
+      delete nv_asm;
       continue;
     }
     GATHER(1, xs_lam, xc_lam);  // v = vt + M^-1 J^T lam
+    delete nv_asm;
+    nv_asm = nullptr;
     for (int it = 0; it < c.p.newton; ++it) {
+      NvtxRange nv_newton("newton", prof != nullptr);
       LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
       if (H->keep && sub == c.p.substeps - 1 && it == c.p.newton - 1)
         CK(cudaMemcpyAsync(c.K.snap_rhs, c.K.r, 8 * (size_t)D.m * D.E, cudaMemcpyDeviceToDevice,
                            st));  // the snapshot's rhs (solver.py:515)
       if (c.p.pcr > 0) {
+        NvtxRange nv_pcr("pcr_solve", prof != nullptr);
         GATHER(0, xs_z, xc_z);
-        LAUNCH(k_apply_rows<EX>, g_red, c, 1);
+#define APPLY(setup_)                                                        \
+  do {                                                                       \
+    if (!EX && H->apply_async)                                               \
+      LAUNCH_SM(k_apply_rows_async, g_red, H->apply_async_smem, c, setup_);  \
+    else                                                                     \
+      LAUNCH(k_apply_rows<EX>, g_red, c, setup_);                            \
+  } while (0)
+        APPLY(1);
         LAUNCH(k_pcr_dir<EX>, g_dir, c, 1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
           LAUNCH(k_pcr_step<EX>, g_el, c, k);
@@ -285,11 +351,16 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
               case 4: LAUNCH_SM(k_gather_fused<4>, g_fu, sm, c, H->fplan); break;
               default: LAUNCH_SM(k_gather_fused<8>, g_fu, sm, c, H->fplan); break;
             }
+          } else if (!EX && c.K.ring) {
+            // persistent tile-pipelined J^T gather (k_jtg): counters reset first
+            const JtgPlan& jp = H->jplan;
+            CK(cudaMemsetAsync(c.K.jctr, 0, sizeof(int) * (1 + 2 * (size_t)jp.tiles), st));
+            LAUNCH(k_jtg, dim3(H->jtg_grid), c, jp);
           } else {
             if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
             GATHER(0, xs_z, xc_z);
           }
-          LAUNCH(k_apply_rows<EX>, g_red, c, 0);
+          APPLY(0);
           LAUNCH(k_pcr_dir<EX>, g_dir, c, 0);
         }
       }
@@ -305,6 +376,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
 }
 #undef LAUNCH
 #undef LAUNCH_SM
+#undef APPLY
 
 int enqueue_frame(ss_handle* H, int w, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
   const Ctx& c = H->wave[w];
@@ -389,7 +461,9 @@ __global__ void k_fill(double* p, size_t n, double val) {
 static int plan_fused(ss_handle* H, const Dims& D, const int* tets, const std::vector<int>& d_i,
                       const std::vector<int>& d_j, const std::vector<int>& a_p,
                       const std::vector<int>& slot_part) {
-  const long mode = env_long("SS_FUSED", -1);  // -1 auto, 0 off, 1 on
+  // off by default: bitwise-different order and latency-bound (r2 measurements:
+  // 42-47 ms/frame vs 46.7 for k_tet_jt + k_gather at 1024 envs)
+  const long mode = env_long("SS_FUSED", 0);  // -1 auto, 0 off, 1 on
   H->fused = 0;
   if (mode == 0 || D.nt == 0 || H->c.p.exact_j || H->use_cluster) return SS_OK;
   const int FW = (int)std::min<long>(env_long("SS_FUSED_W", 8), D.E);
@@ -948,6 +1022,13 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   *out = nullptr;
   CK(cudaSetDevice(device));
   const GridCaps caps = grid_caps(device);
+  struct GuardScope {  // SS_GUARD bands for this create only
+    GuardScope() { g_guard = env_long("SS_GUARD", 0) ? 256 : 0; }
+    ~GuardScope() {
+      g_guard = 0;
+      g_spans = nullptr;
+    }
+  } guard_scope;
 
   Dims D{};
   // lanes of one wave: ss_params.wave_envs, or by default at most
@@ -1176,6 +1257,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // ---- allocations
   ss_handle* H = new ss_handle();
   H->caps = caps;
+  g_spans = &H->guards;
   {
     // 0 = auto: the widest split up to 4 whose lanes still fit one resident
     // wave (coupled 2/10-snake scenes at E = 1: 7.8 -> 5.6 / 9.1 -> 7.1 ms per
@@ -1375,6 +1457,10 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.last_step = A.take<int>(Es);
     K.broken = A.take<int>(Es);
     K.snap_rhs = p->keep_matrix ? A.take<double>((size_t)D.m * Es) : nullptr;
+    // k_jtg ring (structured streaming path with E % 32 == 0; SS_JTG=0 off)
+    const bool jtg = jtg_wanted(H, D);
+    K.ring = jtg ? A.take<double>((size_t)jtg_ring_slots() * 12 * D.nt * 32) : nullptr;
+    K.jctr = jtg ? A.take<int>(1 + 2 * (size_t)(Es / 32)) : nullptr;
   };
   Arena sa, wa;
   plan_state(sa);
@@ -1446,7 +1532,12 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   }
   H->bytes += sblock * H->n_waves + wa.cap * H->n_work;
   CK(cudaMemsetAsync(H->state_mem, 0, sblock * H->n_waves, H->stream));
-  CK(cudaMemsetAsync(H->work_mem, 0, wa.cap * H->n_work, H->stream));
+  // SS_POISON: workspace bytes 0xFF (doubles NaN, ints -1) instead of zeros
+  CK(cudaMemsetAsync(H->work_mem, env_long("SS_POISON", 0) ? 0xFF : 0, wa.cap * H->n_work,
+                     H->stream));
+  // the reduction tickets start at zero by design (the last block resets them)
+  for (int l = 0; l < H->n_work; ++l)
+    CK(cudaMemsetAsync(blk_work[l].cnt, 0, sizeof(int) * D.tiles, H->stream));
   H->lane_stream[0] = H->stream;
   if (H->n_lanes > 1) {
     CK(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
@@ -1482,6 +1573,25 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     const size_t cmd_n = (size_t)H->n_waves * H->c.D.E * std::max(1, D.links);
     CK(cudaMalloc(&H->d_cmd, 8 * cmd_n));
     CK(cudaMemsetAsync(H->d_cmd, 0, 8 * cmd_n, H->stream));
+  }
+  for (const auto& g : H->guards) CK(cudaMemsetAsync(g.first, 0xA5, g.second, H->stream));
+  {
+    int occ = 3, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_jtg, SS_THREADS, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
+    H->jtg_grid = (int)env_long("SS_JTG_GRID", (long)std::max(1, occ) * sms);
+    H->jplan = jtg_plan(H->c.D);
+    H->jplan.ring = jtg_ring_slots();  // as allocated
+    if (H->jplan.lag >= H->jplan.ring) H->jplan.lag = H->jplan.ring - 1;
+  }
+  // cp.async-staged k_apply_rows (structured streaming path; SS_APPLY_ASYNC=0 off)
+  // opt-in (SS_APPLY_ASYNC=1): bitwise equal, 37.5 vs 37.9 ms/frame at 1024 envs
+  // with 2 stages, slower with 3-4 (the staging buffers take the L1 the u gathers use)
+  if (!H->c.p.exact_j && !H->use_cluster && D.nt > 0 && env_long("SS_APPLY_ASYNC", 0)) {
+    H->apply_async_smem = SS_APPLYA_STAGES * 16 * SS_THREADS * sizeof(double);
+    CK(cudaFuncSetAttribute(k_apply_rows_async, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)H->apply_async_smem));
+    H->apply_async = 1;
   }
   {
     int frc = plan_fused(H, H->c.D, t->tets, d_i, d_j, a_p, slot_part);
@@ -1618,6 +1728,7 @@ int ss_get_state_device(ss_handle* H, int env0, int n, ss_state_view* v) {
 // on_device: 0 host commands, 1 device commands, 2 on-device gait (cmd unused)
 static int step_impl(ss_handle* H, const double* cmd, int on_device, int latency, int n_frames) {
   if (!H) return fail(SS_EINVAL, "null handle");
+  NvtxRange nv_step("ss_step");
   if (n_frames < 0) return fail(SS_EINVAL, "n_frames must be >= 0");
   CK(cudaSetDevice(H->device));
   const Dims& D = H->c.D;
@@ -1968,6 +2079,21 @@ int ss_cluster_stamps(ss_handle* H, long long* out) {
   if (!H || !out) return fail(SS_EINVAL, "null argument");
   if (!H->plan.dbg) return fail(SS_EINVAL, "stamps off (set SS_CLUSTER_STAMPS)");
   CK(cudaMemcpy(out, H->plan.dbg, 16 * sizeof(long long), cudaMemcpyDeviceToHost));
+  return SS_OK;
+}
+
+int ss_check_guards(ss_handle* H, int64_t* bad_bytes) {
+  if (!H || !bad_bytes) return fail(SS_EINVAL, "null argument");
+  CK(cudaSetDevice(H->device));
+  CK(cudaDeviceSynchronize());
+  int64_t bad = 0;
+  std::vector<unsigned char> buf;
+  for (const auto& g : H->guards) {
+    buf.resize(g.second);
+    CK(cudaMemcpy(buf.data(), g.first, g.second, cudaMemcpyDeviceToHost));
+    for (unsigned char b : buf) bad += b != 0xA5;
+  }
+  *bad_bytes = H->guards.empty() ? -1 : bad;
   return SS_OK;
 }
 

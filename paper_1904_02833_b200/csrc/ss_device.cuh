@@ -101,6 +101,11 @@ struct Work {
   int* last_step;               // [E] index of the last executed k_pcr_step (-1: none)
   int* broken;                  // [E]
   double* snap_rhs;             // [m] rhs of the last Newton pass (keep_matrix only)
+  // k_jtg (persistent, tile-pipelined J^T z gather): ring of tet column sums
+  // [JTG_RING][12][nt][32] and its counters ([0] queue head, then per tile
+  // [tiles] P1 done, [tiles] P2 done); reset by a memset node per launch
+  double* ring;
+  int* jctr;
 };
 
 struct Ctx {
@@ -1358,6 +1363,166 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
   }
 }
 
+// ------------------------------------ persistent tile-pipelined J^T z gather
+// k_tet_jt + k_gather<1> (mode 0) of one PCR iteration as ONE persistent
+// launch over a queue of work items, per 32-env tile: P1(T) pieces compute
+// the tet column sums of tile T into a ring slot, P2(T) pieces gather them
+// per DOF (same code, same order: bitwise the two-kernel result). The queue
+// interleaves tiles with a lag (P1(T + lag) before P2(T)), so a tile's
+// column sums are read back a few microseconds after they are written and
+// stay in L2 (the ring is an L2-persisting access window): the 24 doubles
+// per tet of tC traffic leave HBM. Items are dequeued with an atomic head,
+// so every item a CTA waits on is held by a running CTA (no deadlock under
+// partial residency). Needs E % 32 == 0 (one tile = 32 env lanes).
+#ifndef JTG_TETS
+#define JTG_TETS 128   // tets per P1 piece (8 item lanes x 16)
+#endif
+#ifndef JTG_NODES
+#define JTG_NODES 64   // DOFs (particles, then bodies) per P2 piece
+#endif
+struct JtgPlan {
+  int tiles, n1, n2, lag, ring, n_items;
+};
+DI void jtg_decode(const JtgPlan& jp, int q, int& phase, int& T, int& piece) {
+  // step s holds [P1(s) if s < tiles][P2(s - lag) if s >= lag]
+  const int tl = jp.tiles, lag = jp.lag, n1 = jp.n1, n2 = jp.n2;
+  // steps 0..lag-1 hold only P1 pieces
+  const int head = lag * n1;
+  if (q < head) {
+    phase = 1; T = q / n1; piece = q % n1;
+    return;
+  }
+  q -= head;
+  const int mid = (tl - lag) * (n1 + n2);  // steps lag..tiles-1 hold both
+  if (q < mid) {
+    const int s = lag + q / (n1 + n2), r = q % (n1 + n2);
+    if (r < n1) { phase = 1; T = s; piece = r; }
+    else { phase = 2; T = s - lag; piece = r - n1; }
+    return;
+  }
+  q -= mid;  // steps tiles..tiles+lag-1 hold only P2 pieces
+  phase = 2; T = tl - lag + q / n2; piece = q % n2;
+}
+DI void jtg_wait(const int* ctr, int target) {
+  if (threadIdx.x == 0) {
+    while (*(volatile const int*)ctr < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+DI void jtg_signal(int* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1);
+  }
+}
+
+#ifndef SS_JTG_MINB
+#define SS_JTG_MINB 3
+#endif
+__global__ void __launch_bounds__(SS_THREADS, SS_JTG_MINB) k_jtg(const Ctx c, const JtgPlan jp) {
+  const int E = c.D.E, nt = c.D.nt, P = c.D.P, nb = c.D.nb;
+  const int lane = threadIdx.x & 31, il = threadIdx.x >> 5;
+  int* head = c.K.jctr;
+  int* p1_done = c.K.jctr + 1;
+  int* p2_done = c.K.jctr + 1 + jp.tiles;
+  const double* __restrict__ xs = c.K.z;
+  const double* __restrict__ xc = c.K.z + (size_t)c.D.ms * E;
+  __shared__ int s_next;
+  if (threadIdx.x == 0) s_next = atomicAdd(head, 1);
+  for (;;) {
+    __syncthreads();
+    const int q = s_next;
+    __syncthreads();
+    if (q >= jp.n_items) return;
+    // the next item is claimed now; its atomic overlaps this item's work
+    if (threadIdx.x == 0) s_next = atomicAdd(head, 1);
+    int phase, T, piece;
+    jtg_decode(jp, q, phase, T, piece);
+    const int env = T * 32 + lane;
+    double* ring = c.K.ring + (size_t)(T % jp.ring) * 12 * nt * 32;
+    if (phase == 1) {
+      if (T >= jp.ring) jtg_wait(p2_done + T - jp.ring, jp.n2);  // ring slot free
+      const int t0 = piece * JTG_TETS;
+      for (int t = t0 + il; t < t0 + JTG_TETS && t < nt; t += 8) {
+        double z6[6], Ri[9], col12[12];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) z6[i] = c.K.z[IX(c.D.ot + i * nt + t)];
+        TetC TT;
+        tet_load(c, t, env, TT);
+        tet_rinv(c, t, Ri);
+        tet_jt_cols(TT, Ri, z6, col12);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) ring[((size_t)k * nt + t) * 32 + lane] = col12[k];
+      }
+      jtg_signal(p1_done + T);
+    } else {
+      jtg_wait(p1_done + T, jp.n1);
+      const int n0 = piece * JTG_NODES;
+      for (int it = n0 + il; it < n0 + JTG_NODES && it < P + nb; it += 8) {
+        const int k0 = c.T.inc_ptr[it], k1 = c.T.inc_ptr[it + 1];
+        if (it < P) {
+          double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+          const int2 tr = c.T.inc_tet[it];
+          for (int k = k0; k < k1; ++k) {
+            if (k == tr.x) {
+              // loads hoisted 6 incidences at a time (k_gather's order of adds)
+              constexpr int GU = 6;
+              for (; k + GU - 1 < tr.y; k += GU) {
+                double a[3 * GU];
+#pragma unroll
+                for (int j = 0; j < GU; ++j) {
+                  const int code = c.T.inc[k + j];
+                  const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+                  const double* rp = ring + ((size_t)(3 * v) * nt + e) * 32 + lane;
+                  a[3 * j] = __ldcg(rp);
+                  a[3 * j + 1] = __ldcg(rp + (size_t)nt * 32);
+                  a[3 * j + 2] = __ldcg(rp + (size_t)2 * nt * 32);
+                }
+#pragma unroll
+                for (int j = 0; j < GU; ++j) {
+                  w0 += a[3 * j];
+                  w1 += a[3 * j + 1];
+                  w2 += a[3 * j + 2];
+                }
+              }
+              for (; k < tr.y; ++k) {
+                const int code = c.T.inc[k];
+                const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+                const double* rp = ring + ((size_t)(3 * v) * nt + e) * 32 + lane;
+                w0 += __ldcg(rp);
+                w1 += __ldcg(rp + (size_t)nt * 32);
+                w2 += __ldcg(rp + (size_t)2 * nt * 32);
+              }
+              if (k >= k1) break;
+            }
+            double a0, a1, a2;
+            if (!inc_particle(c, c.T.inc[k], 0, xs, xc, env, a0, a1, a2)) continue;
+            w0 += a0;
+            w1 += a1;
+            w2 += a2;
+          }
+          const double im = c.T.inv_mass[it];
+          c.K.u[IX(3 * it)] = im * w0;
+          c.K.u[IX(3 * it + 1)] = im * w1;
+          c.K.u[IX(3 * it + 2)] = im * w2;
+        } else {
+          double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+          for (int k = k0; k < k1; ++k) {
+            double acc[6];
+            if (!inc_body(c, c.T.inc[k], 0, xs, xc, env, acc)) continue;
+#pragma unroll
+            for (int kk = 0; kk < 6; ++kk) w[kk] += acc[kk];
+          }
+          gather_body_out(c, it - P, 0, w, env);
+        }
+      }
+      jtg_signal(p2_done + T);
+    }
+  }
+}
+
 // ------------------------------------------------ fused J^T z gather
 // The PCR operator's J^T z -> u = M^-1 J^T z without the tet column sums in
 // HBM (structured mode). Particles are partitioned into blocks (the snake:
@@ -1945,6 +2110,180 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY_MINB) k_apply_rows(const 
       part += z1 * a1;
     }
   }
+  double tot;
+  if (reduce_env(c, part, &tot)) {
+    if (setup) {
+      c.K.rho[env] = tot;
+    } else if (!c.K.broken[env]) {
+      const double rho = c.K.rho[env];
+      c.K.beta[env] = rho > 1e-300 ? tot / rho : 0.0;
+      c.K.rho[env] = tot;
+    }
+  }
+}
+
+// k_apply_rows (structured mode) with the tet operands staged through shared
+// memory by cp.async: the quaternion, S and z of a thread's NEXT tet item
+// (16 doubles) are copied asynchronously into the other half of a per-thread
+// double buffer while the current item computes, so the loads of two items
+// are in flight per thread without holding them in registers (the kernel is
+// bound by memory-level parallelism at 16 warps/SM). The first tet item's
+// copy is issued at kernel start and overlaps the distance rows. Same
+// arithmetic in the same order per thread: bitwise k_apply_rows<false>.
+DI void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+DI void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+DI void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+DI void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+#ifndef SS_APPLYA_MINB
+#define SS_APPLYA_MINB 2
+#endif
+#ifndef SS_APPLYA_STAGES
+#define SS_APPLYA_STAGES 2
+#endif
+template <int N>
+DI void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__global__ void __launch_bounds__(SS_THREADS, SS_APPLYA_MINB) k_apply_rows_async(const Ctx c,
+                                                                                 int setup) {
+  SETUP
+  extern __shared__ double abuf[];  // [SS_APPLYA_STAGES][16][SS_THREADS]
+  constexpr int NST = SS_APPLYA_STAGES;
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const double* u = c.K.u;
+  const double* z = c.K.z;
+  const int stride = gridDim.y * IL;
+  auto stage_tet = [&](int t, int st) {
+    double* b = abuf + (size_t)st * 16 * SS_THREADS + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cp_async8(b + k * SS_THREADS, c.S.quat + IX(k * nt + t));
+#pragma unroll
+    for (int k = 0; k < 6; ++k) cp_async8(b + (4 + k) * SS_THREADS, c.K.tS + IX(k * nt + t));
+#pragma unroll
+    for (int i = 0; i < 6; ++i) cp_async8(b + (10 + i) * SS_THREADS, z + IX(c.D.ot + i * nt + t));
+  };
+  // the first NST-1 tet items of this thread, staged now (overlap the distance rows)
+  int stg = 0;
+  int it_pf;  // the next tet item to stage
+  {
+    int it0 = blockIdx.y * IL + il;
+    if (it0 < nd) it0 += ((nd - it0 + stride - 1) / stride) * stride;
+    it_pf = it0;
+    for (int q = 0; q < NST - 1; ++q) {
+      if (it_pf < nd + nt) stage_tet(it_pf - nd, q);
+      cp_async_commit();
+      it_pf += stride;
+    }
+  }
+  double part = 0.0;
+  int pf_t = -1, pf_n0 = 0, pf_n1 = 0, pf_n2 = 0, pf_n3 = 0;
+  FOR_ITEMS(it, nd + nt + na + nh + ns) {
+    if (it < nd) {
+      const int row = c.D.od + it;
+      const double zr = z[IX(row)];
+      const double az = row_dist(c, it, u, env) + c.T.d_dyn[it] * zr;
+      c.K.az[IX(row)] = az;
+      part += zr * az;
+    } else if (it < nd + nt) {
+      const int t = it - nd;
+      double Ri[9], y[6], zz[6], ez[6], uv[12];
+      int nid[4];
+      if (pf_t == t) {
+        nid[0] = pf_n0; nid[1] = pf_n1; nid[2] = pf_n2; nid[3] = pf_n3;
+      } else {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + t];
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) uv[3 * v + a] = u[IX(3 * nid[v] + a)];
+      tet_rinv(c, t, Ri);
+      const int tn = t + stride;
+      if (tn < nt) {
+        pf_t = tn;
+        pf_n0 = c.T.t_idx[tn];
+        pf_n1 = c.T.t_idx[nt + tn];
+        pf_n2 = c.T.t_idx[2 * nt + tn];
+        pf_n3 = c.T.t_idx[3 * nt + tn];
+      }
+      {
+        int sn = stg + NST - 1;
+        if (sn >= NST) sn -= NST;
+        if (it_pf < nd + nt) stage_tet(it_pf - nd, sn);
+        cp_async_commit();
+        it_pf += stride;
+      }
+      cp_async_wait_n<NST - 1>();  // this item's stage has landed
+      const double* b = abuf + (size_t)stg * 16 * SS_THREADS + threadIdx.x;
+      double q[4], sv[6];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = b[k * SS_THREADS];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sv[k] = b[(4 + k) * SS_THREADS];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) zz[i] = b[(10 + i) * SS_THREADS];
+      stg = stg + 1 == NST ? 0 : stg + 1;
+      TetC T;
+      tet_unpack(q, sv, T);
+      tet_forward_uv(T, Ri, uv, y);
+      ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], zz, ez);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double az = y[i] + ez[i];
+        c.K.az[IX(c.D.ot + i * nt + t)] = az;
+        part += zz[i] * az;
+      }
+    } else if (it < nd + nt + na) {
+      const int a = it - nd - nt;
+      double y[3];
+      rows_att(c, a, u, env, y);
+      const double dyn = c.T.a_dyn[a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int row = c.D.oa + i * na + a;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else if (it < nd + nt + na + nh) {
+      const int hh = it - nd - nt - na;
+      double y[5];
+      rows_hinge(c, hh, u, env, y);
+      const double dyn = c.T.h_dyn[hh];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int row = c.D.oh + i * nh + hh;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else {
+      const int s = it - nd - nt - na - nh;
+      if (!c.K.present[IX(s)]) continue;
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+      const double zn = z[IX(rn)], z0 = z[IX(rf0)], z1 = z[IX(rf1)];
+      double y[3];
+      rows_slot(c, s, u, env, y);
+      const double an = y[0] + c.K.dynn[IX(s)] * zn;
+      double a0 = z0, a1 = z1;
+      if (c.K.actf[IX(s)] != 0.0) {
+        a0 = y[1] + c.p.fdyn * z0;
+        a1 = y[2] + c.p.fdyn * z1;
+      }
+      c.K.az[IX(rn)] = an;
+      c.K.az[IX(rf0)] = a0;
+      c.K.az[IX(rf1)] = a1;
+      part += zn * an;
+      part += z0 * a0;
+      part += z1 * a1;
+    }
+  }
+  cp_async_wait0();
   double tot;
   if (reduce_env(c, part, &tot)) {
     if (setup) {

@@ -61,6 +61,11 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
     if kernel == "k_apply_rows":
         # compact J, small-family J, u (once), z (own rows), write az
         return jc + small_j + F8 * d["ndof"] + F8 * 2 * rows + flags
+    if kernel == "k_gather_fused":
+        # z of every row of the particle families (tet z, dist, attach, contact
+        # rows), compact J, dirs, flags; write u — no tC
+        return F8 * 6 * d["nt"] + jc + F8 * (rows - 6 * d["nt"]) + small_j + \
+            F8 * 9 * d["nb"] + flags + F8 * d["ndof"]
     if kernel == "k_gather":
         # tC once, non-tet x rows once, small-family J, ang_inv; write u
         return tc + F8 * (rows - 6 * d["nt"]) + small_j + F8 * 9 * d["nb"] + flags + \
@@ -76,3 +81,27 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
         return F8 * (3 * d["P"] + 8 * d["nt"] + 6 * d["nt"] + 6 * d["nt"] + 12 * d["nt"]
                      + 6 * d["nt"])
     return 0.0
+
+
+def survey_model(d: dict, nc: float, substeps: int = 2, newton: int = 4, pcr: int = 20) -> dict:
+    """SURVEY.md §8(d) algorithmic bytes per snake-step in the reference's
+    data layout (fp64 values, int32 indices, the 6x12 tet J stored and read
+    twice per operator apply, the 6x6 E_tet block per tet):
+      B_apply = 2 (8 Jnnz + 4 idx) + 8*36 T + 8 (4 m) + 8 (4 ndof) + 8*9 nb
+      B_vec   = 8*11 m
+      frame   = substeps [newton (21 (B_apply + B_vec) + 2 Jpass + 6 m-vectors) + 3 Jpass]
+    with Jpass = 8 Jnnz + 4 idx. Shared by identical envs: the index arrays
+    and E_tet; the rest is env-private. (The 21 applies are pcr + 1.)"""
+    nt, nd, na, nh = d["nt"], d["nd"], d["na"], d["nh"]
+    m = d["ms"] + 3 * nc
+    jnnz = 6 * nd + 72 * nt + 27 * na + 60 * nh + 18 * nc
+    idx = 6 * nd + 12 * nt + 9 * na + 12 * nh + 6 * nc
+    b_apply = 2 * (F8 * jnnz + 4 * idx) + F8 * 36 * nt + F8 * 4 * m + F8 * 4 * d["ndof"] + \
+        F8 * 9 * d["nb"]
+    b_vec = F8 * 11 * m
+    jpass = F8 * jnnz + 4 * idx
+    applies = pcr + 1
+    total = substeps * (newton * (applies * (b_apply + b_vec) + 2 * jpass + 6 * F8 * m) + 3 * jpass)
+    sh_apply = 2 * 4 * idx + F8 * 36 * nt
+    shared = substeps * (newton * (applies * sh_apply + 2 * 4 * idx) + 3 * 4 * idx)
+    return {"total": float(total), "shared": float(shared), "env_private": float(total - shared)}

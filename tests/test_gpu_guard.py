@@ -1,0 +1,75 @@
+"""Memory-safety checks without compute-sanitizer (closed on this GPU pool):
+SS_GUARD=1 puts a 0xA5 band after every device array and ss_check_guards
+counts changed bytes (out-of-bounds writes); SS_POISON=1 fills the
+workspace with NaN bytes instead of zeros, so a kernel reading workspace
+before writing it changes the result. Each path (streaming kernels with
+last-block reductions, the fused shared-memory gather, the cluster solver
+with DSMEM, the 1024-env bench layout) must leave every guard intact and
+give bitwise the unpoisoned state."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import paper_1904_02833_b200 as M
+from paper_1904_02833_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__ as g
+    g.build()
+
+
+def _run(case, debug):
+    env = {"SS_GUARD": "1", "SS_POISON": "1"} if debug else {}
+    if case in ("streaming", "fused", "bench"):
+        env["SS_FUSED"] = "1" if case == "fused" else ("0" if case == "streaming" else "")
+        env = {k: v for k, v in env.items() if v != ""}
+    os.environ.update(env)
+    try:
+        sc = M.SceneConfig()
+        if case == "cluster":
+            m = M.build_bend_fixture(sc)
+            m.sim.config.solver = "cluster"
+            n = 1
+        else:
+            n = 1024 if case == "bench" else 64
+            m = M.build_snake(sc, n_envs=n)
+            m.sim.config.solver = "auto" if case == "bench" else "streaming"
+        sim = m.sim
+        sim._ensure()
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+    rng = np.random.default_rng(4)
+    links = sim.n_links
+    for _ in range(2):
+        sim.step(np.clip(rng.normal(0, 4, (n, links)), -8, 8), latency=True)
+    sim.synchronize()
+    bad = C.c_int64(0)
+    _native.check(_native.lib().ss_check_guards(sim._h, C.byref(bad)))
+    out = sim.get_state_arrays()
+    info = sim.solver_info
+    sim.close()
+    return out, bad.value, info
+
+
+@pytest.mark.parametrize("case", ["streaming", "fused", "cluster", "bench"])
+def test_guards_intact_and_poison_invisible(case):
+    ref, bad0, info0 = _run(case, False)
+    got, bad, info = _run(case, True)
+    assert bad0 == -1 and bad == 0, f"{bad} guard bytes overwritten"
+    assert info == info0
+    if case == "fused":
+        assert info["fused_gather"]
+    if case == "cluster":
+        assert info["cluster"]
+    for k in ref:
+        assert np.array_equal(ref[k], got[k], equal_nan=True), k
+    assert np.isfinite(got["positions"]).all()

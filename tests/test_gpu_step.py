@@ -337,3 +337,63 @@ def test_fused_gather_matches_gather(n, fw, smem):
         a, b = out["0"][k], out["1"][k]
         scale = max(float(np.max(np.abs(a))), 1e-30)
         assert np.max(np.abs(a - b)) <= tol * scale, k
+
+
+@pytest.mark.parametrize("n", [40, 96])
+def test_apply_async_bitwise(n):
+    """k_apply_rows_async (tet operands staged through shared memory by
+    cp.async) gives bitwise the state of k_apply_rows<false>."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(9)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_APPLY_ASYNC"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_APPLY_ASYNC", None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_apply_rows_async"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("n,ring,lag", [(96, "3", "2"), (256, "2", "1"), (128, "4", "3")])
+def test_jtg_bitwise(n, ring, lag):
+    """k_jtg (persistent tile-pipelined J^T z gather, column sums through an
+    L2-resident ring) gives bitwise the state of k_tet_jt + k_gather."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(13)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        env = {"SS_JTG": mode, "SS_JTG_RING": ring, "SS_JTG_LAG": lag}
+        os.environ.update(env)
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_jtg"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k

@@ -1,0 +1,81 @@
+"""Per-core speed of the reference's own CPU path (the numba Simulator of
+/root/reference, SURVEY.md §8(d) protocol: one process per core, pinned,
+*_NUM_THREADS=1) against the oracle C port that bench.py times on the GPU
+box (the reference cannot travel there). Run in this container:
+
+    python tools/cpu_calibration.py [frames]
+
+Writes profiles/cpu_calibration.json: per-core snake-steps/s of both on the
+same host, same scene (build_snake(SceneConfig())), same commands (default
+gait), 3 warm-up frames excluded; and the aggregate over all cores.
+"""
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FR = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+
+CHILD = r"""
+import os, sys, time
+os.sched_setaffinity(0, {int(sys.argv[2])})
+kind, frames = sys.argv[1], int(sys.argv[3])
+sys.path.insert(0, %r)
+import numpy as np
+if kind == "numba":
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import softsnake as R
+    sc = R.SceneConfig(backend="numba")
+    m = R.build_snake(sc)
+    step = lambda c: m.sim.step(c, latency=True)
+    cmd = lambda i: m.commands(i * sc.dt)
+else:
+    import paper_1904_02833_b200 as M
+    from paper_1904_02833_b200.model import build_scene_parts
+    from oracle.oracle import OracleSim
+    sc = M.SceneConfig()
+    parts, *_ = build_scene_parts(sc)
+    o = OracleSim(config=sc.solver_config(), **parts)
+    g = M.GaitParams.from_scene(sc)
+    step = lambda c: o.step(c, True)
+    cmd = lambda i: M.gait_commands(g, i * sc.dt, 4, 4)
+for i in range(3):
+    step(cmd(i))
+t = time.perf_counter()
+for i in range(3, 3 + frames):
+    step(cmd(i))
+print(frames / (time.perf_counter() - t))
+""" % ROOT
+
+
+def run(kind, cores):
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               NUMBA_NUM_THREADS="1", NUMBA_CACHE_DIR="/tmp/numba_cache",
+               PYTHONPATH="/root/reference/pkg/src")
+    procs = [subprocess.Popen([sys.executable, "-c", CHILD, kind, str(c), str(FR)], env=env,
+                              stdout=subprocess.PIPE, text=True) for c in cores]
+    return [float(p.communicate()[0].strip().splitlines()[-1]) for p in procs]
+
+
+def main():
+    cpus = sorted(os.sched_getaffinity(0))
+    out = {"host_cores": len(cpus), "frames": FR, "scene": "build_snake(SceneConfig())"}
+    for kind in ("numba", "port"):
+        one = run(kind, cpus[:1])[0]
+        allc = run(kind, cpus)
+        out[kind] = {"per_core_1proc": one, "aggregate_all_cores": sum(allc),
+                     "per_core_all": [round(x, 3) for x in allc]}
+    out["port_over_numba_per_core"] = out["port"]["per_core_1proc"] / out["numba"]["per_core_1proc"]
+    out["port_over_numba_aggregate"] = (out["port"]["aggregate_all_cores"]
+                                       / out["numba"]["aggregate_all_cores"])
+    out["when"] = time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", "cpu_calibration.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
