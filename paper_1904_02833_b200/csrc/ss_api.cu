@@ -84,6 +84,7 @@ struct Arena {
 
 }  // namespace
 
+constexpr int kMaxGyRed2 = 96;  // k_apply_rows2 grid rows (partials per env) at most
 struct GridCaps {
   long stream = 148 * 32;  // PCR step, tet J^T z, element kernels without reduction
   long eval = 148 * 8;     // per-substep eval / integrate kernels
@@ -135,6 +136,9 @@ struct ss_handle {
   int fused_chunks = 0;
   int apply_async = 0;       // k_apply_rows_async (cp.async-staged tet operands)
   int jtg_grid = 0;          // k_jtg persistent grid (resident CTAs)
+  int pdl = 0;               // programmatic dependent launch of the frame kernels (SS_PDL)
+  int apply2 = 0;            // k_apply_rows2 (tet split over two warps; SS_APPLY2)
+  int gy_red2 = 1;           // its grid rows (one resident wave)
   JtgPlan jplan{};           // k_jtg plan (fixed at ss_create)
   size_t apply_async_smem = 0;
   std::vector<std::pair<char*, size_t>> guards;  // SS_GUARD spans
@@ -185,8 +189,8 @@ const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots", 
                                     "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_apply_rows",
                                     "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
                                     "k_tet_jt",      "k_newton_cluster", "k_gather_fused",
-                                    "k_apply_rows_async", "k_jtg"};
-constexpr int kNumKernels = 17;
+                                    "k_apply_rows_async", "k_jtg", "k_apply_rows2"};
+constexpr int kNumKernels = 18;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -207,7 +211,21 @@ int kid(const char* name) {
       cudaEventCreate(&e1_);                                             \
       cudaEventRecord(e0_, st);                                          \
     }                                                                    \
-    kern<<<grid, blk, smem, st>>>(__VA_ARGS__);                          \
+    if (H->pdl) {                                                        \
+      cudaLaunchConfig_t cfg_ = {};                                      \
+      cudaLaunchAttribute at_[1];                                        \
+      at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;    \
+      at_[0].val.programmaticStreamSerializationAllowed = 1;             \
+      cfg_.attrs = at_;                                                  \
+      cfg_.numAttrs = 1;                                                 \
+      cfg_.gridDim = grid;                                               \
+      cfg_.blockDim = blk;                                               \
+      cfg_.dynamicSmemBytes = smem;                                      \
+      cfg_.stream = st;                                                  \
+      CK(cudaLaunchKernelEx(&cfg_, kern, __VA_ARGS__));                  \
+    } else {                                                             \
+      kern<<<grid, blk, smem, st>>>(__VA_ARGS__);                        \
+    }                                                                    \
     if (prof) {                                                          \
       cudaEventRecord(e1_, st);                                          \
       prof->ev.push_back({kid(#kern), {e0_, e1_}});                      \
@@ -263,6 +281,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 g_gather = grid_items(D, (long)(D.P + D.nb) * gsp, H->caps.gather);
   const dim3 g_el = grid_items(D, n_el, H->caps.stream);
   const dim3 g_red(D.tiles, H->gy_red);
+  const dim3 g_red2(D.tiles, H->gy_red2);
   const dim3 g_dir(D.tiles, H->gy_dir);
   const dim3 g_int = grid_items(D, D.P + D.nb, H->caps.eval);
   const double* xs_lam = c.S.lam;
@@ -333,7 +352,9 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
         GATHER(0, xs_z, xc_z);
 #define APPLY(setup_)                                                        \
   do {                                                                       \
-    if (!EX && H->apply_async)                                               \
+    if (!EX && H->apply2)                                                    \
+      LAUNCH(k_apply_rows2, g_red2, c, setup_);                              \
+    else if (!EX && H->apply_async)                                          \
       LAUNCH_SM(k_apply_rows_async, g_red, H->apply_async_smem, c, setup_);  \
     else                                                                     \
       LAUNCH(k_apply_rows<EX>, g_red, c, setup_);                            \
@@ -1424,7 +1445,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   };
   auto plan_work = [&](Arena& A) {
     const size_t Es = H->c.D.E;
-    const int gy_max = std::max(H->gy_red, H->gy_dir);
+    const int gy_max = std::max(std::max(H->gy_red, H->gy_dir), kMaxGyRed2);
     Work& K = H->c.K;
     K.v = A.take<double>((size_t)D.ndof * Es);
     K.u = A.take<double>((size_t)D.ndof * Es);
@@ -1575,6 +1596,19 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     CK(cudaMemsetAsync(H->d_cmd, 0, 8 * cmd_n, H->stream));
   }
   for (const auto& g : H->guards) CK(cudaMemsetAsync(g.first, 0xA5, g.second, H->stream));
+  if (!H->c.p.exact_j && !H->use_cluster && D.nt > 0 && D.W == 32 && env_long("SS_APPLY2", 1)) {
+    // partials per env = grid rows: must fit the part buffer sized for gy_red / gy_dir
+    int occ = 3, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_rows2, SS_THREADS, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
+    long want = (long)sms * std::max(1, occ) / D.tiles;
+    want = std::max(1L, std::min(want, (long)kMaxGyRed2));
+    H->gy_red2 = (int)std::min<long>(env_long("SS_APPLY2_GY", want), kMaxGyRed2);
+    H->apply2 = 1;
+  }
+  // opt-in: no gain measured (coupled 2-snake frame 6.16 ms either way; 1024 envs and
+  // the 1M-tet scene within noise, profiles/r2_summary.md)
+  H->pdl = (int)env_long("SS_PDL", 0);
   {
     int occ = 3, sms = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_jtg, SS_THREADS, 0);

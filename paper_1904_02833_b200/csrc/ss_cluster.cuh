@@ -557,6 +557,7 @@ DI double cl_ddiv(double x, double dstored) { return EXACT ? x / dstored : x * d
 
 template <bool EXACT>
 __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, const ClPlan L) {
+  pdl_wait();
   extern __shared__ __align__(16) double sm_[];
   __shared__ double scratch[64];
   __shared__ double* peers[CL_MAXC];

@@ -116,7 +116,21 @@ struct Ctx {
   Work K;
 };
 
+// Programmatic dependent launch: every frame kernel may be launched before
+// its predecessor on the stream has finished (ss_api.cu, SS_PDL); it waits
+// here, before its first read, for the predecessor's memory to be visible
+// (a no-op without PDL). Only the launch latency and the predecessor's tail
+// overlap; no kernel reads anything before this point.
+DI void pdl_wait() {
+#ifndef SS_NO_PDL_TRIGGER
+  // the next kernel may start launching once every CTA of this one has started
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 #define SETUP                                              \
+  pdl_wait();                                              \
   const int E = c.D.E;                                     \
   const int lane = threadIdx.x & (c.D.W - 1);              \
   const int il = threadIdx.x >> c.D.lgW;                   \
@@ -1422,6 +1436,7 @@ DI void jtg_signal(int* ctr) {
 #define SS_JTG_MINB 3
 #endif
 __global__ void __launch_bounds__(SS_THREADS, SS_JTG_MINB) k_jtg(const Ctx c, const JtgPlan jp) {
+  pdl_wait();
   const int E = c.D.E, nt = c.D.nt, P = c.D.P, nb = c.D.nb;
   const int lane = threadIdx.x & 31, il = threadIdx.x >> 5;
   int* head = c.K.jctr;
@@ -1666,6 +1681,7 @@ DI void fused_contrib(const Ctx& c, const FLoad& L, int* node, double* v) {
 #endif
 template <int FW>
 __global__ void __launch_bounds__(SS_THREADS, SS_FUSED_MINB) k_gather_fused(const Ctx c, const FusedPlan fp) {
+  pdl_wait();
   extern __shared__ double fsm[];
   constexpr int FIL = SS_THREADS / FW;
   const int E = c.D.E;
@@ -2025,7 +2041,9 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY_MINB) k_apply_rows(const 
         for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
       } else {
         // every load of the tet issued before any arithmetic (one memory
-        // round trip per item instead of three)
+        // round trip per item instead of three); 32-bit element offsets
+        // stepped by the row stride nt*E (fewer integer instructions per
+        // address than the 64-bit IX products)
         double q[4], sv[6], uv[12];
         int nid[4];
         if (pf_t == t) {
@@ -2034,16 +2052,26 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY_MINB) k_apply_rows(const 
 #pragma unroll
           for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + t];
         }
+        const unsigned uE = (unsigned)E;
+        const unsigned ntE = (unsigned)nt * uE;
+        const unsigned tb = (unsigned)t * uE + (unsigned)env;
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
+        for (int v = 0; v < 4; ++v) {
+          const double* up = u + ((unsigned)(3 * nid[v]) * uE + (unsigned)env);
 #pragma unroll
-          for (int a = 0; a < 3; ++a) uv[3 * v + a] = u[IX(3 * nid[v] + a)];
+          for (int a = 0; a < 3; ++a) uv[3 * v + a] = up[a * uE];
+        }
+        {
+          const double* qp = c.S.quat + tb;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
+          for (int k = 0; k < 4; ++k) q[k] = qp[k * ntE];
+          const double* sp = c.K.tS + tb;
 #pragma unroll
-        for (int k = 0; k < 6; ++k) sv[k] = c.K.tS[IX(k * nt + t)];
+          for (int k = 0; k < 6; ++k) sv[k] = sp[k * ntE];
+          const double* zp = z + ((unsigned)c.D.ot * uE + tb);
 #pragma unroll
-        for (int i = 0; i < 6; ++i) zz[i] = z[IX(c.D.ot + i * nt + t)];
+          for (int i = 0; i < 6; ++i) zz[i] = zp[i * ntE];
+        }
         tet_rinv(c, t, Ri);
         const int tn = t + gridDim.y * IL;
         if (tn < nt) {
@@ -2057,11 +2085,16 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY_MINB) k_apply_rows(const 
         tet_forward_uv(T, Ri, uv, y);
       }
       ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], zz, ez);
+      {
+        const unsigned uE = (unsigned)E;
+        const unsigned ntE = (unsigned)nt * uE;
+        double* ap = c.K.az + ((unsigned)c.D.ot * uE + (unsigned)t * uE + (unsigned)env);
 #pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        const double az = y[i] + ez[i];
-        c.K.az[IX(c.D.ot + i * nt + t)] = az;
-        part += zz[i] * az;
+        for (int i = 0; i < 6; ++i) {
+          const double az = y[i] + ez[i];
+          ap[i * ntE] = az;
+          part += zz[i] * az;
+        }
       }
     } else if (it < nd + nt + na) {
       const int a = it - nd - nt;
@@ -2284,6 +2317,191 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLYA_MINB) k_apply_rows_async
     }
   }
   cp_async_wait0();
+  double tot;
+  if (reduce_env(c, part, &tot)) {
+    if (setup) {
+      c.K.rho[env] = tot;
+    } else if (!c.K.broken[env]) {
+      const double rho = c.K.rho[env];
+      c.K.beta[env] = rho > 1e-300 ? tot / rho : 0.0;
+      c.K.rho[env] = tot;
+    }
+  }
+}
+
+// k_apply_rows (structured mode, E >= 32) with each tet split over TWO warps
+// of the same 32 envs: warp A (even item lane) loads the 4 nodes' u, the
+// rest-shape inverse and the quaternion and forms G = R^T sum_v u_v w_v^T;
+// warp B (odd item lane) loads S, z and E_tet, forms K^-1, takes G through
+// shared memory (one named barrier per warp pair and item, G double
+// buffered) and finishes w = K^-1 ax(G), J u = voigt(sym(G) - sym(skew(w) S)),
+// az and the rho partial. The same operations as tet_forward_uv (every az
+// bitwise equal); half the live registers per thread, so three CTAs per SM
+// (24 warps) instead of two keep more loads in flight. The rho partials are
+// summed over a different thread assignment (rounding-level differences).
+#ifndef SS_APPLY2_MINB
+#define SS_APPLY2_MINB 3
+#endif
+DI void named_bar(int id, int count) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory"); }
+
+__global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(const Ctx c, int setup) {
+  SETUP
+  __shared__ double gsh[4][2][9][32];  // [pair][buffer][G entry][env lane]
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const double* u = c.K.u;
+  const double* z = c.K.z;
+  const int pair = il >> 1, role = il & 1;
+  const unsigned uE = (unsigned)E;
+  const unsigned ntE = (unsigned)nt * uE;
+  double part = 0.0;
+  int buf = 0;
+  // ---- tets: item lanes paired
+  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += gridDim.y * (IL >> 1)) {
+    const unsigned tb = (unsigned)t * uE + (unsigned)env;
+    double* g = &gsh[pair][buf][0][lane];
+    if (role == 0) {
+      int nid[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + t];
+      double uv[12], q[4], Ri[9];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const double* up = u + ((unsigned)(3 * nid[v]) * uE + (unsigned)env);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) uv[3 * v + a] = up[a * uE];
+      }
+      const double* qp = c.S.quat + tb;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = qp[k * ntE];
+      tet_rinv(c, t, Ri);
+      // tet_forward_uv, first half: du, L, G
+      double du[9];
+#pragma unroll
+      for (int v = 1; v < 4; ++v)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) du[3 * (v - 1) + a] = uv[3 * v + a] - uv[a];
+      double L[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          L[3 * a + j] = dot3(du[a], Ri[j], du[3 + a], Ri[3 + j], du[6 + a], Ri[6 + j]);
+      double R[9];
+      quat_to_mat(q[0], q[1], q[2], q[3], R);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          g[(3 * i + j) * 32] = dot3(R[i], L[j], R[3 + i], L[3 + j], R[6 + i], L[6 + j]);
+      named_bar(1 + pair, 64);
+    } else {
+      double sv[6], zz[6];
+      const double* sp = c.K.tS + tb;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sv[k] = sp[k * ntE];
+      const double* zp = z + ((unsigned)c.D.ot * uE + tb);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) zz[i] = zp[i * ntE];
+      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
+      double S[9], Ki[9];
+      S[0] = sv[0]; S[4] = sv[1]; S[8] = sv[2];
+      S[5] = sv[3]; S[7] = sv[3];
+      S[2] = sv[4]; S[6] = sv[4];
+      S[1] = sv[5]; S[3] = sv[5];
+      tet_kinv(S, Ki);
+      named_bar(1 + pair, 64);
+      double G[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) G[k] = g[k * 32];
+      // tet_forward_uv, second half
+      const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
+      const double w0 = dot3(Ki[0], g0, Ki[1], g1, Ki[2], g2);
+      const double w1 = dot3(Ki[3], g0, Ki[4], g1, Ki[5], g2);
+      const double w2 = dot3(Ki[6], g0, Ki[7], g1, Ki[8], g2);
+      const double ws00 = __fma_rn(w1, S[6], -w2 * S[3]);
+      const double ws01 = __fma_rn(w1, S[7], -w2 * S[4]);
+      const double ws02 = __fma_rn(w1, S[8], -w2 * S[5]);
+      const double ws10 = __fma_rn(w2, S[0], -w0 * S[6]);
+      const double ws11 = __fma_rn(w2, S[1], -w0 * S[7]);
+      const double ws12 = __fma_rn(w2, S[2], -w0 * S[8]);
+      const double ws20 = __fma_rn(w0, S[3], -w1 * S[0]);
+      const double ws21 = __fma_rn(w0, S[4], -w1 * S[1]);
+      const double ws22 = __fma_rn(w0, S[5], -w1 * S[2]);
+      double y[6], ez[6];
+      y[0] = G[0] - ws00;
+      y[1] = G[4] - ws11;
+      y[2] = G[8] - ws22;
+      y[3] = 0.5 * ((G[5] + G[7]) - (ws12 + ws21));
+      y[4] = 0.5 * ((G[2] + G[6]) - (ws02 + ws20));
+      y[5] = 0.5 * ((G[1] + G[3]) - (ws01 + ws10));
+      ereg6(ed, eo, es, zz, ez);
+      double* ap = c.K.az + ((unsigned)c.D.ot * uE + tb);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double az = y[i] + ez[i];
+        ap[i * ntE] = az;
+        part += zz[i] * az;
+      }
+    }
+    buf ^= 1;
+  }
+  // ---- every other item (distance, attachment, hinge, contact slot rows)
+  const int n_other = nd + na + nh + ns;
+  for (int q2 = blockIdx.y * IL + il; q2 < n_other; q2 += gridDim.y * IL) {
+    int it = q2 < nd ? q2 : q2 + nt;
+    if (it < nd) {
+      const int row = c.D.od + it;
+      const double zr = z[IX(row)];
+      const double az = row_dist(c, it, u, env) + c.T.d_dyn[it] * zr;
+      c.K.az[IX(row)] = az;
+      part += zr * az;
+    } else if (it < nd + nt + na) {
+      const int a = it - nd - nt;
+      double y[3];
+      rows_att(c, a, u, env, y);
+      const double dyn = c.T.a_dyn[a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int row = c.D.oa + i * na + a;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else if (it < nd + nt + na + nh) {
+      const int hh = it - nd - nt - na;
+      double y[5];
+      rows_hinge(c, hh, u, env, y);
+      const double dyn = c.T.h_dyn[hh];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int row = c.D.oh + i * nh + hh;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else {
+      const int s = it - nd - nt - na - nh;
+      if (!c.K.present[IX(s)]) continue;
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+      const double zn = z[IX(rn)], z0 = z[IX(rf0)], z1 = z[IX(rf1)];
+      double y[3];
+      rows_slot(c, s, u, env, y);
+      const double an = y[0] + c.K.dynn[IX(s)] * zn;
+      double a0 = z0, a1 = z1;
+      if (c.K.actf[IX(s)] != 0.0) {
+        a0 = y[1] + c.p.fdyn * z0;
+        a1 = y[2] + c.p.fdyn * z1;
+      }
+      c.K.az[IX(rn)] = an;
+      c.K.az[IX(rf0)] = a0;
+      c.K.az[IX(rf1)] = a1;
+      part += zn * an;
+      part += z0 * a0;
+      part += z1 * a1;
+    }
+  }
   double tot;
   if (reduce_env(c, part, &tot)) {
     if (setup) {

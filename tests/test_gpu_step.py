@@ -397,3 +397,36 @@ def test_jtg_bitwise(n, ring, lag):
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("n", [64, 96])
+def test_apply2_matches_apply(n):
+    """k_apply_rows2 (each tet split over two warps) against k_apply_rows:
+    every az is the same expression; only the rho partials are summed over
+    another thread assignment (three frames apart at rounding level)."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(17)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_APPLY2"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_APPLY2", None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_apply_rows2"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k, tol in (("positions", 1e-9), ("velocities", 1e-7), ("lam_tetra", 1e-7),
+                   ("pressures", 0.0), ("tet_quats", 1e-9)):
+        a, b = out["0"][k], out["1"][k]
+        scale = max(float(np.max(np.abs(a))), 1e-30)
+        assert np.max(np.abs(a - b)) <= tol * scale, k
