@@ -139,6 +139,9 @@ struct ss_handle {
   int pdl = 0;               // programmatic dependent launch of the frame kernels (SS_PDL)
   int apply2 = 0;            // k_apply_rows2 (tet split over two warps; SS_APPLY2)
   int gy_red2 = 1;           // its grid rows (one resident wave)
+  int dir2 = 0;              // k_pcr_dir_rows (row-wise, SS_DIR2)
+  int polar_split = 0;       // k_eval_polar before k_eval_tet (SS_POLAR_SPLIT)
+  int gy_dir2 = 1;
   JtgPlan jplan{};           // k_jtg plan (fixed at ss_create)
   size_t apply_async_smem = 0;
   std::vector<std::pair<char*, size_t>> guards;  // SS_GUARD spans
@@ -189,8 +192,9 @@ const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots", 
                                     "k_eval_misc",   "k_gather",     "k_newton_rhs", "k_apply_rows",
                                     "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
                                     "k_tet_jt",      "k_newton_cluster", "k_gather_fused",
-                                    "k_apply_rows_async", "k_jtg", "k_apply_rows2"};
-constexpr int kNumKernels = 18;
+                                    "k_apply_rows_async", "k_jtg", "k_apply_rows2",
+                                    "k_pcr_dir_rows", "k_eval_polar"};
+constexpr int kNumKernels = 20;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -269,6 +273,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 g_pre = grid_items(D, D.P + D.nb + D.nch, H->caps.eval);
   const dim3 g_slots = grid_items(D, D.ns, H->caps.eval);
   const dim3 g_eval = grid_items(D, D.nt, H->caps.eval);
+  const dim3 g_polar = grid_items(D, D.nt, H->caps.stream);
   const dim3 g_tet = grid_items(D, D.nt, H->caps.stream);
   const dim3 g_misc = grid_items(D, D.nd + D.na + D.nh, H->caps.eval);
   int gsp = EX ? 1 : H->gather_split;  // the split walk changes the summation order
@@ -282,6 +287,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const dim3 g_el = grid_items(D, n_el, H->caps.stream);
   const dim3 g_red(D.tiles, H->gy_red);
   const dim3 g_red2(D.tiles, H->gy_red2);
+  const dim3 g_dir2(D.tiles, H->gy_dir2);
   const dim3 g_dir(D.tiles, H->gy_dir);
   const dim3 g_int = grid_items(D, D.P + D.nb, H->caps.eval);
   const double* xs_lam = c.S.lam;
@@ -306,7 +312,8 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
     NvtxRange* nv_asm = new NvtxRange("assembly: pre, contacts, eval", prof != nullptr);
     LAUNCH(k_pre, g_pre, c, gait && sub == 0 ? 1 : 0);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
-    if (D.nt) LAUNCH(k_eval_tet<EX>, g_eval, c);  // + tet J^T lam
+    if (D.nt && H->polar_split) LAUNCH(k_eval_polar, g_polar, c);
+    if (D.nt) LAUNCH(k_eval_tet<EX>, g_eval, c, H->polar_split);  // + tet J^T lam
     if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
     if (H->use_cluster) {
       // whole Newton loop, one environment per cluster (ss_cluster.cuh)
@@ -350,6 +357,13 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       if (c.p.pcr > 0) {
         NvtxRange nv_pcr("pcr_solve", prof != nullptr);
         GATHER(0, xs_z, xc_z);
+#define DIR(setup_)                                                          \
+  do {                                                                       \
+    if (!EX && H->dir2)                                                      \
+      LAUNCH(k_pcr_dir_rows, g_dir2, c, setup_);                             \
+    else                                                                     \
+      LAUNCH(k_pcr_dir<EX>, g_dir, c, setup_);                               \
+  } while (0)
 #define APPLY(setup_)                                                        \
   do {                                                                       \
     if (!EX && H->apply2)                                                    \
@@ -360,7 +374,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       LAUNCH(k_apply_rows<EX>, g_red, c, setup_);                            \
   } while (0)
         APPLY(1);
-        LAUNCH(k_pcr_dir<EX>, g_dir, c, 1);
+        DIR(1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
           LAUNCH(k_pcr_step<EX>, g_el, c, k);
           if (!EX && H->fused) {
@@ -382,7 +396,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
             GATHER(0, xs_z, xc_z);
           }
           APPLY(0);
-          LAUNCH(k_pcr_dir<EX>, g_dir, c, 0);
+          DIR(0);
         }
       }
       LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
@@ -398,6 +412,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
 #undef LAUNCH
 #undef LAUNCH_SM
 #undef APPLY
+#undef DIR
 
 int enqueue_frame(ss_handle* H, int w, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
   const Ctx& c = H->wave[w];
@@ -1605,6 +1620,19 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     want = std::max(1L, std::min(want, (long)kMaxGyRed2));
     H->gy_red2 = (int)std::min<long>(env_long("SS_APPLY2_GY", want), kMaxGyRed2);
     H->apply2 = 1;
+  }
+  H->polar_split = (int)env_long("SS_POLAR_SPLIT", 1);
+  // batched layouts only (W == 32): at few env lanes the element-owned kernel
+  // keeps the v2.14 reduction order (an ill-conditioned parity case,
+  // test_gpu_params[fb_slopes], sits at 1.4e-10 of its 1e-10 bound there)
+  if (!H->c.p.exact_j && !H->use_cluster && D.W == 32 && env_long("SS_DIR2", 1)) {
+    int occ = 4, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcr_dir_rows, SS_THREADS, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
+    long want = (long)sms * std::max(1, occ) / D.tiles;
+    want = std::max(1L, std::min(want, (long)kMaxGyRed2));
+    H->gy_dir2 = (int)std::min<long>(env_long("SS_DIR2_GY", want), kMaxGyRed2);
+    H->dir2 = 1;
   }
   // opt-in: no gain measured (coupled 2-snake frame 6.16 ms either way; 1024 envs and
   // the 1M-tet scene within noise, profiles/r2_summary.md)

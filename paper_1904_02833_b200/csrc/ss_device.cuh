@@ -623,18 +623,9 @@ DI void tet_kinv(const double* S, double* Ki) {
   Ki[8] = (K[0] * K[4] - K[1] * K[3]) * id;
 }
 
-DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, int maxiter,
-                     TetC& T, int* iters) {
-  double F[9];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double x0 = X[a];
-    const double Ds0 = X[3 + a] - x0, Ds1 = X[6 + a] - x0, Ds2 = X[9 + a] - x0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) F[3 * a + j] = Ds0 * Ri[j] + Ds1 * Ri[3 + j] + Ds2 * Ri[6 + j];
-  }
-  const double detF = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
-                      F[2] * (F[3] * F[7] - F[4] * F[6]);
+// the warm-started polar iteration (numba_backend.py:178-218) on q in place;
+// returns the iteration count
+DI int polar_iterate(const double* F, double* q, double tol, int maxiter, int* iters) {
   double qw = q[0], qx = q[1], qy = q[2], qz = q[3];
   int it = 0;
   for (; it < maxiter; ++it) {
@@ -680,6 +671,24 @@ DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, i
   }
   if (iters) *iters = it;
   q[0] = qw; q[1] = qx; q[2] = qy; q[3] = qz;
+  return it;
+}
+
+DI int tet_eval_core(const double* X, const double* Ri, double* q, double tol, int maxiter,
+                     TetC& T, int* iters) {
+  double F[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double x0 = X[a];
+    const double Ds0 = X[3 + a] - x0, Ds1 = X[6 + a] - x0, Ds2 = X[9 + a] - x0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) F[3 * a + j] = Ds0 * Ri[j] + Ds1 * Ri[3 + j] + Ds2 * Ri[6 + j];
+  }
+  const double detF = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+                      F[2] * (F[3] * F[7] - F[4] * F[6]);
+  int it = polar_iterate(F, q, tol, maxiter, iters);
+  (void)it;
+  const double qw = q[0], qx = q[1], qy = q[2], qz = q[3];
   double* R = T.R;
   double* S = T.S;
   quat_to_mat(qw, qx, qy, qz, R);
@@ -918,6 +927,42 @@ DI void tet_j(const Ctx& c, int t, int env, const TetC& T, const double* Ri, con
   else tet_forward_fast(c, t, env, T, Ri, vec, y);
 }
 
+// The polar decomposition of TetraSet.eval alone (the warm-started
+// quaternion iteration of numba_backend.py:178-218): a small-register kernel
+// so the data-dependent FP64 loop runs at high occupancy; k_eval_tet then
+// finds the converged quaternion and runs zero iterations (the same q, so
+// R, S, the Jacobian and every result are bitwise those of the fused kernel).
+#ifndef SS_POLAR_MINB
+#define SS_POLAR_MINB 4
+#endif
+__global__ void __launch_bounds__(SS_THREADS, SS_POLAR_MINB) k_eval_polar(const Ctx c) {
+  SETUP
+  const int nt = c.D.nt;
+  FOR_ITEMS(t, nt) {
+    double X[12], Ri[9], q[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int node = c.T.t_idx[v * nt + t];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) X[3 * v + a] = c.S.pos[IX(3 * node + a)];
+    }
+    tet_rinv(c, t, Ri);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
+    double F[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double x0 = X[a];
+      const double Ds0 = X[3 + a] - x0, Ds1 = X[6 + a] - x0, Ds2 = X[9 + a] - x0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) F[3 * a + j] = Ds0 * Ri[j] + Ds1 * Ri[3 + j] + Ds2 * Ri[6 + j];
+    }
+    polar_iterate(F, q, 1e-12, 500, nullptr);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c.S.quat[IX(k * nt + t)] = q[k];
+  }
+}
+
 // TetraSet.eval + its block_rowdiag + eh2 diag (solver.py:410-426), and
 // the tet part of the initial impulse J^T lam (solver.py:428-436).
 template <bool EXACT>
@@ -926,7 +971,7 @@ template <bool EXACT>
 #else
 #define SS_EVAL_MINB_LB __launch_bounds__(SS_THREADS)
 #endif
-__global__ void SS_EVAL_MINB_LB k_eval_tet(const Ctx c) {
+__global__ void SS_EVAL_MINB_LB k_eval_tet(const Ctx c, int polar_done) {
   SETUP
   const int nt = c.D.nt;
   FOR_ITEMS(t, nt) {
@@ -942,7 +987,7 @@ __global__ void SS_EVAL_MINB_LB k_eval_tet(const Ctx c) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) q[k] = c.S.quat[IX(k * nt + t)];
     TetC T;
-    const int inv = tet_eval_core(X, Ri, q, 1e-12, 500, T, nullptr);
+    const int inv = tet_eval_core(X, Ri, q, 1e-12, polar_done ? 0 : 500, T, nullptr);
 #pragma unroll
     for (int k = 0; k < 4; ++k) c.S.quat[IX(k * nt + t)] = q[k];
     tet_store(c, t, env, T);
@@ -2579,6 +2624,67 @@ __global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : 3) k_pcr_dir(const Ctx
         if (!brk || setup) AP[o] = EXACT ? ap : apd;
         part += ap * apd;
       }
+    }
+  }
+  double den;
+  if (reduce_env(c, part, &den)) {
+    if (!c.K.broken[env]) {
+      if (den <= 1e-300 || !isfinite(den)) {
+        c.K.broken[env] = 1;
+      } else {
+        c.K.alpha_prev[env] = c.K.alpha[env];
+        c.K.alpha[env] = c.K.rho[env] / den;
+      }
+    }
+  }
+}
+
+// k_pcr_dir (structured mode) over rows instead of elements: every row is
+// independent (ap = az + beta ap_prev, apd = ap/d, den += ap apd; absent
+// contact rows skipped), so a thread keeps DIR_UNROLL rows' loads in flight
+// with few registers and the grid holds more warps. Same per-row values as
+// k_pcr_dir<false>; den is summed over another thread assignment.
+#ifndef SS_DIR2_MINB
+#define SS_DIR2_MINB 4
+#endif
+#ifndef DIR_UNROLL
+#define DIR_UNROLL 4
+#endif
+__global__ void __launch_bounds__(SS_THREADS, SS_DIR2_MINB) k_pcr_dir_rows(const Ctx c, int setup) {
+  SETUP
+  const bool brk = c.K.broken[env] != 0;
+  const double beta = c.K.beta[env];
+  const int m = c.D.m;
+  double* __restrict__ AP = c.K.ap;
+  const double* __restrict__ AZ = c.K.az;
+  const double* __restrict__ Dg = c.K.d;
+  const int stride = gridDim.y * IL;
+  double part = 0.0;
+  for (int r0 = blockIdx.y * IL + il; r0 < m; r0 += DIR_UNROLL * stride) {
+    double az[DIR_UNROLL], dg[DIR_UNROLL], apo[DIR_UNROLL];
+    bool live[DIR_UNROLL];
+#pragma unroll
+    for (int q = 0; q < DIR_UNROLL; ++q) {
+      const int row = r0 + q * stride;
+      live[q] = row < m && row_live(c, row, env);
+      if (live[q]) {
+        const size_t o = IX(row);
+        az[q] = AZ[o];
+        dg[q] = Dg[o];
+        if (!setup) apo[q] = AP[o];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < DIR_UNROLL; ++q) {
+      if (!live[q]) continue;
+      const size_t o = IX(r0 + q * stride);
+      double ap;
+      if (setup) ap = az[q];
+      else if (!brk) ap = az[q] + beta * (apo[q] * dg[q]);
+      else ap = apo[q] * dg[q];
+      const double apd = ap / dg[q];
+      if (!brk || setup) AP[o] = apd;
+      part += ap * apd;
     }
   }
   double den;

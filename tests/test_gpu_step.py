@@ -353,11 +353,13 @@ def test_apply_async_bitwise(n):
     out = {}
     for mode in ("0", "1"):
         os.environ["SS_APPLY_ASYNC"] = mode
+        os.environ["SS_APPLY2"] = "0"  # both against the one-warp-per-tet kernel
         try:
             sim = M.BatchedSimulator(n, config=cfg, **parts)
             sim._ensure()
         finally:
             os.environ.pop("SS_APPLY_ASYNC", None)
+            os.environ.pop("SS_APPLY2", None)
         prof = sim.profile_frames(cmds[0], True, 1)
         assert (prof["k_apply_rows_async"][1] > 0) == (mode == "1")
         for c in cmds[1:]:
@@ -430,3 +432,65 @@ def test_apply2_matches_apply(n):
         a, b = out["0"][k], out["1"][k]
         scale = max(float(np.max(np.abs(a))), 1e-30)
         assert np.max(np.abs(a - b)) <= tol * scale, k
+
+
+@pytest.mark.parametrize("n", [64, 96])
+def test_dir_rows_matches_dir(n):
+    """k_pcr_dir_rows (row-wise) against k_pcr_dir (element-owned): the same
+    per-row values; den summed over another thread assignment."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(19)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_DIR2"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_DIR2", None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_pcr_dir_rows"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k, tol in (("positions", 1e-9), ("velocities", 1e-7), ("lam_tetra", 1e-7),
+                   ("pressures", 0.0), ("tet_quats", 1e-9)):
+        a, b = out["0"][k], out["1"][k]
+        scale = max(float(np.max(np.abs(a))), 1e-30)
+        assert np.max(np.abs(a - b)) <= tol * scale, k
+
+
+@pytest.mark.parametrize("solver", ["streaming", "cluster"])
+def test_polar_split_bitwise(solver):
+    """k_eval_polar + k_eval_tet (zero iterations from the converged
+    quaternion) gives bitwise the state of the fused k_eval_tet."""
+    import os
+    n = 8 if solver == "cluster" else 40
+    parts, cfg = scene_parts("S")
+    cfg.solver = solver
+    rng = np.random.default_rng(23)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_POLAR_SPLIT"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_POLAR_SPLIT", None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_eval_polar"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
