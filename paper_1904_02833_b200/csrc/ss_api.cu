@@ -141,6 +141,7 @@ struct ss_handle {
   int gy_red2 = 1;           // its grid rows (one resident wave)
   int dir2 = 0;              // k_pcr_dir_rows (row-wise, SS_DIR2)
   int polar_split = 0;       // k_eval_polar before k_eval_tet (SS_POLAR_SPLIT)
+  int stepjt = 0;            // k_step_jt (step + tet J^T z in one pass; SS_STEPJT)
   int gy_dir2 = 1;
   JtgPlan jplan{};           // k_jtg plan (fixed at ss_create)
   size_t apply_async_smem = 0;
@@ -193,8 +194,8 @@ const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots", 
                                     "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
                                     "k_tet_jt",      "k_newton_cluster", "k_gather_fused",
                                     "k_apply_rows_async", "k_jtg", "k_apply_rows2",
-                                    "k_pcr_dir_rows", "k_eval_polar"};
-constexpr int kNumKernels = 20;
+                                    "k_pcr_dir_rows", "k_eval_polar", "k_step_jt"};
+constexpr int kNumKernels = 21;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -376,6 +377,11 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
         APPLY(1);
         DIR(1);
         for (int k = 0; k + 1 < c.p.pcr; ++k) {
+          if (!EX && H->stepjt) {
+            // step + tet column sums in one pass, then the DOF gather
+            LAUNCH(k_step_jt, g_el, c, k);
+            GATHER(0, xs_z, xc_z);
+          } else {
           LAUNCH(k_pcr_step<EX>, g_el, c, k);
           if (!EX && H->fused) {
             const dim3 g_fu(D.E / H->fplan.FW, H->fplan.n_blocks + 1);
@@ -394,6 +400,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
           } else {
             if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
             GATHER(0, xs_z, xc_z);
+          }
           }
           APPLY(0);
           DIR(0);
@@ -1622,6 +1629,11 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     H->apply2 = 1;
   }
   H->polar_split = (int)env_long("SS_POLAR_SPLIT", 1);
+  // opt-in: bitwise equal but 60-68 ms/frame against 58.5 for k_pcr_step +
+  // k_tet_jt (the separate kernels run at 0.95 / 0.91 of HBM; the fused one
+  // loses the step's occupancy to the tet math)
+  H->stepjt = (!H->c.p.exact_j && !H->use_cluster && D.nt > 0 && D.W == 32 &&
+               env_long("SS_STEPJT", 0)) ? 1 : 0;
   // batched layouts only (W == 32): at few env lanes the element-owned kernel
   // keeps the v2.14 reduction order (an ill-conditioned parity case,
   // test_gpu_params[fb_slopes], sits at 1.4e-10 of its 1e-10 bound there)

@@ -142,7 +142,14 @@ DI void pdl_wait() {
 #define IX(item) ((size_t)(item) * E + env)
 // tet column sums tC: [12][nt][E] (a [nt][12] layout for E = 1 was tried:
 // the gather did not speed up and the strided writes cost k_tet_jt 35%)
+#ifndef SS_TC_COMPMAJOR
+// [nt][12][E]: a tet's 12 column sums are 12 consecutive env rows (k_tet_jt
+// writes, and the gather reads, contiguous 3 KB runs per tet at E = 32;
+// 0.5 ms/frame faster than [12][nt][E] at 1024 envs)
+#define TCX(k, t) (((size_t)(t) * 12 + (k)) * E + env)
+#else
 #define TCX(k, t) (((size_t)(k) * nt + (t)) * E + env)
+#endif
 
 // ------------------------------------------------------------ small math
 // numpy.maximum: NaN in a propagates
@@ -2765,6 +2772,109 @@ __global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : SS_STEP_MINB) k_pcr_st
           if (upd_x) X_[o] = (xr[q] + alpha_prev * pr[q]) + alpha * pn;
           Z_[o] = rr[q] - alpha * apr[q];
         }
+      }
+    }
+  }
+}
+
+// k_pcr_step + k_tet_jt in one pass (structured mode, E >= 32): a tet's 6
+// rows are stepped by warp A (x, p, z, ap/d in; x, p, z out), which hands the
+// new z to warp B through shared memory (named barrier per warp pair, double
+// buffered); B loads the quaternion, S and the rest-shape inverse and writes
+// the tet's 12 column sums of J^T z. The same operations as the two kernels
+// (bitwise the same x, p, z and tC), without re-reading the tet rows of z and
+// with one launch fewer per PCR iteration. Broken envs skip every store (the
+// reference skips the whole iteration; tC keeps the previous pass).
+#ifndef SS_STEPJT_MINB
+#define SS_STEPJT_MINB 3
+#endif
+__global__ void __launch_bounds__(SS_THREADS, SS_STEPJT_MINB) k_step_jt(const Ctx c, int k) {
+  SETUP
+  __shared__ double zsh[4][2][6][32];  // [pair][buffer][row][env lane]
+  const bool brk = c.K.broken[env] != 0;
+  const bool first = k == 0;
+  const bool upd_x = (k & 1) != 0;
+  const double alpha = c.K.alpha[env];
+  const double beta = c.K.beta[env];
+  const double alpha_prev = c.K.alpha_prev[env];
+  if (!brk && blockIdx.y == 0 && il == 0) c.K.last_step[env] = k;
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  double* __restrict__ X_ = c.K.x;
+  double* __restrict__ Z_ = c.K.z;
+  double* __restrict__ P_ = c.K.p;
+  const double* __restrict__ AP = c.K.ap;
+  const int pair = il >> 1, role = il & 1;
+  const unsigned uE = (unsigned)E;
+  const unsigned ntE = (unsigned)nt * uE;
+  int buf = 0;
+  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += gridDim.y * (IL >> 1)) {
+    double* zs = &zsh[pair][buf][0][lane];
+    if (role == 0) {
+      const unsigned ob = (unsigned)c.D.ot * uE + (unsigned)t * uE + (unsigned)env;
+      double xr[6], pr[6], rr[6], apr[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const unsigned o = ob + q * ntE;
+        if (upd_x) xr[q] = X_[o];
+        if (!first) pr[q] = P_[o];
+        rr[q] = Z_[o];
+        apr[q] = AP[o];
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const unsigned o = ob + q * ntE;
+        const double pn = first ? rr[q] : rr[q] + beta * pr[q];
+        const double zn = rr[q] - alpha * apr[q];
+        if (!brk) {
+          P_[o] = pn;
+          if (upd_x) X_[o] = (xr[q] + alpha_prev * pr[q]) + alpha * pn;
+          Z_[o] = zn;
+        }
+        zs[q * 32] = zn;
+      }
+      named_bar(1 + pair, 64);
+    } else {
+      TetC T;
+      double Ri[9];
+      tet_load(c, t, env, T);
+      tet_rinv(c, t, Ri);
+      named_bar(1 + pair, 64);
+      if (!brk) {
+        double z6[6], col12[12];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) z6[q] = zs[q * 32];
+        tet_jt_cols(T, Ri, z6, col12);
+#pragma unroll
+        for (int kk = 0; kk < 12; ++kk) c.K.tC[TCX(kk, t)] = col12[kk];
+      }
+    }
+    buf ^= 1;
+  }
+  if (brk) return;  // after the last named barrier of this thread's pair
+  const int n_other = nd + na + nh + ns;
+  for (int q2 = blockIdx.y * IL + il; q2 < n_other; q2 += gridDim.y * IL) {
+    const int it = q2 < nd ? q2 : q2 + nt;
+    int rows[6];
+    const int nr = item_rows(c, it, env, rows);
+    double xr[6], pr[6], rr[6], apr[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q < nr) {
+        const size_t o = IX(rows[q]);
+        if (upd_x) xr[q] = X_[o];
+        if (!first) pr[q] = P_[o];
+        rr[q] = Z_[o];
+        apr[q] = AP[o];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q < nr) {
+        const size_t o = IX(rows[q]);
+        const double pn = first ? rr[q] : rr[q] + beta * pr[q];
+        P_[o] = pn;
+        if (upd_x) X_[o] = (xr[q] + alpha_prev * pr[q]) + alpha * pn;
+        Z_[o] = rr[q] - alpha * apr[q];
       }
     }
   }

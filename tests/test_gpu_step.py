@@ -494,3 +494,32 @@ def test_polar_split_bitwise(solver):
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("n", [64, 96])
+def test_step_jt_bitwise(n):
+    """k_step_jt (step + tet column sums in one pass) gives bitwise the state
+    of k_pcr_step + k_tet_jt."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(29)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_STEPJT"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_STEPJT", None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_step_jt"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
