@@ -142,6 +142,7 @@ struct ss_handle {
   int dir2 = 0;              // k_pcr_dir_rows (row-wise, SS_DIR2)
   int polar_split = 0;       // k_eval_polar before k_eval_tet (SS_POLAR_SPLIT)
   int stepjt = 0;            // k_step_jt (step + tet J^T z in one pass; SS_STEPJT)
+  int newton2 = 0;           // k_newton_rhs2 / k_newton_final2 (SS_NEWTON2)
   int gy_dir2 = 1;
   JtgPlan jplan{};           // k_jtg plan (fixed at ss_create)
   size_t apply_async_smem = 0;
@@ -194,8 +195,9 @@ const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots", 
                                     "k_pcr_dir",     "k_pcr_step",   "k_newton_final", "k_integrate",
                                     "k_tet_jt",      "k_newton_cluster", "k_gather_fused",
                                     "k_apply_rows_async", "k_jtg", "k_apply_rows2",
-                                    "k_pcr_dir_rows", "k_eval_polar", "k_step_jt"};
-constexpr int kNumKernels = 21;
+                                    "k_pcr_dir_rows", "k_eval_polar", "k_step_jt",
+                                    "k_newton_rhs2", "k_newton_final2"};
+constexpr int kNumKernels = 23;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -351,7 +353,8 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
     nv_asm = nullptr;
     for (int it = 0; it < c.p.newton; ++it) {
       NvtxRange nv_newton("newton", prof != nullptr);
-      LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
+      if (!EX && H->newton2) LAUNCH(k_newton_rhs2, g_el, c);
+      else LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
       if (H->keep && sub == c.p.substeps - 1 && it == c.p.newton - 1)
         CK(cudaMemcpyAsync(c.K.snap_rhs, c.K.r, 8 * (size_t)D.m * D.E, cudaMemcpyDeviceToDevice,
                            st));  // the snapshot's rhs (solver.py:515)
@@ -406,8 +409,12 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
           DIR(0);
         }
       }
-      LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
-             c.p.pcr == 1 ? 1 : 0);
+      if (!EX && H->newton2)
+        LAUNCH(k_newton_final2, g_red2, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
+               c.p.pcr == 1 ? 1 : 0);
+      else
+        LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
+               c.p.pcr == 1 ? 1 : 0);
       GATHER(1, xs_dl, xc_dl);  // v += M^-1 J^T dlam
     }
     LAUNCH(k_integrate, g_int, c);
@@ -1629,6 +1636,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     H->apply2 = 1;
   }
   H->polar_split = (int)env_long("SS_POLAR_SPLIT", 1);
+  H->newton2 = (H->apply2 && env_long("SS_NEWTON2", 1)) ? 1 : 0;  // needs g_red2 (apply2 plan)
   // opt-in: bitwise equal but 60-68 ms/frame against 58.5 for k_pcr_step +
   // k_tet_jt (the separate kernels run at 0.95 / 0.91 of HBM; the fused one
   // loses the step's occupancy to the tet math)

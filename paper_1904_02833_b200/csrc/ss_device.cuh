@@ -1940,6 +1940,109 @@ DI int item_rows(const Ctx& c, int it, int env, int* rows) {
   return 3;
 }
 
+// one item of the Newton head (k_newton_rhs): jv = J v, rhs, FB, active
+// set, diagonal, z = r/d, x = 0, and the tet column sums of J^T z
+template <bool EXACT>
+DI void rhs_item(const Ctx& c, int it, int env) {
+  const int E = c.D.E;
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const double g = c.p.gamma, h = c.p.h;
+  const double* v = c.K.v;
+#define SETROW(row, rhsv, diagv)                            \
+  {                                                         \
+    const double dg_ = (diagv);                             \
+    const double d_ = dg_ > 1e-300 ? dg_ : 1.0;             \
+    const double r_ = (rhsv);                               \
+    c.K.r[IX(row)] = r_;                                    \
+    c.K.d[IX(row)] = d_;                                    \
+    c.K.z[IX(row)] = r_ / d_;                               \
+    c.K.x[IX(row)] = 0.0;                                   \
+  }
+  if (it < nd) {
+    const int row = c.D.od + it;
+    const double jv = row_dist(c, it, v, env);
+    const double dyn = c.T.d_dyn[it];
+    SETROW(row, -(g * c.K.res[IX(row)] / h + jv + dyn * c.S.lam[IX(row)]),
+           npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
+  } else if (it < nd + nt) {
+    const int t = it - nd;
+    TetC T;
+    double Ri[9], jv[6], lm[6], el[6], rs[6], z6[6];
+    tet_load(c, t, env, T);
+    tet_rinv(c, t, Ri);
+    tet_j<EXACT>(c, t, env, T, Ri, v, jv);
+    tet_res(T, rs);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
+    ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], lm, el);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const int row = c.D.ot + i * nt + t;
+      const double dg = npmax(c.K.bdiag[IX(row)] + 0.0, 1e-30);
+      const double d = dg > 1e-300 ? dg : 1.0;
+      const double r = -(g * rs[i] / h + jv[i] + el[i]);
+      z6[i] = r / d;
+      c.K.r[IX(row)] = r;
+      c.K.d[IX(row)] = d;
+      c.K.z[IX(row)] = z6[i];
+      c.K.x[IX(row)] = 0.0;
+    }
+    tet_jt<EXACT>(c, t, env, T, Ri, z6);
+  } else if (it < nd + nt + na) {
+    const int a = it - nd - nt;
+    double jv[3];
+    rows_att(c, a, v, env, jv);
+    const double dyn = c.T.a_dyn[a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int row = c.D.oa + i * na + a;
+      SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + dyn * c.S.lam[IX(row)]),
+             npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
+    }
+  } else if (it < nd + nt + na + nh) {
+    const int hh = it - nd - nt - na;
+    double jv[5];
+    rows_hinge(c, hh, v, env, jv);
+    const double dyn = c.T.h_dyn[hh];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int row = c.D.oh + i * nh + hh;
+      SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + dyn * c.S.lam[IX(row)]),
+             npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
+    }
+  } else {
+    const int s = it - nd - nt - na - nh;
+    if (!c.K.present[IX(s)]) {
+      c.K.actf[IX(s)] = 0.0;
+      return;
+    }
+    const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+    double jv[3];
+    rows_slot(c, s, v, env, jv);
+    const double ln = c.K.lamc[IX(s)];
+    const double a = c.K.gap[IX(s)] / h + jv[0];
+    const double b = ln;
+    const double root = sqrt(a * a + b * b + c.p.fb_delta);
+    const double phi = a + b - root;
+    double da = 1.0 - a / root;
+    const double db = 1.0 - b / root;
+    if (da < c.p.smin) da = c.p.smin;
+    else if (da > c.p.smax) da = c.p.smax;
+    const double dynn = db / da;
+    c.K.dynn[IX(s)] = dynn;
+    SETROW(rn, -phi / da, npmax(c.K.bdiag[IX(rn)] + dynn, 1e-30));
+    const double on = (c.p.mu * npmax(ln, 0.0) > 0.0) ? 1.0 : 0.0;
+    c.K.actf[IX(s)] = on;
+    const double fd = c.p.fdyn;
+    const double lf0 = c.K.lamc[IX(ns + s)], lf1 = c.K.lamc[IX(2 * ns + s)];
+    SETROW(rf0, -on * (jv[1] + fd * lf0),
+           on > 0.0 ? npmax(c.K.bdiag[IX(rf0)] + fd, 1e-30) : 1.0);
+    SETROW(rf1, -on * (jv[2] + fd * lf1),
+           on > 0.0 ? npmax(c.K.bdiag[IX(rf1)] + fd, 1e-30) : 1.0);
+  }
+#undef SETROW
+}
+
 // Newton head: jv = J v, velocity-level rhs, FB rows, friction active set,
 // Jacobi diagonal; PCR setup r = rhs, z = r/d, x = 0, and the tet column
 // sums of J^T z for the first apply (solver.py:439-478, 36-48, 62-70;
@@ -1955,106 +2058,15 @@ __global__ void SS_RHS_MINB_LB k_newton_rhs(const Ctx c) {
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
   const double g = c.p.gamma, h = c.p.h;
   const double* v = c.K.v;
-#define SETROW(row, rhsv, diagv)                            \
-  {                                                         \
-    const double dg_ = (diagv);                             \
-    const double d_ = dg_ > 1e-300 ? dg_ : 1.0;             \
-    const double r_ = (rhsv);                               \
-    c.K.r[IX(row)] = r_;                                    \
-    c.K.d[IX(row)] = d_;                                    \
-    c.K.z[IX(row)] = r_ / d_;                               \
-    c.K.x[IX(row)] = 0.0;                                   \
-  }
+  (void)g; (void)h; (void)v; (void)nd; (void)nt; (void)na; (void)nh; (void)ns;
   FOR_ITEMS(it, nd + nt + na + nh + ns) {
     if (it == 0) {
       c.K.broken[env] = 0;
       c.K.beta[env] = 0.0;
       c.K.last_step[env] = -1;
     }
-    if (it < nd) {
-      const int row = c.D.od + it;
-      const double jv = row_dist(c, it, v, env);
-      const double dyn = c.T.d_dyn[it];
-      SETROW(row, -(g * c.K.res[IX(row)] / h + jv + dyn * c.S.lam[IX(row)]),
-             npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
-    } else if (it < nd + nt) {
-      const int t = it - nd;
-      TetC T;
-      double Ri[9], jv[6], lm[6], el[6], rs[6], z6[6];
-      tet_load(c, t, env, T);
-      tet_rinv(c, t, Ri);
-      tet_j<EXACT>(c, t, env, T, Ri, v, jv);
-      tet_res(T, rs);
-#pragma unroll
-      for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[IX(c.D.ot + i * nt + t)];
-      ereg6(c.T.t_e3[t], c.T.t_e3[nt + t], c.T.t_e3[2 * nt + t], lm, el);
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        const int row = c.D.ot + i * nt + t;
-        const double dg = npmax(c.K.bdiag[IX(row)] + 0.0, 1e-30);
-        const double d = dg > 1e-300 ? dg : 1.0;
-        const double r = -(g * rs[i] / h + jv[i] + el[i]);
-        z6[i] = r / d;
-        c.K.r[IX(row)] = r;
-        c.K.d[IX(row)] = d;
-        c.K.z[IX(row)] = z6[i];
-        c.K.x[IX(row)] = 0.0;
-      }
-      tet_jt<EXACT>(c, t, env, T, Ri, z6);
-    } else if (it < nd + nt + na) {
-      const int a = it - nd - nt;
-      double jv[3];
-      rows_att(c, a, v, env, jv);
-      const double dyn = c.T.a_dyn[a];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int row = c.D.oa + i * na + a;
-        SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + dyn * c.S.lam[IX(row)]),
-               npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
-      }
-    } else if (it < nd + nt + na + nh) {
-      const int hh = it - nd - nt - na;
-      double jv[5];
-      rows_hinge(c, hh, v, env, jv);
-      const double dyn = c.T.h_dyn[hh];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        const int row = c.D.oh + i * nh + hh;
-        SETROW(row, -(g * c.K.res[IX(row)] / h + jv[i] + dyn * c.S.lam[IX(row)]),
-               npmax(c.K.bdiag[IX(row)] + dyn, 1e-30));
-      }
-    } else {
-      const int s = it - nd - nt - na - nh;
-      if (!c.K.present[IX(s)]) {
-        c.K.actf[IX(s)] = 0.0;
-        continue;
-      }
-      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
-      double jv[3];
-      rows_slot(c, s, v, env, jv);
-      const double ln = c.K.lamc[IX(s)];
-      const double a = c.K.gap[IX(s)] / h + jv[0];
-      const double b = ln;
-      const double root = sqrt(a * a + b * b + c.p.fb_delta);
-      const double phi = a + b - root;
-      double da = 1.0 - a / root;
-      const double db = 1.0 - b / root;
-      if (da < c.p.smin) da = c.p.smin;
-      else if (da > c.p.smax) da = c.p.smax;
-      const double dynn = db / da;
-      c.K.dynn[IX(s)] = dynn;
-      SETROW(rn, -phi / da, npmax(c.K.bdiag[IX(rn)] + dynn, 1e-30));
-      const double on = (c.p.mu * npmax(ln, 0.0) > 0.0) ? 1.0 : 0.0;
-      c.K.actf[IX(s)] = on;
-      const double fd = c.p.fdyn;
-      const double lf0 = c.K.lamc[IX(ns + s)], lf1 = c.K.lamc[IX(2 * ns + s)];
-      SETROW(rf0, -on * (jv[1] + fd * lf0),
-             on > 0.0 ? npmax(c.K.bdiag[IX(rf0)] + fd, 1e-30) : 1.0);
-      SETROW(rf1, -on * (jv[2] + fd * lf1),
-             on > 0.0 ? npmax(c.K.bdiag[IX(rf1)] + fd, 1e-30) : 1.0);
-    }
+    rhs_item<EXACT>(c, it, env);
   }
-#undef SETROW
 }
 
 // az = A z rows (apply_a second half, solver.py:388-399) + rho partial z.az.
@@ -2900,6 +2912,108 @@ __global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : SS_TETJT_MINB) k_tet_j
   }
 }
 
+// one item of the Newton tail (k_newton_final): the last PCR step of its
+// rows, lam += dl with the contact projection, dlam, the tet column sums of
+// J^T dlam; r.z of its rows added to part
+struct FinalArgs {
+  bool step, pend, first;
+  int last;
+  double alpha, beta, alpha_pend;
+};
+template <bool EXACT>
+DI void final_item(const Ctx& c, int it, int env, const FinalArgs& F, double& part) {
+  const int E = c.D.E;
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns, nw = c.D.nw;
+  (void)na;
+  const bool step = F.step, pend = F.pend, first = F.first;
+  const int last = F.last;
+  const double alpha = F.alpha, beta = F.beta, alpha_pend = F.alpha_pend;
+  int rows[6];
+  const int nr = item_rows(c, it, env, rows);
+  // one pass per row: only dl survives into the multiplier update (the
+  // two-pass load-all-then-compute form spilled the loaded rows at 128
+  // registers, and each spill store waited on its load)
+  double dl[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    if (q < nr) {
+      const size_t o = IX(rows[q]);
+      double x = c.K.x[o], z = c.K.z[o];
+      double r = EXACT ? c.K.r[o] : 0.0;
+      const double dq = (step || !EXACT) ? c.K.d[o] : 1.0;
+      const double po = (!EXACT && (pend || (step && !first))) ? c.K.p[o] : 0.0;
+      if (pend) x += alpha_pend * po;
+      if (step) {
+        double pq;
+        if (EXACT) pq = c.K.p[o];
+        else pq = first ? z : z + beta * po;  // the direction as k_pcr_step forms it
+        const double apq = c.K.ap[o];
+        x += alpha * pq;
+        if (EXACT) {
+          r -= alpha * apq;
+          z = r / dq;
+        } else {
+          z -= alpha * apq;  // the ap buffer holds ap/d (k_pcr_dir)
+        }
+      }
+      if (!EXACT) r = dq * z;  // structured mode keeps r = d z implicit
+      part += r * z;
+      dl[q] = x;
+    }
+  }
+  if (it < nd + nt + na + nh) {
+    double d6[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q >= nr) break;
+      const size_t o = IX(rows[q]);
+      const double l0 = c.S.lam[o];
+      const double l1 = l0 + dl[q];
+      c.S.lam[o] = l1;
+      d6[q] = l1 - l0;
+      c.K.az[o] = d6[q];
+    }
+    if (it >= nd && it < nd + nt) {
+      const int t = it - nd;
+      TetC T;
+      double Ri[9];
+      tet_load(c, t, env, T);
+      tet_rinv(c, t, Ri);
+      tet_jt<EXACT>(c, t, env, T, Ri, d6);
+    }
+  } else {
+    const int s = it - nd - nt - na - nh;
+    double n1 = 0.0, a1 = 0.0, b1 = 0.0;
+    if (nr) {
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+      const double n0 = c.K.lamc[IX(s)], a0 = c.K.lamc[IX(ns + s)], b0 = c.K.lamc[IX(2 * ns + s)];
+      n1 = n0 + dl[0];
+      a1 = a0 + dl[1];
+      b1 = b0 + dl[2];
+      n1 = npmax(n1, 0.0);
+      const double rad = c.p.mu * npmax(n1, 0.0);
+      const double nrm = sqrt(a1 * a1 + b1 * b1);
+      if (nrm > rad) {
+        const double sc = nrm > 0.0 ? rad / nrm : 0.0;
+        a1 *= sc;
+        b1 *= sc;
+      }
+      c.K.lamc[IX(s)] = n1;
+      c.K.lamc[IX(ns + s)] = a1;
+      c.K.lamc[IX(2 * ns + s)] = b1;
+      c.K.az[IX(rn)] = n1 - n0;
+      c.K.az[IX(rf0)] = a1 - a0;
+      c.K.az[IX(rf1)] = b1 - b0;
+    }
+    if (last && s < nw) {
+      c.S.warm_valid[IX(s)] = nr ? 1 : 0;
+      c.S.warm[IX(s)] = n1;
+      c.S.warm[IX(nw + s)] = a1;
+      c.S.warm[IX(2 * nw + s)] = b1;
+    }
+  }
+}
+
 // Last PCR step fused with the Newton multiplier update (solver.py:81-85,
 // 487-509; contact.py:157-165): dl = x + alpha p, lam += dl, contact
 // projection, dlam = lam_after - lam_before into az (rows) and the tet
@@ -2926,91 +3040,242 @@ __global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int la
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns, nw = c.D.nw;
   const int n_el = nd + nt + na + nh + ns;
   double part = 0.0;
+  FinalArgs FA{step, pend, first != 0, last, alpha, beta, alpha_pend};
+  (void)nw; (void)na; (void)nh; (void)ns; (void)nd; (void)nt;
   FOR_ITEMS(it, n_el) {
-    int rows[6];
-    const int nr = item_rows(c, it, env, rows);
-    // one pass per row: only dl survives into the multiplier update (the
-    // two-pass load-all-then-compute form spilled the loaded rows at 128
-    // registers, and each spill store waited on its load)
-    double dl[6];
+    final_item<EXACT>(c, it, env, FA, part);
+  }
+  double rz;
+  if (reduce_env(c, part, &rz)) c.S.resid[env] = sqrt(0.0 > rz ? 0.0 : rz);
+}
+
+// k_newton_rhs / k_newton_final (structured mode, E >= 32) with each tet
+// split over two warps of the same 32 envs, as k_apply_rows2: the same
+// expressions as tet_forward_uv / tet_res / tet_jt_cols (bitwise the same
+// rows and column sums), half the live registers per thread.
+#ifndef SS_NEWTON2_MINB
+#define SS_NEWTON2_MINB 3
+#endif
+__global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(const Ctx c) {
+  SETUP
+  __shared__ double gsh[4][9][32];   // G (A -> B)
+  __shared__ double zsh[4][9][32];   // z6 and n (B -> A)
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const double gm = c.p.gamma, h = c.p.h;
+  const double* v = c.K.v;
+  if (blockIdx.y == 0 && il == 0) {
+    c.K.broken[env] = 0;
+    c.K.beta[env] = 0.0;
+    c.K.last_step[env] = -1;
+  }
+  const int pair = il >> 1, role = il & 1;
+  const unsigned uE = (unsigned)E;
+  const unsigned ntE = (unsigned)nt * uE;
+  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += gridDim.y * (IL >> 1)) {
+    const unsigned tb = (unsigned)t * uE + (unsigned)env;
+    double* g = &gsh[pair][0][lane];
+    double* zs = &zsh[pair][0][lane];
+    if (role == 0) {
+      int nid[4];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      if (q < nr) {
-        const size_t o = IX(rows[q]);
-        double x = c.K.x[o], z = c.K.z[o];
-        double r = EXACT ? c.K.r[o] : 0.0;
-        const double dq = (step || !EXACT) ? c.K.d[o] : 1.0;
-        const double po = (!EXACT && (pend || (step && !first))) ? c.K.p[o] : 0.0;
-        if (pend) x += alpha_pend * po;
-        if (step) {
-          double pq;
-          if (EXACT) pq = c.K.p[o];
-          else pq = first ? z : z + beta * po;  // the direction as k_pcr_step forms it
-          const double apq = c.K.ap[o];
-          x += alpha * pq;
-          if (EXACT) {
-            r -= alpha * apq;
-            z = r / dq;
-          } else {
-            z -= alpha * apq;  // the ap buffer holds ap/d (k_pcr_dir)
-          }
-        }
-        if (!EXACT) r = dq * z;  // structured mode keeps r = d z implicit
-        part += r * z;
-        dl[q] = x;
-      }
-    }
-    if (it < nd + nt + na + nh) {
-      double d6[6];
+      for (int vv = 0; vv < 4; ++vv) nid[vv] = c.T.t_idx[vv * nt + t];
+      double uv[12], q[4], Ri[9];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        if (q >= nr) break;
-        const size_t o = IX(rows[q]);
-        const double l0 = c.S.lam[o];
-        const double l1 = l0 + dl[q];
-        c.S.lam[o] = l1;
-        d6[q] = l1 - l0;
-        c.K.az[o] = d6[q];
+      for (int vv = 0; vv < 4; ++vv) {
+        const double* up = v + ((unsigned)(3 * nid[vv]) * uE + (unsigned)env);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) uv[3 * vv + a] = up[a * uE];
       }
-      if (it >= nd && it < nd + nt) {
-        const int t = it - nd;
-        TetC T;
-        double Ri[9];
-        tet_load(c, t, env, T);
-        tet_rinv(c, t, Ri);
-        tet_jt<EXACT>(c, t, env, T, Ri, d6);
+      const double* qp = c.S.quat + tb;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = qp[k * ntE];
+      tet_rinv(c, t, Ri);
+      double du[9];
+#pragma unroll
+      for (int vv = 1; vv < 4; ++vv)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) du[3 * (vv - 1) + a] = uv[3 * vv + a] - uv[a];
+      double L[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          L[3 * a + j] = dot3(du[a], Ri[j], du[3 + a], Ri[3 + j], du[6 + a], Ri[6 + j]);
+      double R[9];
+      quat_to_mat(q[0], q[1], q[2], q[3], R);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          g[(3 * i + j) * 32] = dot3(R[i], L[j], R[3 + i], L[3 + j], R[6 + i], L[6 + j]);
+      named_bar(1 + pair, 64);  // G ready
+      named_bar(1 + pair, 64);  // z6, n ready
+      // tet_jt_cols, per-vertex part
+      const double Z00 = zs[0], Z11 = zs[32], Z22 = zs[64];
+      const double Z12 = 0.5 * zs[96], Z02 = 0.5 * zs[128], Z01 = 0.5 * zs[160];
+      const double n0 = zs[192], n1 = zs[224], n2 = zs[256];
+#pragma unroll
+      for (int vv = 0; vv < 4; ++vv) {
+        double wv[3];
+        tet_wv(Ri, vv, wv);
+        const double q0 = dot3(Z00, wv[0], Z01, wv[1], Z02, wv[2]) - __fma_rn(n1, wv[2], -n2 * wv[1]);
+        const double q1 = dot3(Z01, wv[0], Z11, wv[1], Z12, wv[2]) - __fma_rn(n2, wv[0], -n0 * wv[2]);
+        const double q2 = dot3(Z02, wv[0], Z12, wv[1], Z22, wv[2]) - __fma_rn(n0, wv[1], -n1 * wv[0]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          c.K.tC[TCX(3 * vv + a, t)] = dot3(R[3 * a], q0, R[3 * a + 1], q1, R[3 * a + 2], q2);
       }
     } else {
-      const int s = it - nd - nt - na - nh;
-      double n1 = 0.0, a1 = 0.0, b1 = 0.0;
-      if (nr) {
-        const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
-        const double n0 = c.K.lamc[IX(s)], a0 = c.K.lamc[IX(ns + s)], b0 = c.K.lamc[IX(2 * ns + s)];
-        n1 = n0 + dl[0];
-        a1 = a0 + dl[1];
-        b1 = b0 + dl[2];
-        n1 = npmax(n1, 0.0);
-        const double rad = c.p.mu * npmax(n1, 0.0);
-        const double nrm = sqrt(a1 * a1 + b1 * b1);
-        if (nrm > rad) {
-          const double sc = nrm > 0.0 ? rad / nrm : 0.0;
-          a1 *= sc;
-          b1 *= sc;
-        }
-        c.K.lamc[IX(s)] = n1;
-        c.K.lamc[IX(ns + s)] = a1;
-        c.K.lamc[IX(2 * ns + s)] = b1;
-        c.K.az[IX(rn)] = n1 - n0;
-        c.K.az[IX(rf0)] = a1 - a0;
-        c.K.az[IX(rf1)] = b1 - b0;
+      double sv[6], lm[6], bd[6];
+      const double* sp = c.K.tS + tb;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sv[k] = sp[k * ntE];
+      const unsigned ob = (unsigned)c.D.ot * uE + tb;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[ob + i * ntE];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) bd[i] = c.K.bdiag[ob + i * ntE];
+      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
+      double S[9], Ki[9];
+      S[0] = sv[0]; S[4] = sv[1]; S[8] = sv[2];
+      S[5] = sv[3]; S[7] = sv[3];
+      S[2] = sv[4]; S[6] = sv[4];
+      S[1] = sv[5]; S[3] = sv[5];
+      tet_kinv(S, Ki);
+      named_bar(1 + pair, 64);  // G ready
+      double G[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) G[k] = g[k * 32];
+      // tet_forward_uv, second half: jv = J v
+      const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
+      const double w0 = dot3(Ki[0], g0, Ki[1], g1, Ki[2], g2);
+      const double w1 = dot3(Ki[3], g0, Ki[4], g1, Ki[5], g2);
+      const double w2 = dot3(Ki[6], g0, Ki[7], g1, Ki[8], g2);
+      const double ws00 = __fma_rn(w1, S[6], -w2 * S[3]);
+      const double ws01 = __fma_rn(w1, S[7], -w2 * S[4]);
+      const double ws02 = __fma_rn(w1, S[8], -w2 * S[5]);
+      const double ws10 = __fma_rn(w2, S[0], -w0 * S[6]);
+      const double ws11 = __fma_rn(w2, S[1], -w0 * S[7]);
+      const double ws12 = __fma_rn(w2, S[2], -w0 * S[8]);
+      const double ws20 = __fma_rn(w0, S[3], -w1 * S[0]);
+      const double ws21 = __fma_rn(w0, S[4], -w1 * S[1]);
+      const double ws22 = __fma_rn(w0, S[5], -w1 * S[2]);
+      double jv[6];
+      jv[0] = G[0] - ws00;
+      jv[1] = G[4] - ws11;
+      jv[2] = G[8] - ws22;
+      jv[3] = 0.5 * ((G[5] + G[7]) - (ws12 + ws21));
+      jv[4] = 0.5 * ((G[2] + G[6]) - (ws02 + ws20));
+      jv[5] = 0.5 * ((G[1] + G[3]) - (ws01 + ws10));
+      // tet_res (numba_backend.py:241-246)
+      double rs[6];
+      rs[0] = S[0] - 1.0;
+      rs[1] = S[4] - 1.0;
+      rs[2] = S[8] - 1.0;
+      rs[3] = S[5];
+      rs[4] = S[2];
+      rs[5] = S[1];
+      double el[6], z6[6];
+      ereg6(ed, eo, es, lm, el);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double dg = npmax(bd[i] + 0.0, 1e-30);
+        const double d = dg > 1e-300 ? dg : 1.0;
+        const double r = -(gm * rs[i] / h + jv[i] + el[i]);
+        z6[i] = r / d;
+        const unsigned o = ob + i * ntE;
+        c.K.r[o] = r;
+        c.K.d[o] = d;
+        c.K.z[o] = z6[i];
+        c.K.x[o] = 0.0;
       }
-      if (last && s < nw) {
-        c.S.warm_valid[IX(s)] = nr ? 1 : 0;
-        c.S.warm[IX(s)] = n1;
-        c.S.warm[IX(nw + s)] = a1;
-        c.S.warm[IX(2 * nw + s)] = b1;
-      }
+      // tet_jt_cols, shared part: n = K^-1 ax(Z S)
+      const double Z00 = z6[0], Z11 = z6[1], Z22 = z6[2];
+      const double Z12 = 0.5 * z6[3], Z02 = 0.5 * z6[4], Z01 = 0.5 * z6[5];
+      const double N21 = dot3(Z02, S[1], Z12, S[4], Z22, S[7]);
+      const double N12 = dot3(Z01, S[2], Z11, S[5], Z12, S[8]);
+      const double N02 = dot3(Z00, S[2], Z01, S[5], Z02, S[8]);
+      const double N20 = dot3(Z02, S[0], Z12, S[3], Z22, S[6]);
+      const double N10 = dot3(Z01, S[0], Z11, S[3], Z12, S[6]);
+      const double N01 = dot3(Z00, S[1], Z01, S[4], Z02, S[7]);
+      const double m0 = N21 - N12, m1 = N02 - N20, m2 = N10 - N01;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) zs[i * 32] = z6[i];
+      zs[192] = dot3(Ki[0], m0, Ki[1], m1, Ki[2], m2);
+      zs[224] = dot3(Ki[3], m0, Ki[4], m1, Ki[5], m2);
+      zs[256] = dot3(Ki[6], m0, Ki[7], m1, Ki[8], m2);
+      named_bar(1 + pair, 64);  // z6, n ready
     }
+  }
+  const int n_other = nd + na + nh + ns;
+  for (int q2 = blockIdx.y * IL + il; q2 < n_other; q2 += gridDim.y * IL) {
+    const int it = q2 < nd ? q2 : q2 + nt;
+    rhs_item<false>(c, it, env);
+  }
+}
+
+__global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_final2(const Ctx c, int do_step,
+                                                                               int last, int first) {
+  SETUP
+  __shared__ double dsh[4][6][32];  // dlam of the tet rows (A -> B)
+  const bool step = do_step && !c.K.broken[env];
+  const double alpha = c.K.alpha[env];
+  const double beta = c.K.beta[env];
+  const int ls = c.K.last_step[env];
+  const bool pend = ls >= 0 && !(ls & 1);
+  const double alpha_pend = pend ? (step ? c.K.alpha_prev[env] : alpha) : 0.0;
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const FinalArgs FA{step, pend, first != 0, last, alpha, beta, alpha_pend};
+  const int pair = il >> 1, role = il & 1;
+  const unsigned uE = (unsigned)E;
+  const unsigned ntE = (unsigned)nt * uE;
+  double part = 0.0;
+  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += gridDim.y * (IL >> 1)) {
+    double* ds = &dsh[pair][0][lane];
+    if (role == 0) {
+      const unsigned ob = (unsigned)c.D.ot * uE + (unsigned)t * uE + (unsigned)env;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const unsigned o = ob + q * ntE;
+        double x = c.K.x[o], z = c.K.z[o];
+        const double dq = c.K.d[o];
+        const double po = (pend || (step && !FA.first)) ? c.K.p[o] : 0.0;
+        if (pend) x += alpha_pend * po;
+        if (step) {
+          const double pq = FA.first ? z : z + beta * po;
+          const double apq = c.K.ap[o];
+          x += alpha * pq;
+          z -= alpha * apq;
+        }
+        const double r = dq * z;
+        part += r * z;
+        const double l0 = c.S.lam[o];
+        const double l1 = l0 + x;
+        c.S.lam[o] = l1;
+        const double d6 = l1 - l0;
+        c.K.az[o] = d6;
+        ds[q * 32] = d6;
+      }
+      named_bar(1 + pair, 64);
+    } else {
+      TetC T;
+      double Ri[9];
+      tet_load(c, t, env, T);
+      tet_rinv(c, t, Ri);
+      named_bar(1 + pair, 64);
+      double d6[6], col12[12];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) d6[q] = ds[q * 32];
+      tet_jt_cols(T, Ri, d6, col12);
+#pragma unroll
+      for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
+    }
+    named_bar(1 + pair, 64);  // ds consumed before the next item overwrites it
+  }
+  const int n_other = nd + na + nh + ns;
+  for (int q2 = blockIdx.y * IL + il; q2 < n_other; q2 += gridDim.y * IL) {
+    const int it = q2 < nd ? q2 : q2 + nt;
+    final_item<false>(c, it, env, FA, part);
   }
   double rz;
   if (reduce_env(c, part, &rz)) c.S.resid[env] = sqrt(0.0 > rz ? 0.0 : rz);

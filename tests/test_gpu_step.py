@@ -523,3 +523,36 @@ def test_step_jt_bitwise(n):
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("n", [64, 96])
+def test_newton2_bitwise(n):
+    """k_newton_rhs2 / k_newton_final2 (tets split over two warps) give
+    bitwise the state of k_newton_rhs / k_newton_final (the residual stat is
+    summed over another thread assignment)."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(31)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out, res = {}, {}
+    for mode in ("0", "1"):
+        os.environ["SS_NEWTON2"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_NEWTON2", None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_newton_rhs2"][1] > 0) == (mode == "1")
+        assert (prof["k_newton_final2"][1] > 0) == (mode == "1")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        res[mode] = np.array([s.residual for s in sim.get_stats()])
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+    assert np.allclose(res["0"], res["1"], rtol=1e-10, atol=0.0)
