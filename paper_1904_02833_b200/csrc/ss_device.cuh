@@ -1361,6 +1361,20 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
       double w0 = 0.0, w1 = 0.0, w2 = 0.0;
       // the list is sorted by family: [dist][tet][attach][contact normal][friction]
       const int2 tr = c.T.inc_tet[it];
+#ifndef SS_GATHER_NO_FLAG_PREFETCH
+      // a contact slot's flags (its last two entries) loaded now, so the slot's
+      // test at the end of the walk does not wait a memory round trip
+      int pf_slot = -1, pf_pres = 0;
+      double pf_act = 0.0;
+      if (k1 - k0 >= 2) {
+        const int cl = c.T.inc[k1 - 1];
+        if ((int)((unsigned)cl >> 29) == F_CF) {
+          pf_slot = cl & 0x1FFFFFF;
+          pf_pres = c.K.present[IX(pf_slot)];
+          pf_act = c.K.actf[IX(pf_slot)];
+        }
+      }
+#endif
       for (int k = k0; k < k1; ++k) {
         if (k == tr.x) {
           // tet run: column sums from tC, loads hoisted 4 incidences at a time
@@ -1397,6 +1411,35 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
         }
         const int code = c.T.inc[k];
         double a0, a1, a2;
+#ifndef SS_GATHER_NO_FLAG_PREFETCH
+        {
+          const int fam = (int)((unsigned)code >> 29);
+          if ((fam == F_CN || fam == F_CF) && (code & 0x1FFFFFF) == pf_slot) {
+            // inc_particle's contact branch with the prefetched flags
+            const bool on = mode == 0 ? (fam == F_CN ? pf_pres != 0 : pf_act != 0.0) : pf_pres != 0;
+            if (!on) continue;
+            const int e = pf_slot;
+            if (fam == F_CN) {
+              const double xn = xc[IX(e)];
+              a0 = 0.0 + 0.0 * xn;
+              a1 = 0.0 + 0.0 * xn;
+              a2 = 0.0 + 1.0 * xn;
+            } else {
+              const double xf0 = xc[IX(ns + e)], xf1 = xc[IX(2 * ns + e)];
+              a0 = 0.0 + 1.0 * xf0;
+              a0 += 0.0 * xf1;
+              a1 = 0.0 + 0.0 * xf0;
+              a1 += 1.0 * xf1;
+              a2 = 0.0 + 0.0 * xf0;
+              a2 += 0.0 * xf1;
+            }
+            w0 += a0;
+            w1 += a1;
+            w2 += a2;
+            continue;
+          }
+        }
+#endif
         if (!inc_particle(c, code, mode, xs, xc, env, a0, a1, a2)) continue;
         w0 += a0;
         w1 += a1;
