@@ -35,6 +35,10 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
     launch; 4 on the first launch of a solve) instead of 8. pcr: the
     PCR budget, for the per-launch average over one solve (pcr k_pcr_dir
     launches, pcr - 1 k_pcr_step launches)."""
+    # round-2 kernels that move the same operands as their round-1 twins
+    kernel = {"k_apply_rows2": "k_apply_rows", "k_apply_rows_async": "k_apply_rows",
+              "k_pcr_dir_rows": "k_pcr_dir", "k_newton_rhs2": "k_newton_rhs",
+              "k_newton_final2": "k_newton_final"}.get(kernel, kernel)
     rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches
     jc = F8 * 10 * d["nt"]                       # compact tet J: quat(4) S(6); R, K^-1 rebuilt
     tc = F8 * 12 * d["nt"]                       # tet column sums J^T x
@@ -76,6 +80,9 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
     if kernel == "k_newton_final":
         # read x r z p ap d + lam, write lam + dlam, compact J, write tC
         return F8 * 9 * rows + jc + tc + flags
+    if kernel == "k_eval_polar":
+        # positions once, quats read and written (the polar loop alone)
+        return F8 * (3 * d["P"] + 8 * d["nt"])
     if kernel == "k_eval_tet":
         # positions once, quats r/w, S + diag + tC written, lam read
         return F8 * (3 * d["P"] + 8 * d["nt"] + 6 * d["nt"] + 6 * d["nt"] + 12 * d["nt"]
