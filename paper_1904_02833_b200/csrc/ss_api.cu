@@ -84,7 +84,6 @@ struct Arena {
 
 }  // namespace
 
-constexpr int kMaxGyRed2 = 96;  // k_apply_rows2 grid rows (partials per env) at most
 struct GridCaps {
   long stream = 148 * 32;  // PCR step, tet J^T z, element kernels without reduction
   long eval = 148 * 8;     // per-substep eval / integrate kernels
@@ -239,6 +238,23 @@ int kid(const char* name) {
     }                                                                    \
     ++n;                                                                 \
   } while (0)
+
+// grid rows of k_apply_rows2 / k_newton_final2 and k_pcr_dir_rows: one
+// resident wave at their occupancy (the partial buffer is sized for them)
+static void set_gy2(ss_handle* H, const Dims& D) {
+  int occ_a = 3, occ_d = 4, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_apply_rows2, SS_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir_rows, SS_THREADS, 0);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
+  const long rows_el = ((long)D.nd + D.nt + D.na + D.nh + D.ns + 3) / 4;  // tet pairs bound
+  const long rows_m = ((long)D.m + 7) / 8;
+  long a = std::max(1L, (long)sms * std::max(1, occ_a) / std::max(1, D.tiles));
+  long d = std::max(1L, (long)sms * std::max(1, occ_d) / std::max(1, D.tiles));
+  a = std::min(a, std::max(1L, rows_el));
+  d = std::min(d, std::max(1L, rows_m));
+  H->gy_red2 = (int)std::min(env_long("SS_APPLY2_GY", a), 65535L);
+  H->gy_dir2 = (int)std::min(env_long("SS_DIR2_GY", d), 65535L);
+}
 
 // ------------------------------------------------------ k_jtg plan
 static int jtg_ring_slots() { return (int)std::max(2L, env_long("SS_JTG_RING", 3)); }
@@ -1443,6 +1459,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     const long n_el = (long)D.nd + D.nt + D.na + D.nh + D.ns;
     H->gy_red = (int)grid_items(D, n_el, H->caps.reduce).y;
     H->gy_dir = (int)grid_items(D, n_el, H->caps.dir).y;
+    set_gy2(H, D);
   }
 
   // state + work (lane count read at call time: the wave cap may shrink it)
@@ -1474,7 +1491,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   };
   auto plan_work = [&](Arena& A) {
     const size_t Es = H->c.D.E;
-    const int gy_max = std::max(std::max(H->gy_red, H->gy_dir), kMaxGyRed2);
+    const int gy_max = std::max(std::max(H->gy_red, H->gy_dir), std::max(H->gy_red2, H->gy_dir2));
     Work& K = H->c.K;
     K.v = A.take<double>((size_t)D.ndof * Es);
     K.u = A.take<double>((size_t)D.ndof * Es);
@@ -1545,6 +1562,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
       H->c.D = D;
       H->gy_red = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, H->caps.reduce).y;
       H->gy_dir = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, H->caps.dir).y;
+      set_gy2(H, D);
       sa = Arena();
       wa = Arena();
       plan_state(sa);
@@ -1625,16 +1643,8 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     CK(cudaMemsetAsync(H->d_cmd, 0, 8 * cmd_n, H->stream));
   }
   for (const auto& g : H->guards) CK(cudaMemsetAsync(g.first, 0xA5, g.second, H->stream));
-  if (!H->c.p.exact_j && !H->use_cluster && D.nt > 0 && D.W == 32 && env_long("SS_APPLY2", 1)) {
-    // partials per env = grid rows: must fit the part buffer sized for gy_red / gy_dir
-    int occ = 3, sms = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_rows2, SS_THREADS, 0);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
-    long want = (long)sms * std::max(1, occ) / D.tiles;
-    want = std::max(1L, std::min(want, (long)kMaxGyRed2));
-    H->gy_red2 = (int)std::min<long>(env_long("SS_APPLY2_GY", want), kMaxGyRed2);
+  if (!H->c.p.exact_j && !H->use_cluster && D.nt > 0 && D.W == 32 && env_long("SS_APPLY2", 1))
     H->apply2 = 1;
-  }
   H->polar_split = (int)env_long("SS_POLAR_SPLIT", 1);
   H->newton2 = (H->apply2 && env_long("SS_NEWTON2", 1)) ? 1 : 0;  // needs g_red2 (apply2 plan)
   // opt-in: bitwise equal but 60-68 ms/frame against 58.5 for k_pcr_step +
@@ -1645,15 +1655,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // batched layouts only (W == 32): at few env lanes the element-owned kernel
   // keeps the v2.14 reduction order (an ill-conditioned parity case,
   // test_gpu_params[fb_slopes], sits at 1.4e-10 of its 1e-10 bound there)
-  if (!H->c.p.exact_j && !H->use_cluster && D.W == 32 && env_long("SS_DIR2", 1)) {
-    int occ = 4, sms = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcr_dir_rows, SS_THREADS, 0);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
-    long want = (long)sms * std::max(1, occ) / D.tiles;
-    want = std::max(1L, std::min(want, (long)kMaxGyRed2));
-    H->gy_dir2 = (int)std::min<long>(env_long("SS_DIR2_GY", want), kMaxGyRed2);
-    H->dir2 = 1;
-  }
+  if (!H->c.p.exact_j && !H->use_cluster && D.W == 32 && env_long("SS_DIR2", 1)) H->dir2 = 1;
   // opt-in: no gain measured (coupled 2-snake frame 6.16 ms either way; 1024 envs and
   // the 1M-tet scene within noise, profiles/r2_summary.md)
   H->pdl = (int)env_long("SS_PDL", 0);

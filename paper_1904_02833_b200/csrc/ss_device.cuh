@@ -142,14 +142,12 @@ DI void pdl_wait() {
 #define IX(item) ((size_t)(item) * E + env)
 // tet column sums tC: [12][nt][E] (a [nt][12] layout for E = 1 was tried:
 // the gather did not speed up and the strided writes cost k_tet_jt 35%)
-#ifndef SS_TC_COMPMAJOR
-// [nt][12][E]: a tet's 12 column sums are 12 consecutive env rows (k_tet_jt
-// writes, and the gather reads, contiguous 3 KB runs per tet at E = 32;
-// 0.5 ms/frame faster than [12][nt][E] at 1024 envs)
-#define TCX(k, t) (((size_t)(t) * 12 + (k)) * E + env)
-#else
-#define TCX(k, t) (((size_t)(k) * nt + (t)) * E + env)
-#endif
+// Batched (E >= 32): [nt][12][E], a tet's 12 column sums are 12 consecutive
+// env rows (contiguous 3 KB runs per tet: 0.5 ms/frame faster than [12][nt][E]
+// at 1024 envs). Few env lanes: [12][nt][E], so consecutive tets of one env
+// stay coalesced for k_tet_jt's stores (the tet-major order costs the 1M-tet
+// scene 9%).
+#define TCX(k, t) (E >= 32 ? ((size_t)(t) * 12 + (k)) * E + env : ((size_t)(k) * nt + (t)) * E + env)
 
 // ------------------------------------------------------------ small math
 // numpy.maximum: NaN in a propagates
