@@ -2460,14 +2460,35 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
   const unsigned ntE = (unsigned)nt * uE;
   double part = 0.0;
   int buf = 0;
+  const int tstride = gridDim.y * (IL >> 1);
+#ifndef SS_APPLY2_NO_NIDPF
+  // warp A: the next item's node ids one item ahead
+  int nid_n[4] = {0, 0, 0, 0};
+  {
+    const int t0 = blockIdx.y * (IL >> 1) + pair;
+    if (role == 0 && t0 < nt) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) nid_n[v] = c.T.t_idx[v * nt + t0];
+    }
+  }
+#endif
   // ---- tets: item lanes paired
-  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += gridDim.y * (IL >> 1)) {
+  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += tstride) {
     const unsigned tb = (unsigned)t * uE + (unsigned)env;
     double* g = &gsh[pair][buf][0][lane];
     if (role == 0) {
       int nid[4];
+#ifndef SS_APPLY2_NO_NIDPF
+#pragma unroll
+      for (int v = 0; v < 4; ++v) nid[v] = nid_n[v];
+      if (t + tstride < nt) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) nid_n[v] = c.T.t_idx[v * nt + t + tstride];
+      }
+#else
 #pragma unroll
       for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + t];
+#endif
       double uv[12], q[4], Ri[9];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
