@@ -1643,7 +1643,12 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     CK(cudaMemsetAsync(H->d_cmd, 0, 8 * cmd_n, H->stream));
   }
   for (const auto& g : H->guards) CK(cudaMemsetAsync(g.first, 0xA5, g.second, H->stream));
-  if (!H->c.p.exact_j && !H->use_cluster && D.nt > 0 && D.W == 32 && env_long("SS_APPLY2", 1))
+  // batched layouts, and one large mesh (E = 1 with >= 64k tets: 32 tets per
+  // warp pair); small single scenes keep the one-thread kernels' reduction
+  // order (test_gpu_params[fb_slopes] sits near its bound there)
+  if (!H->c.p.exact_j && !H->use_cluster && D.nt > 0 &&
+      (D.W == 32 || (D.W == 1 && D.nt >= env_long("SS_APPLY2_MIN_NT", 65536))) &&
+      env_long("SS_APPLY2", 1))
     H->apply2 = 1;
   H->polar_split = (int)env_long("SS_POLAR_SPLIT", 1);
   H->newton2 = (H->apply2 && env_long("SS_NEWTON2", 1)) ? 1 : 0;  // needs g_red2 (apply2 plan)

@@ -2434,6 +2434,18 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLYA_MINB) k_apply_rows_async
   }
 }
 
+// Tet mapping of the two-warp kernels: a pair of warps takes one tet for 32
+// env lanes (W == 32) or 32 consecutive tets of the single env (W == 1).
+// Every thread of a pair runs the same trip count (tw_act masks the tail), so
+// the pair's named barriers always see both warps.
+#define TW_SETUP                                                              \
+  const int tw_slot = threadIdx.x & 31;                                       \
+  const int pair = (threadIdx.x >> 5) >> 1, role = (threadIdx.x >> 5) & 1;     \
+  const int tw_mul = c.D.W == 1 ? 32 : 1;                                     \
+  const int tw_base = (blockIdx.y * 4 + pair) * tw_mul;                        \
+  const int tw_off = c.D.W == 1 ? tw_slot : 0;                                \
+  const int tw_stride = gridDim.y * 4 * tw_mul;
+
 // k_apply_rows (structured mode, E >= 32) with each tet split over TWO warps
 // of the same 32 envs: warp A (even item lane) loads the 4 nodes' u, the
 // rest-shape inverse and the quaternion and forms G = R^T sum_v u_v w_v^T;
@@ -2455,17 +2467,17 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
   const double* u = c.K.u;
   const double* z = c.K.z;
-  const int pair = il >> 1, role = il & 1;
+  TW_SETUP
   const unsigned uE = (unsigned)E;
   const unsigned ntE = (unsigned)nt * uE;
   double part = 0.0;
   int buf = 0;
-  const int tstride = gridDim.y * (IL >> 1);
+  const int tstride = tw_stride;
 #ifndef SS_APPLY2_NO_NIDPF
   // warp A: the next item's node ids one item ahead
   int nid_n[4] = {0, 0, 0, 0};
   {
-    const int t0 = blockIdx.y * (IL >> 1) + pair;
+    const int t0 = tw_base + tw_off;
     if (role == 0 && t0 < nt) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) nid_n[v] = c.T.t_idx[v * nt + t0];
@@ -2473,9 +2485,12 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
   }
 #endif
   // ---- tets: item lanes paired
-  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += tstride) {
-    const unsigned tb = (unsigned)t * uE + (unsigned)env;
-    double* g = &gsh[pair][buf][0][lane];
+  for (int tw_t = tw_base; tw_t < nt; tw_t += tw_stride) {
+    const int t = tw_t + tw_off;
+    const bool tw_act = t < nt;
+    const int tc = tw_act ? t : nt - 1;  // tail lanes load a valid tet, store nothing
+    const unsigned tb = (unsigned)tc * uE + (unsigned)env;
+    double* g = &gsh[pair][buf][0][tw_slot];
     if (role == 0) {
       int nid[4];
 #ifndef SS_APPLY2_NO_NIDPF
@@ -2487,7 +2502,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       }
 #else
 #pragma unroll
-      for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + t];
+      for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + tc];
 #endif
       double uv[12], q[4], Ri[9];
 #pragma unroll
@@ -2499,7 +2514,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       const double* qp = c.S.quat + tb;
 #pragma unroll
       for (int k = 0; k < 4; ++k) q[k] = qp[k * ntE];
-      tet_rinv(c, t, Ri);
+      tet_rinv(c, tc, Ri);
       // tet_forward_uv, first half: du, L, G
       double du[9];
 #pragma unroll
@@ -2528,7 +2543,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       const double* zp = z + ((unsigned)c.D.ot * uE + tb);
 #pragma unroll
       for (int i = 0; i < 6; ++i) zz[i] = zp[i * ntE];
-      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
+      const double ed = c.T.t_e3[tc], eo = c.T.t_e3[nt + tc], es = c.T.t_e3[2 * nt + tc];
       double S[9], Ki[9];
       S[0] = sv[0]; S[4] = sv[1]; S[8] = sv[2];
       S[5] = sv[3]; S[7] = sv[3];
@@ -2563,11 +2578,12 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       ereg6(ed, eo, es, zz, ez);
       double* ap = c.K.az + ((unsigned)c.D.ot * uE + tb);
 #pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        const double az = y[i] + ez[i];
-        ap[i * ntE] = az;
-        part += zz[i] * az;
-      }
+      if (tw_act)
+        for (int i = 0; i < 6; ++i) {
+          const double az = y[i] + ez[i];
+          ap[i * ntE] = az;
+          part += zz[i] * az;
+        }
     }
     buf ^= 1;
   }
@@ -3130,17 +3146,20 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(con
     c.K.beta[env] = 0.0;
     c.K.last_step[env] = -1;
   }
-  const int pair = il >> 1, role = il & 1;
+  TW_SETUP
   const unsigned uE = (unsigned)E;
   const unsigned ntE = (unsigned)nt * uE;
-  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += gridDim.y * (IL >> 1)) {
-    const unsigned tb = (unsigned)t * uE + (unsigned)env;
-    double* g = &gsh[pair][0][lane];
-    double* zs = &zsh[pair][0][lane];
+  for (int tw_t = tw_base; tw_t < nt; tw_t += tw_stride) {
+    const int t = tw_t + tw_off;
+    const bool tw_act = t < nt;
+    const int tc = tw_act ? t : nt - 1;  // tail lanes load a valid tet, store nothing
+    const unsigned tb = (unsigned)tc * uE + (unsigned)env;
+    double* g = &gsh[pair][0][tw_slot];
+    double* zs = &zsh[pair][0][tw_slot];
     if (role == 0) {
       int nid[4];
 #pragma unroll
-      for (int vv = 0; vv < 4; ++vv) nid[vv] = c.T.t_idx[vv * nt + t];
+      for (int vv = 0; vv < 4; ++vv) nid[vv] = c.T.t_idx[vv * nt + tc];
       double uv[12], q[4], Ri[9];
 #pragma unroll
       for (int vv = 0; vv < 4; ++vv) {
@@ -3151,7 +3170,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(con
       const double* qp = c.S.quat + tb;
 #pragma unroll
       for (int k = 0; k < 4; ++k) q[k] = qp[k * ntE];
-      tet_rinv(c, t, Ri);
+      tet_rinv(c, tc, Ri);
       double du[9];
 #pragma unroll
       for (int vv = 1; vv < 4; ++vv)
@@ -3185,7 +3204,8 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(con
         const double q2 = dot3(Z02, wv[0], Z12, wv[1], Z22, wv[2]) - __fma_rn(n0, wv[1], -n1 * wv[0]);
 #pragma unroll
         for (int a = 0; a < 3; ++a)
-          c.K.tC[TCX(3 * vv + a, t)] = dot3(R[3 * a], q0, R[3 * a + 1], q1, R[3 * a + 2], q2);
+          if (tw_act)
+            c.K.tC[TCX(3 * vv + a, t)] = dot3(R[3 * a], q0, R[3 * a + 1], q1, R[3 * a + 2], q2);
       }
     } else {
       double sv[6], lm[6], bd[6];
@@ -3197,7 +3217,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(con
       for (int i = 0; i < 6; ++i) lm[i] = c.S.lam[ob + i * ntE];
 #pragma unroll
       for (int i = 0; i < 6; ++i) bd[i] = c.K.bdiag[ob + i * ntE];
-      const double ed = c.T.t_e3[t], eo = c.T.t_e3[nt + t], es = c.T.t_e3[2 * nt + t];
+      const double ed = c.T.t_e3[tc], eo = c.T.t_e3[nt + tc], es = c.T.t_e3[2 * nt + tc];
       double S[9], Ki[9];
       S[0] = sv[0]; S[4] = sv[1]; S[8] = sv[2];
       S[5] = sv[3]; S[7] = sv[3];
@@ -3246,10 +3266,12 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(con
         const double r = -(gm * rs[i] / h + jv[i] + el[i]);
         z6[i] = r / d;
         const unsigned o = ob + i * ntE;
-        c.K.r[o] = r;
-        c.K.d[o] = d;
-        c.K.z[o] = z6[i];
-        c.K.x[o] = 0.0;
+        if (tw_act) {
+          c.K.r[o] = r;
+          c.K.d[o] = d;
+          c.K.z[o] = z6[i];
+          c.K.x[o] = 0.0;
+        }
       }
       // tet_jt_cols, shared part: n = K^-1 ax(Z S)
       const double Z00 = z6[0], Z11 = z6[1], Z22 = z6[2];
@@ -3288,14 +3310,17 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_final2(c
   const double alpha_pend = pend ? (step ? c.K.alpha_prev[env] : alpha) : 0.0;
   const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
   const FinalArgs FA{step, pend, first != 0, last, alpha, beta, alpha_pend};
-  const int pair = il >> 1, role = il & 1;
+  TW_SETUP
   const unsigned uE = (unsigned)E;
   const unsigned ntE = (unsigned)nt * uE;
   double part = 0.0;
-  for (int t = blockIdx.y * (IL >> 1) + pair; t < nt; t += gridDim.y * (IL >> 1)) {
-    double* ds = &dsh[pair][0][lane];
+  for (int tw_t = tw_base; tw_t < nt; tw_t += tw_stride) {
+    const int t = tw_t + tw_off;
+    const bool tw_act = t < nt;
+    const int tc = tw_act ? t : nt - 1;  // tail lanes load a valid tet, store nothing
+    double* ds = &dsh[pair][0][tw_slot];
     if (role == 0) {
-      const unsigned ob = (unsigned)c.D.ot * uE + (unsigned)t * uE + (unsigned)env;
+      const unsigned ob = (unsigned)c.D.ot * uE + (unsigned)tc * uE + (unsigned)env;
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const unsigned o = ob + q * ntE;
@@ -3310,27 +3335,30 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_final2(c
           z -= alpha * apq;
         }
         const double r = dq * z;
-        part += r * z;
         const double l0 = c.S.lam[o];
         const double l1 = l0 + x;
-        c.S.lam[o] = l1;
         const double d6 = l1 - l0;
-        c.K.az[o] = d6;
+        if (tw_act) {
+          part += r * z;
+          c.S.lam[o] = l1;
+          c.K.az[o] = d6;
+        }
         ds[q * 32] = d6;
       }
       named_bar(1 + pair, 64);
     } else {
       TetC T;
       double Ri[9];
-      tet_load(c, t, env, T);
-      tet_rinv(c, t, Ri);
+      tet_load(c, tc, env, T);
+      tet_rinv(c, tc, Ri);
       named_bar(1 + pair, 64);
       double d6[6], col12[12];
 #pragma unroll
       for (int q = 0; q < 6; ++q) d6[q] = ds[q * 32];
       tet_jt_cols(T, Ri, d6, col12);
+      if (tw_act)
 #pragma unroll
-      for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
+        for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
     }
     named_bar(1 + pair, 64);  // ds consumed before the next item overwrites it
   }
