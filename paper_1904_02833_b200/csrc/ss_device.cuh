@@ -2492,6 +2492,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
     const unsigned tb = (unsigned)tc * uE + (unsigned)env;
     double* g = &gsh[pair][buf][0][tw_slot];
     if (role == 0) {
+      double uv[12], q[4], Ri[9];
       int nid[4];
 #ifndef SS_APPLY2_NO_NIDPF
 #pragma unroll
@@ -2504,7 +2505,6 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
 #pragma unroll
       for (int v = 0; v < 4; ++v) nid[v] = c.T.t_idx[v * nt + tc];
 #endif
-      double uv[12], q[4], Ri[9];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const double* up = u + ((unsigned)(3 * nid[v]) * uE + (unsigned)env);
@@ -2577,13 +2577,14 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       y[5] = 0.5 * ((G[1] + G[3]) - (ws01 + ws10));
       ereg6(ed, eo, es, zz, ez);
       double* ap = c.K.az + ((unsigned)c.D.ot * uE + tb);
+      if (tw_act) {
 #pragma unroll
-      if (tw_act)
         for (int i = 0; i < 6; ++i) {
           const double az = y[i] + ez[i];
           ap[i * ntE] = az;
           part += zz[i] * az;
         }
+      }
     }
     buf ^= 1;
   }
@@ -3356,9 +3357,10 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_final2(c
 #pragma unroll
       for (int q = 0; q < 6; ++q) d6[q] = ds[q * 32];
       tet_jt_cols(T, Ri, d6, col12);
-      if (tw_act)
+      if (tw_act) {
 #pragma unroll
         for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
+      }
     }
     named_bar(1 + pair, 64);  // ds consumed before the next item overwrites it
   }
