@@ -314,7 +314,11 @@ int64_t ss_device_bytes(ss_handle* h);
  * cluster, info[2] shared bytes per CTA, info[3] env lanes per wave,
  * info[4] number of waves, info[5] 1 if the PCR loop's J^T z gather is
  * fused (k_gather_fused), info[6] its particle blocks, info[7] its chunks
- * over all blocks. info must hold 8 ints. */
+ * over all blocks, info[8] clusters per environment (> 1: a multi-component
+ * scene with one cluster per component, dot products combined through
+ * global memory), info[9] nonzero if a cross-cluster reduction faulted
+ * (a cluster never arrived or the plan's reduction count was exceeded).
+ * info must hold 10 ints. */
 int ss_solver_info(ss_handle* h, int* info);
 /* Debug: with SS_GUARD=1 set at ss_create every device array is followed by
  * a 0xA5 guard band; *bad_bytes = guard bytes changed since (an out-of-

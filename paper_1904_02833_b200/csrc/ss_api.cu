@@ -127,6 +127,7 @@ struct ss_handle {
   char* d_init = nullptr;  // reset template: one env's state, packed per field
   ClPlan plan{};
   void* plan_mem = nullptr;
+  void* xmem = nullptr;     // cross-cluster reduction buffers (multi-cluster plans)
   // fused J^T z gather of the PCR loop (k_gather_fused; structured mode)
   int fused = 0;
   FusedPlan fplan{};
@@ -351,9 +352,11 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       cfg.attrs = at;
       cfg.numAttrs = 1;
       cfg.blockDim = dim3(CL_THREADS);
-      cfg.gridDim = dim3(H->plan.C * D.E);
+      cfg.gridDim = dim3(H->plan.C * H->plan.G * D.E);
       cfg.dynamicSmemBytes = 8 * (size_t)H->plan.smem_doubles;
       cfg.stream = st;
+      if (H->plan.G > 1)  // cross-cluster arrival counters of this launch
+        CK(cudaMemsetAsync(H->plan.xcnt, 0, sizeof(int) * (size_t)H->plan.xn, st));
       CK(cudaLaunchKernelEx(&cfg, k_newton_cluster<EX>, c, H->plan));
       if (prof) {
         cudaEventRecord(e1_, st);
@@ -742,15 +745,30 @@ struct PlanBuild {
   size_t smem_bytes;
 };
 
+// comp (optional, multi-cluster plans): the connected component of every
+// node (particles, then P + body), G groups of C CTAs, group k owning
+// component k; without it one group of C CTAs owns the whole scene.
 static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& d_i,
                            const std::vector<int>& d_j, const std::vector<int>& tets,
                            const std::vector<int>& a_p, const std::vector<int>& a_b,
                            const std::vector<int>& h_a, const std::vector<int>& h_b,
                            const std::vector<int>& w_body, const std::vector<int>& slot_part,
-                           const std::vector<int>& inc_ptr_g) {
+                           const std::vector<int>& inc_ptr_g,
+                           const std::vector<int>* comp = nullptr, int G = 1) {
+  const int Cg = B.C / G;  // CTAs per group (cluster)
   const int C = B.C;
   B.own_t.assign(D.nt, 0);
-  for (int t = 0; t < D.nt; ++t) B.own_t[t] = (int)((long)t * C / std::max(D.nt, 1));
+  if (!comp) {
+    for (int t = 0; t < D.nt; ++t) B.own_t[t] = (int)((long)t * C / std::max(D.nt, 1));
+  } else {
+    // contiguous tet ranges within each component
+    std::vector<int> n_k(G, 0), j_k(G, 0);
+    for (int t = 0; t < D.nt; ++t) ++n_k[(*comp)[tets[4 * (size_t)t]]];
+    for (int t = 0; t < D.nt; ++t) {
+      const int k = (*comp)[tets[4 * (size_t)t]];
+      B.own_t[t] = k * Cg + (int)((long)j_k[k]++ * Cg / std::max(n_k[k], 1));
+    }
+  }
   B.own_p.assign(D.P, -1);
   for (int t = 0; t < D.nt; ++t)
     for (int v = 0; v < 4; ++v) {
@@ -758,7 +776,8 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
       if (B.own_p[p] < 0) B.own_p[p] = B.own_t[t];
     }
   for (int p = 0; p < D.P; ++p)
-    if (B.own_p[p] < 0) B.own_p[p] = (int)((long)p * C / std::max(D.P, 1));
+    if (B.own_p[p] < 0)
+      B.own_p[p] = comp ? (*comp)[p] * Cg : (int)((long)p * C / std::max(D.P, 1));
   B.own_b.assign(D.nb, -1);
   for (int a = 0; a < D.na; ++a)
     if (B.own_b[a_b[a]] < 0) B.own_b[a_b[a]] = B.own_p[a_p[a]];
@@ -768,7 +787,7 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
       if (B.own_b[h_b[h]] < 0 && B.own_b[h_a[h]] >= 0) B.own_b[h_b[h]] = B.own_b[h_a[h]];
     }
   for (int b = 0; b < D.nb; ++b)
-    if (B.own_b[b] < 0) B.own_b[b] = b % C;
+    if (B.own_b[b] < 0) B.own_b[b] = comp ? (*comp)[D.P + b] * Cg : b % C;
   B.own_d.resize(D.nd);
   for (int d = 0; d < D.nd; ++d) B.own_d[d] = B.own_p[d_i[d]];
   B.own_a.resize(D.na);
@@ -807,7 +826,12 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
     for (int x : B.Lh[c]) { need(D.P + h_a[x]); need(D.P + h_b[x]); }
     for (int s : B.Ls[c]) {
       if (s < D.nw) need(D.P + w_body[s]);
-      else { need(slot_part[s - D.nw]); need(0); }
+      else {
+        need(slot_part[s - D.nw]);
+        // the padded columns reference DOF 0 with zero values (contact.py:210-214);
+        // another group's particle 0 is replaced by the slot's own particle
+        if (own_of(0) / Cg == c / Cg) need(0);
+      }
     }
     std::sort(h.begin(), h.end());
     h.erase(std::unique(h.begin(), h.end()), h.end());
@@ -827,7 +851,8 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
   };
   ClPlan& P = B.P;
   P = ClPlan{};
-  P.C = C;
+  P.C = Cg;
+  P.G = G;
   P.MT = mx(B.Lt); P.MD = mx(B.Ld); P.MA = mx(B.La); P.MH = mx(B.Lh); P.MS = mx(B.Ls);
   P.MP = mx(B.Lp); P.MB = mx(B.Lb);
   P.MW = 1;
@@ -860,7 +885,7 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
   P.oDyn = take(P.MS); P.oBdn = take(P.MS); P.oBdf = take(2 * P.MS);
   P.oResD = take(P.MD); P.oResA = take(3 * P.MA); P.oResH = take(5 * P.MH);
   P.oU = take(P.MDOFX); P.oV = take(P.MDOFX); P.oAng = take(9 * P.MB);
-  P.oRed = take(16 * C);
+  P.oRed = take(16 * Cg);
   P.smem_doubles = off;
   B.smem_bytes = 8 * (size_t)off;
 }
@@ -873,7 +898,8 @@ static int plan_upload(ss_handle* H, PlanBuild& B, const Dims& D, const std::vec
                        const std::vector<int>& w_body, const std::vector<int>& slot_part,
                        const std::vector<int>& inc_ptr_g, const std::vector<int>& inc_g) {
   ClPlan& P = B.P;
-  const int C = B.C;
+  const int C = B.C;       // CTAs over all groups
+  const int Cg = P.C;      // CTAs per group (cluster): DSMEM ranks
   auto own_of = [&](int gn) { return gn < D.P ? B.own_p[gn] : B.own_b[gn - D.P]; };
   // local U/V offset of a global node in CTA c (owned or halo)
   std::vector<std::vector<int>> halo_off(C);
@@ -906,7 +932,7 @@ static int plan_upload(ss_handle* H, PlanBuild& B, const Dims& D, const std::vec
       for (int k = inc_ptr_g[gn]; k < inc_ptr_g[gn + 1]; ++k) {
         const int code = inc_g[k];
         const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
-        const int d = (c << 24) | o;
+        const int d = ((c % Cg) << 24) | o;
         switch (fam) {
           case F_DIST: dst_d[2 * (size_t)e + v] = d; break;
           case F_TET: dst_t[4 * (size_t)e + v] = d; break;
@@ -950,7 +976,10 @@ static int plan_upload(ss_handle* H, PlanBuild& B, const Dims& D, const std::vec
     for (int x : B.Lh[c]) put(x, {D.P + h_a[x], D.P + h_b[x]}, {dst_h[2 * (size_t)x], dst_h[2 * (size_t)x + 1]});
     for (int s : B.Ls[c]) {
       if (s < D.nw) put(s, {D.P + w_body[s]}, {dst_cn[s], dst_cf[s]});
-      else put(s, {slot_part[s - D.nw], 0}, {dst_cn[s], dst_cf[s]});
+      else {
+        const int pz = own_of(0) / Cg == c / Cg ? 0 : slot_part[s - D.nw];
+        put(s, {slot_part[s - D.nw], pz}, {dst_cn[s], dst_cf[s]});
+      }
     }
   }
   // halo pushes: owner -> every consumer holding a halo copy
@@ -963,7 +992,7 @@ static int plan_upload(ss_handle* H, PlanBuild& B, const Dims& D, const std::vec
     int n = 0;
     auto emit = [&](int gn) {
       hp_ptr[(size_t)c * (P.MN + 1) + n] = (int)hpush.size();
-      for (auto& pr : consumers[gn]) hpush.push_back((pr.first << 24) | pr.second);
+      for (auto& pr : consumers[gn]) hpush.push_back(((pr.first % Cg) << 24) | pr.second);
       ++n;
     };
     for (int p : B.Lp[c]) emit(p);
@@ -994,6 +1023,12 @@ static int plan_upload(ss_handle* H, PlanBuild& B, const Dims& D, const std::vec
   return SS_OK;
 }
 
+// reductions one k_newton_cluster launch performs at most (exact mode: two
+// per PCR iteration, one per Newton tail)
+static int c_max_reductions(const ss_handle* H) {
+  return H->c.p.newton * (2 * std::max(H->c.p.pcr, 1) + 2) + 8;
+}
+
 // choose the smallest cluster whose shared-memory plan fits, or none
 static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i,
                         const std::vector<int>& d_j, const std::vector<int>& tets,
@@ -1004,21 +1039,62 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
                         int allow) {
   H->use_cluster = 0;
   if (!allow) return SS_OK;
-  // rows of the largest cluster (16 CTAs x CL_RPT rows x CL_THREADS threads): a
-  // larger scene (e.g. the 1M-tet snake) cannot fit, skip the partitioning
-  if ((long)D.m > 16L * CL_RPT * CL_THREADS) return SS_OK;
   int dev = H->device, max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t budget = (size_t)max_smem - 1024;  // static reduction scratch
+  // Multi-cluster plan (one env of G disconnected components, e.g. a coupled
+  // n-snake scene, build_snake(n_snakes=n)): component k in cluster k, the
+  // clusters combine their dot products through global memory.
+  std::vector<int> comp;
+  int G = 1;
+  if (D.E == 1 && D.n_real == 1 && env_long("SS_MULTI_CLUSTER", 1)) {
+    std::vector<int> par(D.P + D.nb);
+    for (size_t i = 0; i < par.size(); ++i) par[i] = (int)i;
+    auto root = [&](int x) {
+      while (par[x] != x) x = par[x] = par[par[x]];
+      return x;
+    };
+    auto join = [&](int x, int y) {
+      x = root(x);
+      y = root(y);
+      if (x != y) par[std::max(x, y)] = std::min(x, y);
+    };
+    for (int t = 0; t < D.nt; ++t)
+      for (int v = 1; v < 4; ++v) join(tets[4 * (size_t)t], tets[4 * (size_t)t + v]);
+    for (int e = 0; e < D.nd; ++e) join(d_i[e], d_j[e]);
+    for (int e = 0; e < D.na; ++e) join(a_p[e], D.P + a_b[e]);
+    for (int e = 0; e < D.nh; ++e) join(D.P + h_a[e], D.P + h_b[e]);
+    // components numbered in order of first appearance
+    comp.assign(par.size(), 0);
+    std::vector<int> seen(par.size(), -1);
+    G = 0;
+    for (size_t i = 0; i < par.size(); ++i) {
+      const int r = root((int)i);
+      if (seen[r] < 0) seen[r] = G++;
+      comp[i] = seen[r];
+    }
+  }
+  // rows of the largest cluster (16 CTAs x CL_RPT rows x CL_THREADS threads): a
+  // larger scene (e.g. the 1M-tet snake) cannot fit one cluster
+  const bool single_fits = (long)D.m <= 16L * CL_RPT * CL_THREADS;
+  const bool multi = G >= 2 && G <= 32;  // co-residency decides below
+  const bool dbg = env_long("SS_CLUSTER_DEBUG", 0) != 0;
+  if (dbg) fprintf(stderr, "[plan_cluster] components %d single_fits %d\n", G, (int)single_fits);
+  if (!single_fits && !multi) return SS_OK;
+  // multi-cluster first (each component gets a whole cluster), else one cluster
+  for (int Gp : {multi ? G : 0, single_fits ? 1 : 0})
   for (int C : {1, 2, 4, 8, 16}) {
+    if (Gp == 0) break;
     PlanBuild B;
-    B.C = C;
-    plan_partition(B, D, d_i, d_j, tets, a_p, a_b, h_a, h_b, w_body, slot_part, inc_ptr_g);
+    B.C = C * Gp;
+    plan_partition(B, D, d_i, d_j, tets, a_p, a_b, h_a, h_b, w_body, slot_part, inc_ptr_g,
+                   Gp > 1 ? &comp : nullptr, Gp);
+    if (dbg) fprintf(stderr, "[plan_cluster] G %d C %d smem %zu budget %zu\n", Gp, C, B.smem_bytes, budget);
     if (B.smem_bytes > budget) continue;
     // one element and one (node, axis) per thread; <= CL_RPT rows per thread
     {
       bool ok = B.P.NR <= CL_RPT * CL_THREADS;
-      for (int c2 = 0; c2 < C; ++c2) {
+      for (int c2 = 0; c2 < B.C; ++c2) {
         const size_t ne = B.Lt[c2].size() + B.Ld[c2].size() + B.La[c2].size() + B.Lh[c2].size() +
                           B.Ls[c2].size();
         if (ne > CL_THREADS || 3 * B.Lp[c2].size() + 6 * B.Lb[c2].size() > CL_THREADS) ok = false;
@@ -1037,10 +1113,13 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cfg.blockDim = dim3(CL_THREADS);
-    cfg.gridDim = dim3(C);
+    cfg.gridDim = dim3(B.C);
     cfg.dynamicSmemBytes = B.smem_bytes;
     int nclus = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclus, fn, &cfg) != cudaSuccess || nclus < 1) {
+    // every cluster of a multi-cluster env must be co-resident (they wait on each other)
+    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclus, fn, &cfg);
+    if (dbg) fprintf(stderr, "[plan_cluster] G %d C %d max active clusters %d (%d)\n", Gp, C, nclus, (int)oe);
+    if (oe != cudaSuccess || nclus < Gp) {
       cudaGetLastError();
       continue;
     }
@@ -1052,6 +1131,16 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
     if (getenv("SS_CLUSTER_STAMPS")) {
       CK(cudaMalloc(&H->plan.dbg, 64 * sizeof(long long)));
       CK(cudaMemset(H->plan.dbg, 0, 64 * sizeof(long long)));
+    }
+    if (Gp > 1) {
+      // cross-cluster reduction buffers: per reduction of a launch, G partials
+      // (4 doubles each) and an arrival counter (reset by a memset node per launch)
+      const int xn = c_max_reductions(H);
+      CK(cudaMalloc(&H->xmem, (size_t)xn * Gp * 4 * sizeof(double) + (size_t)(xn + 4) * sizeof(int)));
+      H->plan.xbuf = (double*)H->xmem;
+      H->plan.xcnt = (int*)(H->plan.xbuf + (size_t)xn * Gp * 4);
+      H->plan.xn = xn;
+      CK(cudaMemset(H->plan.xcnt, 0, (size_t)(xn + 4) * sizeof(int)));
     }
     H->use_cluster = 1;
     return SS_OK;
@@ -1707,6 +1796,7 @@ int ss_destroy(ss_handle* H) {
   if (H->d_stage) cudaFree(H->d_stage);
   if (H->d_init) cudaFree(H->d_init);
   if (H->plan_mem) cudaFree(H->plan_mem);
+  if (H->xmem) cudaFree(H->xmem);
   if (H->fplan_mem) cudaFree(H->fplan_mem);
   if (H->plan.dbg) cudaFree(H->plan.dbg);
   for (int l = 1; l < ss_handle::kMaxLanes; ++l) {
@@ -2196,6 +2286,12 @@ int ss_solver_info(ss_handle* H, int* info) {
   info[5] = H->fused;
   info[6] = H->fused ? H->fplan.n_blocks : 0;
   info[7] = H->fused ? H->fused_chunks : 0;
+  info[8] = H->use_cluster ? H->plan.G : 0;
+  info[9] = 0;
+  if (H->use_cluster && H->plan.G > 1) {
+    CK(cudaStreamSynchronize(H->stream));
+    CK(cudaMemcpy(&info[9], H->plan.xcnt + H->plan.xn, sizeof(int), cudaMemcpyDeviceToHost));
+  }
   return SS_OK;
 }
 

@@ -47,6 +47,10 @@ struct ClPlan {
   int oU, oV, oAng;                         // [MDOFX] (owned then halo DOFs) x2, [9][MB]
   int oRed;                                 // reduction partials [16][C]
   int smem_doubles;
+  int G;               // clusters per environment (multi-cluster plans: one per component)
+  double* xbuf;        // [xn][G][4] cluster partials of every reduction of a launch (G > 1)
+  int* xcnt;           // [xn] arrivals per reduction (+ [xn] error flag), reset per launch
+  int xn;
   long long* dbg;      // optional phase timestamps (nullptr = off)
   const int* cnt;      // [C][8]: nT nD nA nH nS nP nB -
   const int* elem;     // [C][ME]    family-local global index of each local element
@@ -142,6 +146,46 @@ DI void cl_cluster_sum3(const ClPlan& L, const ClSmem& S, const double* v, int s
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < 3; ++q) out[q] = scratch[48 + q];
+}
+
+// Multi-cluster environments (G > 1): the per-cluster totals v[0..n) (equal in
+// every CTA of a cluster) are combined across the G clusters through global
+// memory: rank 0 of each cluster publishes its totals for reduction `seq`,
+// then every CTA waits for the G arrivals and adds the partials in cluster
+// order (the same sum everywhere, deterministic). The wait is bounded: a
+// missing cluster (never the case when all are co-resident, which ss_create
+// checks) ends it after ~2^32 cycles with an error flag instead of a hang.
+DI void cl_xsum(const ClPlan& L, int grp, int rank, int& seq, double* v, int n, double* scratch) {
+  if (L.G <= 1) return;
+  const int r = seq++;
+  if (r >= L.xn) {  // more reductions than the plan sized for: flag, never hang
+    if (threadIdx.x == 0) L.xcnt[L.xn] = 2;
+    return;
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    for (int q = 0; q < n; ++q) L.xbuf[((size_t)r * L.G + grp) * 4 + q] = v[q];
+    __threadfence();
+    atomicAdd(&L.xcnt[r], 1);
+  }
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    while (*(volatile int*)&L.xcnt[r] < L.G) {
+      __nanosleep(32);
+      if (clock64() - t0 > (1LL << 32)) {
+        L.xcnt[L.xn] = 1;  // error flag
+        break;
+      }
+    }
+    __threadfence();
+    for (int q = 0; q < n; ++q) {
+      double t = 0.0;
+      for (int g2 = 0; g2 < L.G; ++g2) t += __ldcg(&L.xbuf[((size_t)r * L.G + g2) * 4 + q]);
+      scratch[56 + q] = t;
+    }
+  }
+  __syncthreads();
+  for (int q = 0; q < n; ++q) v[q] = scratch[56 + q];
+  __syncthreads();
 }
 
 // ------------------------------------------------------------ node gather
@@ -563,7 +607,12 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
   __shared__ double* peers[CL_MAXC];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
-  const int env = blockIdx.x / L.C;
+  // multi-cluster plans: G clusters per env, plan tables indexed by the
+  // env-local CTA index (cluster grp, rank within it)
+  const int gcta = blockIdx.x % (L.C * L.G);
+  const int grp = gcta / L.C;
+  const int env = blockIdx.x / (L.C * L.G);
+  int xseq = 0;  // cross-cluster reduction sequence of this launch
   const int E = c.D.E;
   const int tid = threadIdx.x;
   if (tid < L.C) peers[tid] = cl.map_shared_rank(sm_, tid);
@@ -571,8 +620,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
   S.b = sm_;
   S.peer = peers;
   double* sb = sm_;
-  const int* cnt = L.cnt + 8 * rank;
-  const int nEl = cl_nel(L, rank);
+  const int* cnt = L.cnt + 8 * gcta;
+  const int nEl = cl_nel(L, gcta);
   const int nP = cnt[5], nB = cnt[6];
   const double g = c.p.gamma, h = c.p.h;
 
@@ -580,11 +629,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
   const bool has_el = tid < nEl;
   ClMe me;
   if (has_el) {
-    me.el = cl_el(L, rank, tid);
+    me.el = cl_el(L, gcta, tid);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      me.ref[q] = L.eref[((size_t)rank * L.ME + tid) * 4 + q];
-      me.dst[q] = L.dest[((size_t)rank * L.ME + tid) * 4 + q];
+      me.ref[q] = L.eref[((size_t)gcta * L.ME + tid) * 4 + q];
+      me.dst[q] = L.dest[((size_t)gcta * L.ME + tid) * 4 + q];
     }
     me.dyn = 0.0;
     if (me.el.fam == CF_DIST) me.dyn = c.T.d_dyn[me.el.g];
@@ -602,7 +651,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
       mn.width = 3;
       mn.base = 3 * n;
       mn.lb = -1;
-      mn.im = c.T.inv_mass[L.node[(size_t)rank * L.MN + n]];
+      mn.im = c.T.inv_mass[L.node[(size_t)gcta * L.MN + n]];
     } else {
       const int q = tid - 3 * nP;
       n = nP + q / 6;
@@ -610,10 +659,10 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
       mn.width = 6;
       mn.lb = q / 6;
       mn.base = 3 * nP + 6 * mn.lb;
-      mn.im = c.T.body_inv_mass[L.node[(size_t)rank * L.MN + n] - c.D.P];
+      mn.im = c.T.body_inv_mass[L.node[(size_t)gcta * L.MN + n] - c.D.P];
     }
-    const int* iptr = L.in_ptr + (size_t)rank * (L.MN + 1);
-    const int* hptr = L.hp_ptr + (size_t)rank * (L.MN + 1);
+    const int* iptr = L.in_ptr + (size_t)gcta * (L.MN + 1);
+    const int* hptr = L.hp_ptr + (size_t)gcta * (L.MN + 1);
     mn.k0 = L.oIn + iptr[n];
     mn.k1 = L.oIn + iptr[n + 1];
     mn.hp0 = hptr[n];
@@ -684,7 +733,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
     }
   }
   for (int n = tid; n < nP + nB; n += CL_THREADS) {
-    const int gn = L.node[(size_t)rank * L.MN + n];
+    const int gn = L.node[(size_t)gcta * L.MN + n];
     if (n < nP) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) sb[L.oV + 3 * n + a] = c.K.v[IX(3 * gn + a)];
@@ -909,6 +958,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
         CL_STAMP(5);
         double tot[3];
         cl_cluster_sum3(L, S, part, rslot, scratch, tot);
+        cl_xsum(L, grp, rank, xseq, tot, 3, scratch);
         rslot = (rslot + 3) & 15;
         CL_STAMP(6);
         if (k == 0) {
@@ -1028,7 +1078,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
           }
         }
         CL_STAMP(5);
-        const double rho_new = cl_cluster_sum(L, S, part, rslot, scratch);
+        double rho_new = cl_cluster_sum(L, S, part, rslot, scratch);
+        cl_xsum(L, grp, rank, xseq, &rho_new, 1, scratch);
         rslot = (rslot + 1) & 15;
         CL_STAMP(6);
         if (!broken) {
@@ -1061,7 +1112,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
           }
         }
         CL_STAMP(7);
-        const double den = cl_cluster_sum(L, S, dpart, rslot, scratch);
+        double den = cl_cluster_sum(L, S, dpart, rslot, scratch);
+        cl_xsum(L, grp, rank, xseq, &den, 1, scratch);
         rslot = (rslot + 1) & 15;
         CL_STAMP(8);
         if (!broken) {
@@ -1141,7 +1193,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
       }
       cl_contrib<EXACT>(c, L, S, me, dlam, 1);
     }
-    const double rz = cl_cluster_sum(L, S, rzp, rslot, scratch);
+    double rz = cl_cluster_sum(L, S, rzp, rslot, scratch);
+    cl_xsum(L, grp, rank, xseq, &rz, 1, scratch);
     rslot = (rslot + 1) & 15;
     resid = sqrt(0.0 > rz ? 0.0 : rz);
     // the reduction's cluster barrier also published the dlam column sums
@@ -1151,7 +1204,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
 
   // ---- write back
   for (int n = tid; n < nP + nB; n += CL_THREADS) {
-    const int gn = L.node[(size_t)rank * L.MN + n];
+    const int gn = L.node[(size_t)gcta * L.MN + n];
     if (n < nP) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) c.K.v[IX(3 * gn + a)] = sb[L.oV + 3 * n + a];
@@ -1161,6 +1214,6 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
       for (int k = 0; k < 6; ++k) c.K.v[IX(o + k)] = sb[L.oV + 3 * nP + 6 * lb + k];
     }
   }
-  if (rank == 0 && tid == 0) c.S.resid[env] = resid;
+  if (gcta == 0 && tid == 0) c.S.resid[env] = resid;
   cl.sync();  // no CTA may exit while peers can still access its shared memory
 }

@@ -185,5 +185,7 @@ def benchmark(scene, snake_counts=(1, 2, 3, 4), frames: int = 60, warmup: int = 
                      "frames": frames, "assembly_ms": total_ms * asm / tot,
                      "solve_ms": total_ms * (tot - asm) / tot, "total_ms": total_ms,
                      "total_ms_std": float(np.std(times)), "total_per_snake_ms": total_ms / count,
-                     "solver": "cluster" if sim.solver_info["cluster"] else "streaming"})
+                     "solver": "cluster" if sim.solver_info["cluster"] else "streaming",
+                     "cluster_size": sim.solver_info["cluster_size"],
+                     "clusters_per_env": sim.solver_info["clusters_per_env"]})
     return rows

@@ -444,11 +444,12 @@ class BatchedSimulator:
 
     @property
     def solver_info(self) -> dict:
-        info = (C.c_int * 8)()
+        info = (C.c_int * 10)()
         _native.check(_native.lib().ss_solver_info(self._ensure(), info))
         return {"cluster": bool(info[0]), "cluster_size": info[1], "smem_bytes": info[2],
                 "env_lanes": info[3], "waves": info[4], "fused_gather": bool(info[5]),
-                "fused_blocks": info[6], "fused_chunks": info[7]}
+                "fused_blocks": info[6], "fused_chunks": info[7], "clusters_per_env": info[8],
+                "cross_cluster_fault": info[9]}
 
     @property
     def launches_per_frame(self) -> int:

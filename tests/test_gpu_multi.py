@@ -36,6 +36,9 @@ def test_two_coupled_snakes_vs_reference(exact):
     cfg.exact_jacobian = exact
     sim = M.Simulator(config=cfg, **parts)
     assert sim.n_links == 8
+    info = sim.solver_info
+    if os.environ.get("SS_MULTI_CLUSTER", "1") != "0":
+        assert info["clusters_per_env"] == 2  # one cluster per snake (component)
     for f in g["frames_captured"]:
         sim.set_state_arrays(golden_frame(g, f, "before"), 0, 1)
         st = sim.step(g[f"f{f}.commands"], latency=True)
@@ -43,6 +46,7 @@ def test_two_coupled_snakes_vs_reference(exact):
                            what=f"S2 frame {f}")
         assert (st.newton_iterations, st.pcr_iterations, st.contact_count,
                 st.inverted_tets) == tuple(g[f"f{f}.stats"])
+    assert sim.solver_info["cross_cluster_fault"] == 0
 
 
 def test_two_coupled_snakes_vs_oracle(oracle_mod):
@@ -76,3 +80,31 @@ def test_coupling_is_real():
     n0 = p1.shape[0]
     d = np.max(np.abs(p2[:n0, [0, 2]] - p1[:, [0, 2]]))  # y is offset by the spacing
     assert d > 1e-12
+
+
+def test_multi_cluster_matches_single_cluster(monkeypatch):
+    """The multi-cluster plan (one cluster per snake, cross-cluster dot
+    products through global memory in cluster order) against the plan the
+    scene gets without it (S2 does not fit one cluster: the streaming
+    kernels) over several frames: same Newton/PCR decisions, states within
+    round-off of the summation-order change."""
+    g = load_golden("step_S2.npz")
+    parts, cfg = scene_parts("S2")
+    runs = {}
+    for mc in ("1", "0"):
+        monkeypatch.setenv("SS_MULTI_CLUSTER", mc)
+        sim = M.Simulator(config=cfg, **parts)
+        runs[mc] = (sim, sim.solver_info["clusters_per_env"])
+    assert runs["1"][1] == 2 and runs["0"][1] in (0, 1)
+    b = golden_frame(g, 0, "before")
+    for sim, _ in runs.values():
+        sim.set_state_arrays(b, 0, 1)
+    for f in range(4):
+        cmds = g["f0.commands"]
+        st = [sim.step(cmds, latency=True) for sim, _ in runs.values()]
+        assert (st[0].newton_iterations, st[0].pcr_iterations) == \
+            (st[1].newton_iterations, st[1].pcr_iterations)
+    a = _one(runs["1"][0].get_state_arrays(0, 1))
+    b1 = _one(runs["0"][0].get_state_arrays(0, 1))
+    assert_state_close(a, b1, what="multi vs single cluster")
+    assert runs["1"][0].solver_info["cross_cluster_fault"] == 0

@@ -9,4 +9,5 @@ from paper_1904_02833_b200 import rollout  # noqa: E402
 
 counts = tuple(int(x) for x in sys.argv[1:]) or (1, 2, 4)
 rows = rollout.benchmark(M.SceneConfig(), counts, frames=30, warmup=5)
-print(" ".join(f"{r['snakes']}:{r['total_ms']:.3f}ms({r['solver'][0]})" for r in rows))
+print(" ".join(f"{r['snakes']}:{r['total_ms']:.3f}ms({r['solver'][0]}"
+               f"{r['clusters_per_env']}x{r['cluster_size']})" for r in rows))
