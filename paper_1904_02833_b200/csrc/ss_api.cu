@@ -355,8 +355,8 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       cfg.gridDim = dim3(H->plan.C * H->plan.G * D.E);
       cfg.dynamicSmemBytes = 8 * (size_t)H->plan.smem_doubles;
       cfg.stream = st;
-      if (H->plan.G > 1)  // cross-cluster arrival counters of this launch
-        CK(cudaMemsetAsync(H->plan.xcnt, 0, sizeof(int) * (size_t)H->plan.xn, st));
+      if (H->plan.G > 1)  // cross-cluster tagged words of this launch
+        CK(cudaMemsetAsync(H->plan.xbuf, 0, (size_t)H->plan.xn * H->plan.G * kClXWords * 16, st));
       CK(cudaLaunchKernelEx(&cfg, k_newton_cluster<EX>, c, H->plan));
       if (prof) {
         cudaEventRecord(e1_, st);
@@ -1041,7 +1041,7 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
   if (!allow) return SS_OK;
   int dev = H->device, max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t budget = (size_t)max_smem - 1024;  // static reduction scratch
+  const size_t budget = (size_t)max_smem - 2048;  // static reduction scratch
   // Multi-cluster plan (one env of G disconnected components, e.g. a coupled
   // n-snake scene, build_snake(n_snakes=n)): component k in cluster k, the
   // clusters combine their dot products through global memory.
@@ -1077,7 +1077,7 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
   // rows of the largest cluster (16 CTAs x CL_RPT rows x CL_THREADS threads): a
   // larger scene (e.g. the 1M-tet snake) cannot fit one cluster
   const bool single_fits = (long)D.m <= 16L * CL_RPT * CL_THREADS;
-  const bool multi = G >= 2 && G <= 32;  // co-residency decides below
+  const bool multi = G >= 2 && G <= kClMaxGroups;  // co-residency decides below
   const bool dbg = env_long("SS_CLUSTER_DEBUG", 0) != 0;
   if (dbg) fprintf(stderr, "[plan_cluster] components %d single_fits %d\n", G, (int)single_fits);
   if (!single_fits && !multi) return SS_OK;
@@ -1136,11 +1136,12 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
       // cross-cluster reduction buffers: per reduction of a launch, G partials
       // (4 doubles each) and an arrival counter (reset by a memset node per launch)
       const int xn = c_max_reductions(H);
-      CK(cudaMalloc(&H->xmem, (size_t)xn * Gp * 4 * sizeof(double) + (size_t)(xn + 4) * sizeof(int)));
+      const size_t xb = (size_t)xn * Gp * kClXWords * 16;
+      CK(cudaMalloc(&H->xmem, xb + 16));
+      CK(cudaMemset(H->xmem, 0, xb + 16));
       H->plan.xbuf = (double*)H->xmem;
-      H->plan.xcnt = (int*)(H->plan.xbuf + (size_t)xn * Gp * 4);
+      H->plan.xcnt = (int*)((char*)H->xmem + xb);
       H->plan.xn = xn;
-      CK(cudaMemset(H->plan.xcnt, 0, (size_t)(xn + 4) * sizeof(int)));
     }
     H->use_cluster = 1;
     return SS_OK;
@@ -2290,7 +2291,7 @@ int ss_solver_info(ss_handle* H, int* info) {
   info[9] = 0;
   if (H->use_cluster && H->plan.G > 1) {
     CK(cudaStreamSynchronize(H->stream));
-    CK(cudaMemcpy(&info[9], H->plan.xcnt + H->plan.xn, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&info[9], H->plan.xcnt, sizeof(int), cudaMemcpyDeviceToHost));
   }
   return SS_OK;
 }

@@ -48,8 +48,8 @@ struct ClPlan {
   int oRed;                                 // reduction partials [16][C]
   int smem_doubles;
   int G;               // clusters per environment (multi-cluster plans: one per component)
-  double* xbuf;        // [xn][G][4] cluster partials of every reduction of a launch (G > 1)
-  int* xcnt;           // [xn] arrivals per reduction (+ [xn] error flag), reset per launch
+  double* xbuf;        // [xn][G][4] 16-byte tagged words: cluster partials of every reduction (G > 1)
+  int* xcnt;           // [0] cross-cluster error flag (sticky)
   int xn;
   long long* dbg;      // optional phase timestamps (nullptr = off)
   const int* cnt;      // [C][8]: nT nD nA nH nS nP nB -
@@ -150,41 +150,57 @@ DI void cl_cluster_sum3(const ClPlan& L, const ClSmem& S, const double* v, int s
 
 // Multi-cluster environments (G > 1): the per-cluster totals v[0..n) (equal in
 // every CTA of a cluster) are combined across the G clusters through global
-// memory: rank 0 of each cluster publishes its totals for reduction `seq`,
-// then every CTA waits for the G arrivals and adds the partials in cluster
-// order (the same sum everywhere, deterministic). The wait is bounded: a
-// missing cluster (never the case when all are co-resident, which ss_create
-// checks) ends it after ~2^32 cycles with an error flag instead of a hang.
+// memory, flag-in-data: rank 0 of each cluster stores every total as one
+// 16-byte word {lo, tag, hi, tag} (tag = reduction index + 1; the buffer is
+// zeroed per launch), and in every CTA one thread per (cluster, total) polls
+// that word until both tags are present — 8-byte halves are single-copy
+// atomic, so a word with both tags holds both halves of the total — then the
+// partials are added in cluster order (the same sum everywhere,
+// deterministic). One L2 round trip, no fences, no atomics. The wait is
+// bounded: a missing cluster (never the case when all are co-resident, which
+// ss_create checks) ends it after ~2^32 cycles with an error flag instead of
+// a hang.
+constexpr int kClMaxGroups = 16;  // scratch[64 + 4 g + q] holds cluster g's totals
+constexpr int kClXWords = 4;      // 16-byte words per (reduction, cluster)
 DI void cl_xsum(const ClPlan& L, int grp, int rank, int& seq, double* v, int n, double* scratch) {
   if (L.G <= 1) return;
   const int r = seq++;
   if (r >= L.xn) {  // more reductions than the plan sized for: flag, never hang
-    if (threadIdx.x == 0) L.xcnt[L.xn] = 2;
+    if (threadIdx.x == 0) L.xcnt[0] = 2;
     return;
   }
-  if (rank == 0 && threadIdx.x == 0) {
-    for (int q = 0; q < n; ++q) L.xbuf[((size_t)r * L.G + grp) * 4 + q] = v[q];
-    __threadfence();
-    atomicAdd(&L.xcnt[r], 1);
+  const unsigned tag = (unsigned)r + 1u;
+  uint4* slots = reinterpret_cast<uint4*>(L.xbuf) + (size_t)r * L.G * kClXWords;
+  if (rank == 0 && (int)threadIdx.x < n) {
+    const int q = threadIdx.x;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v[q]);
+    uint4* w = slots + grp * kClXWords + q;
+    asm volatile("st.relaxed.gpu.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(w),
+                 "r"((unsigned)bits), "r"(tag), "r"((unsigned)(bits >> 32)), "r"(tag)
+                 : "memory");
   }
-  if (threadIdx.x == 0) {
+  if ((int)threadIdx.x < L.G * n) {
+    const int g = threadIdx.x / n, q = threadIdx.x % n;
+    const uint4* w = slots + g * kClXWords + q;
+    unsigned a, b, c, d;
     const long long t0 = clock64();
-    while (*(volatile int*)&L.xcnt[r] < L.G) {
-      __nanosleep(32);
+    while (true) {
+      asm volatile("ld.relaxed.gpu.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(w) : "memory");
+      if (b == tag && d == tag) break;
       if (clock64() - t0 > (1LL << 32)) {
-        L.xcnt[L.xn] = 1;  // error flag
+        L.xcnt[0] = 1;
         break;
       }
     }
-    __threadfence();
-    for (int q = 0; q < n; ++q) {
-      double t = 0.0;
-      for (int g2 = 0; g2 < L.G; ++g2) t += __ldcg(&L.xbuf[((size_t)r * L.G + g2) * 4 + q]);
-      scratch[56 + q] = t;
-    }
+    scratch[64 + 4 * g + q] = __longlong_as_double((long long)(((unsigned long long)c << 32) | a));
   }
   __syncthreads();
-  for (int q = 0; q < n; ++q) v[q] = scratch[56 + q];
+  for (int q = 0; q < n; ++q) {
+    double t = 0.0;
+    for (int g = 0; g < L.G; ++g) t += scratch[64 + 4 * g + q];
+    v[q] = t;
+  }
   __syncthreads();
 }
 
@@ -603,7 +619,7 @@ template <bool EXACT>
 __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, const ClPlan L) {
   pdl_wait();
   extern __shared__ __align__(16) double sm_[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[64 + 4 * kClMaxGroups];
   __shared__ double* peers[CL_MAXC];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
