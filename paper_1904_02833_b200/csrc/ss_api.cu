@@ -316,12 +316,22 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const double* xc_z = c.K.z + (size_t)D.ms * D.E;
   const double* xs_dl = c.K.az;
   const double* xc_dl = c.K.az + (size_t)D.ms * D.E;
-#define GATHER(mode, xs, xc)                                        \
-  do {                                                              \
-    if (gsp == 8) LAUNCH(k_gather<8>, g_gather, c, mode, xs, xc);    \
-    else if (gsp == 4) LAUNCH(k_gather<4>, g_gather, c, mode, xs, xc); \
-    else if (gsp == 2) LAUNCH(k_gather<2>, g_gather, c, mode, xs, xc); \
-    else LAUNCH(k_gather<1>, g_gather, c, mode, xs, xc);             \
+  // tet column sums in incidence order (one large mesh): separate
+  // instantiations of the kernels that write or read them
+  const bool ib = D.tc_inbox != 0;
+#define GATHER(mode, xs, xc)                                           \
+  do {                                                                 \
+    if (ib) {                                                          \
+      if (gsp == 8) LAUNCH(k_gather<24>, g_gather, c, mode, xs, xc);      \
+      else if (gsp == 4) LAUNCH(k_gather<20>, g_gather, c, mode, xs, xc); \
+      else if (gsp == 2) LAUNCH(k_gather<18>, g_gather, c, mode, xs, xc); \
+      else LAUNCH(k_gather<17>, g_gather, c, mode, xs, xc);               \
+    } else {                                                           \
+      if (gsp == 8) LAUNCH(k_gather<8>, g_gather, c, mode, xs, xc);       \
+      else if (gsp == 4) LAUNCH(k_gather<4>, g_gather, c, mode, xs, xc);  \
+      else if (gsp == 2) LAUNCH(k_gather<2>, g_gather, c, mode, xs, xc);  \
+      else LAUNCH(k_gather<1>, g_gather, c, mode, xs, xc);                \
+    }                                                                  \
   } while (0)
   // has_cmd: 0 no commands, 1 commands in d_cmd, 2 on-device gait generator
   const int gait = has_cmd == 2 ? 1 : 0;
@@ -372,7 +382,10 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
     nv_asm = nullptr;
     for (int it = 0; it < c.p.newton; ++it) {
       NvtxRange nv_newton("newton", prof != nullptr);
-      if (!EX && H->newton2) LAUNCH(k_newton_rhs2, g_el, c);
+      if (!EX && H->newton2) {
+        if (ib) LAUNCH(k_newton_rhs2<1>, g_el, c);
+        else LAUNCH(k_newton_rhs2<0>, g_el, c);
+      }
       else LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
       if (H->keep && sub == c.p.substeps - 1 && it == c.p.newton - 1)
         CK(cudaMemcpyAsync(c.K.snap_rhs, c.K.r, 8 * (size_t)D.m * D.E, cudaMemcpyDeviceToDevice,
@@ -420,7 +433,8 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
             CK(cudaMemsetAsync(c.K.jctr, 0, sizeof(int) * (1 + 2 * (size_t)jp.tiles), st));
             LAUNCH(k_jtg, dim3(H->jtg_grid), c, jp);
           } else {
-            if (D.nt) LAUNCH(k_tet_jt<EX>, g_tet, c);
+            if (D.nt && ib) LAUNCH(k_tet_jt<EX ? 3 : 2>, g_tet, c);
+            else if (D.nt) LAUNCH(k_tet_jt<EX ? 1 : 0>, g_tet, c);
             GATHER(0, xs_z, xc_z);
           }
           }
@@ -428,8 +442,11 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
           DIR(0);
         }
       }
-      if (!EX && H->newton2)
-        LAUNCH(k_newton_final2, g_red2, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
+      if (!EX && H->newton2 && ib)
+        LAUNCH(k_newton_final2<1>, g_red2, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
+               c.p.pcr == 1 ? 1 : 0);
+      else if (!EX && H->newton2)
+        LAUNCH(k_newton_final2<0>, g_red2, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
                c.p.pcr == 1 ? 1 : 0);
       else
         LAUNCH(k_newton_final<EX>, g_red, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
@@ -1396,6 +1413,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   }
   std::vector<int> inc_ptr((size_t)D.P + D.nb + 1, 0), inc;
   std::vector<int2> inc_tet((size_t)D.P);
+  std::vector<int> tdst(4 * (size_t)D.nt, 0);  // incidence of each tet vertex
   for (size_t i = 0; i < lists.size(); ++i) {
     std::stable_sort(lists[i].begin(), lists[i].end(),
                      [](const Inc& a, const Inc& b) { return a.key < b.key; });
@@ -1405,10 +1423,17 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
       const int rank = (int)(lists[i][k].key >> 40);
       if (rank == 1 && tb < 0) tb = inc_ptr[i] + (int)k;
       if (rank == 1) te = inc_ptr[i] + (int)k + 1;
-      inc.push_back(lists[i][k].code);
+      const int code = lists[i][k].code;
+      if ((int)((unsigned)code >> 29) == F_TET)
+        tdst[4 * (size_t)(code & 0x1FFFFFF) + ((code >> 25) & 15)] = inc_ptr[i] + (int)k;
+      inc.push_back(code);
     }
     if (i < (size_t)D.P) inc_tet[i] = make_int2(tb, te);
   }
+  D.n_inc = (int)inc.size();
+  // one large mesh: tet column sums in incidence order (ss_device.cuh tc_put;
+  // SS_TC_INBOX=0 keeps the component-major [12][nt] layout)
+  D.tc_inbox = (D.E == 1 && env_long("SS_TC_INBOX", 1)) ? 1 : 0;
 
   // ---- allocations
   ss_handle* H = new ss_handle();
@@ -1462,6 +1487,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     T.inc_ptr = A.take<int>((size_t)D.P + D.nb + 1);
     T.inc = A.take<int>(inc.size());
     T.inc_tet = A.take<int2>((size_t)D.P);
+    T.tdst = A.take<int>(4 * (size_t)D.nt);
   };
   plan_topo(ta);
   ta.cap = ta.off;
@@ -1512,6 +1538,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   rc |= up(T.inc_ptr, inc_ptr.data(), 4 * inc_ptr.size());
   rc |= up(T.inc, inc.data(), 4 * inc.size());
   rc |= up(T.inc_tet, inc_tet.data(), sizeof(int2) * inc_tet.size());
+  rc |= up(T.tdst, tdst.data(), 4 * tdst.size());
   if (rc) {
     ss_destroy(H);
     return SS_ECUDA;
@@ -1588,7 +1615,8 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.ang_inv = A.take<double>(9 * (size_t)D.nb * Es);
     K.res = A.take<double>((size_t)D.ms * Es);
     K.tS = A.take<double>(6 * (size_t)D.nt * Es);
-    K.tC = A.take<double>(12 * (size_t)D.nt * Es);
+    K.tC = D.tc_inbox ? A.take<double>(4 * (size_t)D.n_inc)
+                      : A.take<double>(12 * (size_t)D.nt * Es);
     K.rw = A.take<double>(3 * (size_t)D.na * Es);
     K.hJ = A.take<double>(60 * (size_t)D.nh * Es);
     K.wJ = A.take<double>(18 * (size_t)D.nw * Es);

@@ -33,6 +33,7 @@ struct Dims {
   int P, nb, ndof, bd0, nd, nt, na, nh, nw, nq, ns, nch, links;
   int ms, m, od, ot, oa, oh, on, of;
   int act_enabled;
+  int tc_inbox, n_inc;  // tet column sums in incidence order (E = 1), incidences
 };
 
 struct Par {
@@ -57,6 +58,7 @@ struct Topo {
   const int* slot_part;                                           // [nq]
   const int *inc_ptr, *inc;                                       // [P+nb+1], codes
   const int2* inc_tet;                                            // [P] tet run [begin, end)
+  const int* tdst;                                                // [nt][4] incidence of each tet vertex
 };
 
 // persistent per-environment state, [item][E]
@@ -148,6 +150,62 @@ DI void pdl_wait() {
 // stay coalesced for k_tet_jt's stores (the tet-major order costs the 1M-tet
 // scene 9%).
 #define TCX(k, t) (E >= 32 ? ((size_t)(t) * 12 + (k)) * E + env : ((size_t)(k) * nt + (t)) * E + env)
+// One large mesh (E = 1, c.D.tc_inbox): the column sums of tet t's vertex v
+// are stored at that vertex's incidence k = tdst[4 t + v] of the J^T list,
+// tC[4k .. 4k+2] (one 32-byte sector per incidence, 256-bit store): a node's
+// tet run [inc_tet.x, inc_tet.y) is then consecutive sectors, read by the
+// gather with 256-bit loads in the same order as before (same sums, bitwise).
+// The scattered access moves from the gather's 8-byte reads (three
+// component arrays, 1M tets apart) to k_tet_jt's full-sector writes.
+DI void tc_st4(double* p, double a0, double a1, double a2) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a0), "d"(a1), "d"(a2),
+               "d"(0.0) : "memory");
+}
+DI void tc_ld4(const double* p, double& a0, double& a1, double& a2) {
+  double q[4];
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(q[0]), "=d"(q[1]), "=d"(q[2]), "=d"(q[3])
+      : "l"(p));
+  a0 = q[0];
+  a1 = q[1];
+  a2 = q[2];
+}
+// the 3 column sums of (tet t, vertex v). IB: 1 inbox layout, 0 the TCX
+// layout, -1 decided at run time (c.D.tc_inbox); the hot kernels are
+// instantiated per layout so the batched path carries no inbox code.
+template <int IB = -1>
+DI void tc_put(const Ctx& c, int t, int v, int env, double a0, double a1, double a2) {
+  const int E = c.D.E, nt = c.D.nt;
+  if (IB < 0 ? c.D.tc_inbox != 0 : IB == 1) {
+    tc_st4(c.K.tC + 4 * (size_t)__ldg(&c.T.tdst[4 * (size_t)t + v]), a0, a1, a2);
+  } else {
+    c.K.tC[TCX(3 * v, t)] = a0;
+    c.K.tC[TCX(3 * v + 1, t)] = a1;
+    c.K.tC[TCX(3 * v + 2, t)] = a2;
+  }
+}
+template <int IB = -1>
+DI void tc_put12(const Ctx& c, int t, int env, const double* col12) {
+  if constexpr (IB == 0) {
+    const int E = c.D.E, nt = c.D.nt;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) tc_put<IB>(c, t, v, env, col12[3 * v], col12[3 * v + 1], col12[3 * v + 2]);
+  }
+}
+// the 3 column sums of incidence k (= tet e's vertex v)
+template <int IB = -1>
+DI void tc_get(const Ctx& c, int k, int v, int e, int env, double& a0, double& a1, double& a2) {
+  const int E = c.D.E, nt = c.D.nt;
+  if (IB < 0 ? c.D.tc_inbox != 0 : IB == 1) {
+    tc_ld4(c.K.tC + 4 * (size_t)k, a0, a1, a2);
+  } else {
+    a0 = c.K.tC[TCX(3 * v, e)];
+    a1 = c.K.tC[TCX(3 * v + 1, e)];
+    a2 = c.K.tC[TCX(3 * v + 2, e)];
+  }
+}
 
 // ------------------------------------------------------------ small math
 // numpy.maximum: NaN in a propagates
@@ -765,13 +823,17 @@ DI void tet_rinv(const Ctx& c, int t, double* Ri) {
 
 // J^T x for one tet: the 12 column sums acc_j = sum_i J[i][j] x_i in the
 // reference's accumulation order (numba_backend.py:43-52), written to tC
+template <int IB = -1>
 DI void tet_contrib(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
                     const double* x6) {
   const int E = c.D.E, nt = c.D.nt;
+  (void)E;
+  (void)nt;
 #pragma unroll 1
   for (int v = 0; v < 4; ++v) {
     double wv[3];
     tet_wv(Ri, v, wv);
+    double acc3[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       double col[6];
@@ -779,8 +841,9 @@ DI void tet_contrib(const Ctx& c, int t, int env, const TetC& T, const double* R
       double acc = 0.0;
 #pragma unroll
       for (int i = 0; i < 6; ++i) acc += col[i] * x6[i];
-      c.K.tC[TCX(3 * v + a, t)] = acc;
+      acc3[a] = acc;
     }
+    tc_put<IB>(c, t, v, env, acc3[0], acc3[1], acc3[2]);
   }
 }
 
@@ -852,13 +915,18 @@ DI void tet_jt_cols(const TetC& T, const double* Ri, const double* z, double* co
     for (int a = 0; a < 3; ++a) col12[3 * v + a] = dot3(R[3 * a], q0, R[3 * a + 1], q1, R[3 * a + 2], q2);
   }
 }
+template <int IB = -1>
 DI void tet_contrib_fast(const Ctx& c, int t, int env, const TetC& T, const double* Ri,
                          const double* z) {
   const int E = c.D.E, nt = c.D.nt;
   double col12[12];
   tet_jt_cols(T, Ri, z, col12);
+  if constexpr (IB == 0) {
 #pragma unroll
-  for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
+    for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
+  } else {
+    tc_put12<IB>(c, t, env, col12);
+  }
 }
 
 // J u of one tet from its 4 node values uv[3v+a] (structured chain rule):
@@ -920,10 +988,10 @@ DI void tet_forward_fast(const Ctx& c, int t, int env, const TetC& T, const doub
 }
 
 // EXACT selects the materialised-column path (bitwise numba sums)
-template <bool EXACT>
+template <bool EXACT, int IB = -1>
 DI void tet_jt(const Ctx& c, int t, int env, const TetC& T, const double* Ri, const double* x6) {
-  if (EXACT) tet_contrib(c, t, env, T, Ri, x6);
-  else tet_contrib_fast(c, t, env, T, Ri, x6);
+  if (EXACT) tet_contrib<IB>(c, t, env, T, Ri, x6);
+  else tet_contrib_fast<IB>(c, t, env, T, Ri, x6);
 }
 template <bool EXACT>
 DI void tet_j(const Ctx& c, int t, int env, const TetC& T, const double* Ri, const double* vec,
@@ -1163,16 +1231,15 @@ __global__ void k_eval_misc(const Ctx c) {
 // One incidence (code = (fam<<29)|(v<<25)|e) of a particle's / a body's
 // J^T list: its contribution to the DOF's w (block_transpose,
 // numba_backend.py:43-52, per row); false when the row is inactive.
-DI bool inc_particle(const Ctx& c, int code, int mode, const double* __restrict__ xs,
+template <int IB = -1>
+DI bool inc_particle(const Ctx& c, int k, int code, int mode, const double* __restrict__ xs,
                      const double* __restrict__ xc, int env, double& a0, double& a1,
                      double& a2) {
   const int E = c.D.E, nt = c.D.nt, na = c.D.na, ns = c.D.ns;
   (void)nt;
   const int fam = (int)((unsigned)code >> 29), v = (code >> 25) & 15, e = code & 0x1FFFFFF;
   if (fam == F_TET) {
-    a0 = c.K.tC[TCX(3 * v, e)];
-    a1 = c.K.tC[TCX(3 * v + 1, e)];
-    a2 = c.K.tC[TCX(3 * v + 2, e)];
+    tc_get<IB>(c, k, v, e, env, a0, a1, a2);
   } else if (fam == F_DIST) {
     const int nd = c.D.nd;
     const double xr = xs[IX(c.D.od + e)];
@@ -1297,10 +1364,13 @@ DI void gather_body_out(const Ctx& c, int b, int mode, const double* w, int env)
 // latency-bound (one CTA column per 256 DOFs), this gives it SPLIT× the
 // loads in flight. Not the reference's summation order (exact mode keeps
 // SPLIT = 1).
-template <int SPLIT>
+// G = SPLIT | 16 * inbox layout
+template <int G>
 __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx c, int mode,
                                                        const double* __restrict__ xs,
                                                        const double* __restrict__ xc) {
+  constexpr int SPLIT = G & 15;
+  constexpr int IB = G >> 4;
   SETUP
   const int P = c.D.P, nt = c.D.nt, na = c.D.na, nh = c.D.nh, nw = c.D.nw, ns = c.D.ns;
   if constexpr (SPLIT > 1) {
@@ -1316,7 +1386,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
         if (it < P) {
           for (int k = k0 + sub; k < k1; k += SPLIT) {
             double a0, a1, a2;
-            if (!inc_particle(c, c.T.inc[k], mode, xs, xc, env, a0, a1, a2)) continue;
+            if (!inc_particle<IB>(c, k, c.T.inc[k], mode, xs, xc, env, a0, a1, a2)) continue;
             w[0] += a0;
             w[1] += a1;
             w[2] += a2;
@@ -1383,13 +1453,18 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
           constexpr int GU = SS_GATHER_UNROLL;
           for (; k + GU - 1 < tr.y; k += GU) {
             double a[3 * GU];
+            if (IB) {
 #pragma unroll
-            for (int j = 0; j < GU; ++j) {
-              const int code = c.T.inc[k + j];
-              const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
-              a[3 * j] = tC[TCX(3 * v, e)];
-              a[3 * j + 1] = tC[TCX(3 * v + 1, e)];
-              a[3 * j + 2] = tC[TCX(3 * v + 2, e)];
+              for (int j = 0; j < GU; ++j) tc_ld4(tC + 4 * (size_t)(k + j), a[3 * j], a[3 * j + 1], a[3 * j + 2]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < GU; ++j) {
+                const int code = c.T.inc[k + j];
+                const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
+                a[3 * j] = tC[TCX(3 * v, e)];
+                a[3 * j + 1] = tC[TCX(3 * v + 1, e)];
+                a[3 * j + 2] = tC[TCX(3 * v + 2, e)];
+              }
             }
 #pragma unroll
             for (int j = 0; j < GU; ++j) {
@@ -1401,9 +1476,11 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
           for (; k < tr.y; ++k) {
             const int code = c.T.inc[k];
             const int v = (code >> 25) & 15, e = code & 0x1FFFFFF;
-            w0 += tC[TCX(3 * v, e)];
-            w1 += tC[TCX(3 * v + 1, e)];
-            w2 += tC[TCX(3 * v + 2, e)];
+            double a0, a1, a2;
+            tc_get<IB>(c, k, v, e, env, a0, a1, a2);
+            w0 += a0;
+            w1 += a1;
+            w2 += a2;
           }
           if (k >= k1) break;
         }
@@ -1438,7 +1515,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
           }
         }
 #endif
-        if (!inc_particle(c, code, mode, xs, xc, env, a0, a1, a2)) continue;
+        if (!inc_particle<IB>(c, k, code, mode, xs, xc, env, a0, a1, a2)) continue;
         w0 += a0;
         w1 += a1;
         w2 += a2;
@@ -1606,7 +1683,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_JTG_MINB) k_jtg(const Ctx c, co
               if (k >= k1) break;
             }
             double a0, a1, a2;
-            if (!inc_particle(c, c.T.inc[k], 0, xs, xc, env, a0, a1, a2)) continue;
+            if (!inc_particle(c, k, c.T.inc[k], 0, xs, xc, env, a0, a1, a2)) continue;
             w0 += a0;
             w1 += a1;
             w2 += a2;
@@ -2935,8 +3012,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_STEPJT_MINB) k_step_jt(const Ct
 #pragma unroll
         for (int q = 0; q < 6; ++q) z6[q] = zs[q * 32];
         tet_jt_cols(T, Ri, z6, col12);
-#pragma unroll
-        for (int kk = 0; kk < 12; ++kk) c.K.tC[TCX(kk, t)] = col12[kk];
+        tc_put12(c, t, env, col12);
       }
     }
     buf ^= 1;
@@ -2971,12 +3047,15 @@ __global__ void __launch_bounds__(SS_THREADS, SS_STEPJT_MINB) k_step_jt(const Ct
   }
 }
 
-// tet column sums of J^T z for the next apply (after k_pcr_step)
-template <bool EXACT>
+// tet column sums of J^T z for the next apply (after k_pcr_step);
+// M = EXACT | 2 * inbox layout
 #ifndef SS_TETJT_MINB
 #define SS_TETJT_MINB 3
 #endif
-__global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : SS_TETJT_MINB) k_tet_jt(const Ctx c) {
+template <int M>
+__global__ void __launch_bounds__(SS_THREADS, (M & 1) ? 2 : SS_TETJT_MINB) k_tet_jt(const Ctx c) {
+  constexpr bool EXACT = (M & 1) != 0;
+  constexpr int IB = (M >> 1) & 1;
   SETUP
   if (c.K.broken[env]) return;  // z unchanged: tC from the previous pass is still valid
   const int nt = c.D.nt;
@@ -2987,7 +3066,7 @@ __global__ void __launch_bounds__(SS_THREADS, EXACT ? 2 : SS_TETJT_MINB) k_tet_j
     TetC T;
     tet_load(c, t, env, T);
     tet_rinv(c, t, Ri);
-    tet_jt<EXACT>(c, t, env, T, Ri, z6);
+    tet_jt<EXACT, IB>(c, t, env, T, Ri, z6);
   }
 }
 
@@ -3135,6 +3214,7 @@ __global__ void SS_FINAL_MINB_LB k_newton_final(const Ctx c, int do_step, int la
 #ifndef SS_NEWTON2_MINB
 #define SS_NEWTON2_MINB 3
 #endif
+template <int IB>
 __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(const Ctx c) {
   SETUP
   __shared__ double gsh[4][9][32];   // G (A -> B)
@@ -3203,10 +3283,9 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(con
         const double q0 = dot3(Z00, wv[0], Z01, wv[1], Z02, wv[2]) - __fma_rn(n1, wv[2], -n2 * wv[1]);
         const double q1 = dot3(Z01, wv[0], Z11, wv[1], Z12, wv[2]) - __fma_rn(n2, wv[0], -n0 * wv[2]);
         const double q2 = dot3(Z02, wv[0], Z12, wv[1], Z22, wv[2]) - __fma_rn(n0, wv[1], -n1 * wv[0]);
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-          if (tw_act)
-            c.K.tC[TCX(3 * vv + a, t)] = dot3(R[3 * a], q0, R[3 * a + 1], q1, R[3 * a + 2], q2);
+        if (tw_act)
+          tc_put<IB>(c, t, vv, env, dot3(R[0], q0, R[1], q1, R[2], q2),
+                 dot3(R[3], q0, R[4], q1, R[5], q2), dot3(R[6], q0, R[7], q1, R[8], q2));
       }
     } else {
       double sv[6], lm[6], bd[6];
@@ -3299,6 +3378,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_rhs2(con
   }
 }
 
+template <int IB>
 __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_final2(const Ctx c, int do_step,
                                                                                int last, int first) {
   SETUP
@@ -3357,10 +3437,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_NEWTON2_MINB) k_newton_final2(c
 #pragma unroll
       for (int q = 0; q < 6; ++q) d6[q] = ds[q * 32];
       tet_jt_cols(T, Ri, d6, col12);
-      if (tw_act) {
-#pragma unroll
-        for (int k = 0; k < 12; ++k) c.K.tC[TCX(k, t)] = col12[k];
-      }
+      if (tw_act) tc_put12<IB>(c, t, env, col12);
     }
     named_bar(1 + pair, 64);  // ds consumed before the next item overwrites it
   }

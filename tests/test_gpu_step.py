@@ -556,3 +556,29 @@ def test_newton2_bitwise(n):
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
     assert np.allclose(res["0"], res["1"], rtol=1e-10, atol=0.0)
+
+
+@pytest.mark.parametrize("exact", [False, True], ids=["structuredJ", "exactJ"])
+def test_tc_inbox_bitwise(exact):
+    """One env on the streaming kernels: tet column sums stored in incidence
+    order (SS_TC_INBOX, 256-bit sector per incidence) give bitwise the state
+    of the component-major tC layout (the gather adds the same values in
+    the same order)."""
+    import os
+    out = {}
+    for mode in ("0", "1"):
+        parts, cfg = scene_parts("S")  # fresh state: the drop-in steps it in place
+        cfg.solver = "streaming"
+        cfg.exact_jacobian = exact
+        os.environ["SS_TC_INBOX"] = mode
+        try:
+            sim = M.Simulator(config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_TC_INBOX", None)
+        for i in range(3):
+            sim.step(M.gait_commands(M.GaitParams(), i * cfg.dt, 4, 4), latency=True)
+        out[mode] = sim.get_state_arrays(0, 1)
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
