@@ -325,7 +325,8 @@ int ss_solver_info(ss_handle* h, int* info);
  * bounds write), or -1 when the handle has no guards. */
 int ss_check_guards(ss_handle* h, int64_t* bad_bytes);
 /* Debug: clock64 phase stamps of one PCR iteration of the cluster solver
- * (handle created with SS_CLUSTER_STAMPS set); out[16]. */
+ * (handle created with SS_CLUSTER_STAMPS=n set): out[16 n], 16 per CTA for
+ * the first n (<= 16) CTAs. */
 int ss_cluster_stamps(ss_handle* h, long long* out);
 /* Kernel names (static strings) of the step, in profiler slot order;
  * returns the number of kernels. */

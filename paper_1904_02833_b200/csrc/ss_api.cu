@@ -844,10 +844,11 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
     for (int s : B.Ls[c]) {
       if (s < D.nw) need(D.P + w_body[s]);
       else {
+        // the padded columns reference DOF 0 with zero values (contact.py:210-214):
+        // read from its owner's shared memory at apply time (plan_upload), not
+        // pushed to every CTA as a halo copy (the owner's gather would push it
+        // to every other CTA of the cluster each PCR iteration)
         need(slot_part[s - D.nw]);
-        // the padded columns reference DOF 0 with zero values (contact.py:210-214);
-        // another group's particle 0 is replaced by the slot's own particle
-        if (own_of(0) / Cg == c / Cg) need(0);
       }
     }
     std::sort(h.begin(), h.end());
@@ -994,8 +995,16 @@ static int plan_upload(ss_handle* H, PlanBuild& B, const Dims& D, const std::vec
     for (int s : B.Ls[c]) {
       if (s < D.nw) put(s, {D.P + w_body[s]}, {dst_cn[s], dst_cf[s]});
       else {
-        const int pz = own_of(0) / Cg == c / Cg ? 0 : slot_part[s - D.nw];
-        put(s, {slot_part[s - D.nw], pz}, {dst_cn[s], dst_cf[s]});
+        // particle 0 of this cluster: local copy, or -1 - (owner rank << 24 | offset)
+        // in the owner's U/V arrays (another group's particle 0 is replaced by the
+        // slot's own particle)
+        const int sp = slot_part[s - D.nw];
+        put(s, {sp, sp}, {dst_cn[s], dst_cf[s]});
+        if (own_of(0) / Cg == c / Cg) {
+          const int o0 = own_of(0);
+          eref[((size_t)c * P.ME + e - 1) * 4 + 1] =
+              o0 == c ? local_off(c, 0) : -1 - (((o0 % Cg) << 24) | local_off(o0, 0));
+        }
       }
     }
   }
@@ -1140,14 +1149,31 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
       cudaGetLastError();
       continue;
     }
+    if (dbg) {
+      for (int c2 = 0; c2 < B.C; ++c2) {
+        int mx_inc = 0, n_inc = 0;
+        for (int p : B.Lp[c2]) {
+          mx_inc = std::max(mx_inc, inc_ptr_g[p + 1] - inc_ptr_g[p]);
+          n_inc += inc_ptr_g[p + 1] - inc_ptr_g[p];
+        }
+        int mx_b = 0;
+        for (int b : B.Lb[c2]) mx_b = std::max(mx_b, inc_ptr_g[D.P + b + 1] - inc_ptr_g[D.P + b]);
+        fprintf(stderr,
+                "[plan_cluster] cta %2d: tets %d dist %d att %d hinge %d slots %d | particles %d "
+                "bodies %d halo %zu | inc %d max/particle %d max/body %d\n",
+                c2, (int)B.Lt[c2].size(), (int)B.Ld[c2].size(), (int)B.La[c2].size(),
+                (int)B.Lh[c2].size(), (int)B.Ls[c2].size(), (int)B.Lp[c2].size(),
+                (int)B.Lb[c2].size(), B.halo[c2].size(), n_inc, mx_inc, mx_b);
+      }
+    }
     int rc = plan_upload(H, B, D, d_i, d_j, tets, a_p, a_b, h_a, h_b, w_body, slot_part,
                          inc_ptr_g, inc_g);
     if (rc) return rc;
     H->plan = B.P;
     H->plan.dbg = nullptr;
     if (getenv("SS_CLUSTER_STAMPS")) {
-      CK(cudaMalloc(&H->plan.dbg, 64 * sizeof(long long)));
-      CK(cudaMemset(H->plan.dbg, 0, 64 * sizeof(long long)));
+      CK(cudaMalloc(&H->plan.dbg, 256 * sizeof(long long)));  // [CTA < 16][16]
+      CK(cudaMemset(H->plan.dbg, 0, 256 * sizeof(long long)));
     }
     if (Gp > 1) {
       // cross-cluster reduction buffers: per reduction of a launch, G partials
@@ -2286,7 +2312,8 @@ int64_t ss_device_bytes(ss_handle* H) { return H ? (int64_t)H->bytes : 0; }
 int ss_cluster_stamps(ss_handle* H, long long* out) {
   if (!H || !out) return fail(SS_EINVAL, "null argument");
   if (!H->plan.dbg) return fail(SS_EINVAL, "stamps off (set SS_CLUSTER_STAMPS)");
-  CK(cudaMemcpy(out, H->plan.dbg, 16 * sizeof(long long), cudaMemcpyDeviceToHost));
+  const long n = std::max(1L, std::min(16L, env_long("SS_CLUSTER_STAMPS", 1)));
+  CK(cudaMemcpy(out, H->plan.dbg, 16 * n * sizeof(long long), cudaMemcpyDeviceToHost));
   return SS_OK;
 }
 

@@ -67,85 +67,72 @@ struct ClSmem {
   double* const* peer;   // shared-memory table of every CTA's base (incl. self)
 };
 
-// fixed-order block sum over CL_THREADS threads (warp shuffles down, then
-// the 16 warp sums in warp order); result valid in every thread
-DI double cl_block_sum(double v, double* scratch) {
+// The fixed shuffle-down tree over 32 lanes (lane i < n holds src[i], the
+// rest 0) evaluated by one thread for lane 0: the same additions in the
+// same order as __shfl_down_sync with offsets 16..1, depth 5 (n <= 16).
+DI double cl_tree16(const double* src, int n) {
+  double v[16];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) scratch[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x < 32) {
-    s = threadIdx.x < (CL_THREADS >> 5) ? scratch[threadIdx.x] : 0.0;
+  for (int i = 0; i < 16; ++i) v[i] = (i < n ? src[i] : 0.0) + 0.0;  // offset 16: zeros
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) scratch[32] = s;
+  for (int o = 8; o > 0; o >>= 1) {
+#pragma unroll
+    for (int i = 0; i < o; ++i) v[i] += v[i + o];
   }
-  __syncthreads();
-  return scratch[32];
+  return v[0];
 }
 
-// cluster-wide deterministic sum: block sum, pushed by thread 0 into slot
-// `slot` of every CTA (DSMEM stores), cluster barrier, then the C partials
-// are added in rank order by one fixed shuffle tree (same result in every
-// CTA). Slots rotate over 16, so a slot is rewritten only 15 barriers later.
-DI double cl_cluster_sum(const ClPlan& L, const ClSmem& S, double v, int slot, double* scratch) {
-  const double bs = cl_block_sum(v, scratch);
-  const int rank = (int)cg::this_cluster().block_rank();
-  if (threadIdx.x < L.C) S.peer[threadIdx.x][L.oRed + slot * L.C + rank] = bs;
-  cg::this_cluster().sync();
-  if (threadIdx.x < 32) {
-    double t = threadIdx.x < L.C ? S.b[L.oRed + slot * L.C + threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-    if (threadIdx.x == 0) scratch[33] = t;
-  }
-  __syncthreads();
-  return scratch[33];
-}
-
-// three cluster-wide sums in one barrier (slots slot, slot+1, slot+2 mod 16)
-DI void cl_cluster_sum3(const ClPlan& L, const ClSmem& S, const double* v, int slot,
+// Cluster-wide deterministic sums of N values (the same result in every
+// CTA): per-warp shuffle trees (N independent chains), the CL_THREADS/32 warp
+// partials combined by N*C threads at once — thread (q, dst) evaluates value
+// q's warp tree and pushes the CTA partial to slot (slot + q) mod 16 of CTA
+// dst (DSMEM store) — one cluster barrier, then the C partials combined by
+// the same tree. The sums are bitwise those of the former shuffle-tree
+// implementation (warp 0 reducing, then broadcasting), with one
+// __syncthreads and two shuffle trees fewer on the critical path
+// (tools/micro/cluster_sync.cu). Slots rotate over 16, so a slot is
+// rewritten only 15 barriers later.
+template <int N>
+DI void cl_cluster_sumN(const ClPlan& L, const ClSmem& S, const double* v, int slot,
                         double* scratch, double* out) {
-  double w[3];
+  constexpr int NW = CL_THREADS >> 5;
+  double w[N];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    w[q] = v[q];
+  for (int q = 0; q < N; ++q) w[q] = v[q];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) w[q] += __shfl_down_sync(0xffffffffu, w[q], o);
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) w[q] += __shfl_down_sync(0xffffffffu, w[q], o);
   }
   const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0)
+  if (l == 0) {
 #pragma unroll
-    for (int q = 0; q < 3; ++q) scratch[q * 16 + wi] = w[q];
+    for (int q = 0; q < N; ++q) scratch[q * NW + wi] = w[q];
+  }
   __syncthreads();
   const int rank = (int)cg::this_cluster().block_rank();
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      double t = threadIdx.x < (CL_THREADS >> 5) ? scratch[q * 16 + threadIdx.x] : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (threadIdx.x < L.C) S.peer[threadIdx.x][L.oRed + ((slot + q) & 15) * L.C + rank] = t;
-    }
+  static_assert(NW == 16, "warp tree over 16 warp partials");
+  if ((int)threadIdx.x < N * L.C) {
+    const int q = threadIdx.x / L.C, dst = threadIdx.x - q * L.C;
+    S.peer[dst][L.oRed + ((slot + q) & 15) * L.C + rank] = cl_tree16(scratch + q * NW, NW);
   }
   cg::this_cluster().sync();
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      double t = threadIdx.x < L.C ? S.b[L.oRed + ((slot + q) & 15) * L.C + threadIdx.x] : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-      if (threadIdx.x == 0) scratch[48 + q] = t;
-    }
+  if ((int)threadIdx.x < N) {
+    const int q = threadIdx.x;
+    scratch[48 + q] = cl_tree16(S.b + L.oRed + ((slot + q) & 15) * L.C, L.C);
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < 3; ++q) out[q] = scratch[48 + q];
+  for (int q = 0; q < N; ++q) out[q] = scratch[48 + q];
+}
+DI double cl_cluster_sum(const ClPlan& L, const ClSmem& S, double v, int slot, double* scratch) {
+  double o;
+  cl_cluster_sumN<1>(L, S, &v, slot, scratch, &o);
+  return o;
+}
+DI void cl_cluster_sum3(const ClPlan& L, const ClSmem& S, const double* v, int slot,
+                        double* scratch, double* out) {
+  cl_cluster_sumN<3>(L, S, v, slot, scratch, out);
 }
 
 // Multi-cluster environments (G > 1): the per-cluster totals v[0..n) (equal in
@@ -566,7 +553,10 @@ DI int cl_forward(const Ctx& c, const ClPlan& L, const ClSmem& S, const ClMe& me
         }
       } else {
         // padded columns reference DOF 0 (contact.py:210-214): particle 0's x
-        const double* p0 = cl_dofp(S, ref[1], arr);
+        // particle 0 (padded columns): local, or read from its owner CTA
+        const int r1 = ref[1];
+        const double* p0 = r1 >= 0 ? cl_dofp(S, r1, arr)
+                                   : S.peer[(unsigned)(-1 - r1) >> 24] + arr + ((-1 - r1) & 0xFFFFFF);
         const double x0 = p[0], x1 = p[1], x2 = p[2], z0 = p0[0];
         double a = 0.0;
         a += 0.0 * x0; a += 0.0 * x1; a += 1.0 * x2; a += 0.0 * z0; a += 0.0 * z0; a += 0.0 * z0;
@@ -611,8 +601,8 @@ DI double cl_ddiv(double x, double dstored) { return EXACT ? x / dstored : x * d
 #define CL_RPT 5
 #define CL_STAMP(id)                                                                    \
   do {                                                                                  \
-    if (L.dbg && blockIdx.x == 0 && threadIdx.x == 0 && itn == 1 && k == 3)             \
-      L.dbg[id] = clock64();                                                            \
+    if (L.dbg && blockIdx.x < 16 && threadIdx.x == 0 && itn == 1 && k == 3)             \
+      L.dbg[16 * blockIdx.x + (id)] = clock64();                                        \
   } while (0)
 
 template <bool EXACT>
@@ -913,10 +903,18 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
           cl_contrib<EXACT>(c, L, S, me, zr, 0);
         }
         CL_STAMP(1);
+        if (L.dbg) {  // stamps: every warp of the CTA done
+          __syncthreads();
+          CL_STAMP(10);
+        }
         cl.sync();                            // column sums of J^T z visible
         CL_STAMP(2);
         cl_gather(L, S, has_na, mn, 0);       // U = M^-1 J^T z (+ halo pushes)
         CL_STAMP(3);
+        if (L.dbg) {
+          __syncthreads();
+          CL_STAMP(11);
+        }
         cl.sync();                            // U visible
         CL_STAMP(4);
         double part[3] = {0.0, 0.0, 0.0};
@@ -972,6 +970,10 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
           }
         }
         CL_STAMP(5);
+        if (L.dbg) {
+          __syncthreads();
+          CL_STAMP(12);
+        }
         double tot[3];
         cl_cluster_sum3(L, S, part, rslot, scratch, tot);
         cl_xsum(L, grp, rank, xseq, tot, 3, scratch);
