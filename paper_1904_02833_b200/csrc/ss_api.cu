@@ -144,6 +144,8 @@ struct ss_handle {
   int stepjt = 0;            // k_step_jt (step + tet J^T z in one pass; SS_STEPJT)
   int newton2 = 0;           // k_newton_rhs2 / k_newton_final2 (SS_NEWTON2)
   int gy_dir2 = 1;
+  int gather_bulk = 0;       // k_gather_bulk (one large mesh: TMA bulk-copied tC; SS_GATHER_BULK)
+  int gbulk_grid = 0;
   JtgPlan jplan{};           // k_jtg plan (fixed at ss_create)
   size_t apply_async_smem = 0;
   std::vector<std::pair<char*, size_t>> guards;  // SS_GUARD spans
@@ -196,8 +198,8 @@ const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots", 
                                     "k_tet_jt",      "k_newton_cluster", "k_gather_fused",
                                     "k_apply_rows_async", "k_jtg", "k_apply_rows2",
                                     "k_pcr_dir_rows", "k_eval_polar", "k_step_jt",
-                                    "k_newton_rhs2", "k_newton_final2"};
-constexpr int kNumKernels = 23;
+                                    "k_newton_rhs2", "k_newton_final2", "k_gather_bulk"};
+constexpr int kNumKernels = 24;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -322,7 +324,9 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
 #define GATHER(mode, xs, xc)                                           \
   do {                                                                 \
     if (ib) {                                                          \
-      if (gsp == 8) LAUNCH(k_gather<24>, g_gather, c, mode, xs, xc);      \
+      if (gsp == 1 && H->gather_bulk)                                  \
+        LAUNCH_SM(k_gather_bulk, dim3(H->gbulk_grid), kGbSmem, c, mode, xs, xc); \
+      else if (gsp == 8) LAUNCH(k_gather<24>, g_gather, c, mode, xs, xc); \
       else if (gsp == 4) LAUNCH(k_gather<20>, g_gather, c, mode, xs, xc); \
       else if (gsp == 2) LAUNCH(k_gather<18>, g_gather, c, mode, xs, xc); \
       else LAUNCH(k_gather<17>, g_gather, c, mode, xs, xc);               \
@@ -1808,6 +1812,17 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // opt-in: no gain measured (coupled 2-snake frame 6.16 ms either way; 1024 envs and
   // the 1M-tet scene within noise, profiles/r2_summary.md)
   H->pdl = (int)env_long("SS_PDL", 0);
+  // one large mesh: the J^T x gather streams each warp's tet-run range of the
+  // incidence-order column sums with bulk copies (bitwise the serial walk)
+  if (D.tc_inbox && env_long("SS_GATHER_BULK", 1)) {
+    CK(cudaFuncSetAttribute(k_gather_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kGbSmem));
+    int occ = 1, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather_bulk, SS_THREADS, kGbSmem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
+    H->gbulk_grid = (int)env_long("SS_GB_GRID", (long)std::max(1, occ) * sms);
+    H->gather_bulk = 1;
+  }
   {
     int occ = 3, sms = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_jtg, SS_THREADS, 0);

@@ -161,6 +161,19 @@ DI void tc_st4(double* p, double a0, double a1, double a2) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a0), "d"(a1), "d"(a2),
                "d"(0.0) : "memory");
 }
+// Streaming loads of data read once per launch (compact tet J, z rows,
+// quaternions): read-only path without an L1 allocation, so the L1 keeps the
+// gathered DOF vector u (each node line is read by ~12 tets).
+// SS_NO_LDHINTS restores plain loads.
+DI double ld_stream(const double* p) {
+#ifdef SS_NO_LDHINTS
+  return *p;
+#else
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#endif
+}
 DI void tc_ld4(const double* p, double& a0, double& a1, double& a2) {
   double q[4];
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(q[0]), "=d"(q[1]), "=d"(q[2]), "=d"(q[3])
@@ -1547,6 +1560,172 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
   }
 }
 
+// ------------------------------- bulk-copy J^T x gather (one large mesh, E = 1)
+// With the incidence-order column sums (tc_inbox) the tet runs of 32
+// consecutive particles are ONE contiguous byte range of tC: [lo, hi) =
+// [first particle's run start, last particle's run end) x 32 B. A warp takes
+// 32 particles; lane 0 streams that range into a per-warp shared-memory ring
+// in windows of SS_GB_WIN incidences with cp.async.bulk (TMA bulk copy,
+// completion counted on an mbarrier), SS_GB_NBUF windows in flight; every
+// lane then adds its own particle's entries from shared memory in incidence
+// order. Each particle's sum is the same sequence of additions as k_gather's
+// serial walk (non-tet entries before and after the run from global memory,
+// as there), so u / v are bitwise k_gather<17>'s. The serial walk issued one
+// scattered 32-byte load per incidence and lane; here the tC stream moves as
+// 4 KB copies (1M-tet scene: 10.0 -> 8.6 ms/frame). Measured and not kept
+// (profiles/r2_summary.md): whole-span buffers per warp (~20 KB, 9 warps/SM),
+// chunk-pipelined double buffers with the non-tet operands of the next chunk
+// in flight (5 warps/SM): 10.6-13.9 ms/frame — the walk needs the warps.
+#ifndef SS_GB_WIN
+#define SS_GB_WIN 128  // incidences per window (32 B each)
+#endif
+#ifndef SS_GB_NBUF
+#define SS_GB_NBUF 2
+#endif
+#ifndef SS_GB_MINB
+#define SS_GB_MINB 3
+#endif
+#define SS_GB_WARPS (SS_THREADS / 32)
+constexpr size_t kGbSmem = (size_t)SS_GB_WARPS * SS_GB_NBUF * SS_GB_WIN * 32;
+
+DI uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+DI void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+DI bool mbar_try_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// lane 0 of a warp: arm the barrier for `bytes` and start the bulk copy
+DI void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(SS_THREADS, SS_GB_MINB) k_gather_bulk(const Ctx c, int mode,
+                                                        const double* __restrict__ xs,
+                                                        const double* __restrict__ xc) {
+  pdl_wait();
+  extern __shared__ __align__(128) double gb_smem[];
+  __shared__ uint64_t gbar[SS_GB_WARPS][SS_GB_NBUF];
+  const int E = 1, env = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = c.D.P;
+  if (lane == 0) {
+#pragma unroll
+    for (int b = 0; b < SS_GB_NBUF; ++b) mbar_init(&gbar[warp][b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  double* ring = gb_smem + (size_t)warp * SS_GB_NBUF * SS_GB_WIN * 4;
+  const double* tC = c.K.tC;
+  uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+  const int nchunks = (P + 31) >> 5;
+  for (int ch = blockIdx.x * SS_GB_WARPS + warp; ch < nchunks; ch += gridDim.x * SS_GB_WARPS) {
+    const int it = ch * 32 + lane;
+    const bool act = it < P;
+    int k0 = 0, k1 = 0;
+    int2 tr = make_int2(-1, -1);
+    if (act) {
+      k0 = c.T.inc_ptr[it];
+      k1 = c.T.inc_ptr[it + 1];
+      tr = c.T.inc_tet[it];
+    }
+    const bool has_run = tr.x >= 0 && tr.y > tr.x;
+    const int lo = __reduce_min_sync(0xffffffffu, has_run ? tr.x : INT_MAX);
+    const int hi = __reduce_max_sync(0xffffffffu, has_run ? tr.y : INT_MIN);
+    const int nwin = lo == INT_MAX ? 0 : (hi - lo + SS_GB_WIN - 1) / SS_GB_WIN;
+    if (lane == 0) {
+      for (int w = 0; w < SS_GB_NBUF && w < nwin; ++w) {
+        const int wlo = lo + w * SS_GB_WIN, wn = min(SS_GB_WIN, hi - wlo);
+        bulk_load(ring + (size_t)w * SS_GB_WIN * 4, tC + 4 * (size_t)wlo, 32u * wn, &gbar[warp][w]);
+      }
+    }
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+    double a0, a1, a2;
+    // entries before the tet run (distance rows), while the first windows land
+    const int kpre = has_run ? tr.x : k1;
+    for (int k = k0; k < kpre; ++k) {
+      if (!inc_particle<1>(c, k, c.T.inc[k], mode, xs, xc, env, a0, a1, a2)) continue;
+      w0 += a0;
+      w1 += a1;
+      w2 += a2;
+    }
+    for (int w = 0; w < nwin; ++w) {
+      const int b = w % SS_GB_NBUF;
+      while (!mbar_try_wait(&gbar[warp][b], (phase >> b) & 1u)) {
+      }
+      phase ^= 1u << b;
+      const int wlo = lo + w * SS_GB_WIN, whi = min(wlo + SS_GB_WIN, hi);
+      if (has_run) {
+        const double* sb = ring + (size_t)b * SS_GB_WIN * 4;
+        const int ka = max(tr.x, wlo), kb = min(tr.y, whi);
+        for (int k = ka; k < kb; ++k) {
+          const double2 v01 = *reinterpret_cast<const double2*>(sb + 4 * (k - wlo));
+          const double v2 = sb[4 * (k - wlo) + 2];
+          w0 += v01.x;
+          w1 += v01.y;
+          w2 += v2;
+        }
+      }
+      // the warp's generic-proxy reads of buffer b are done (syncwarp); the
+      // fence orders them before the async-proxy refill (this window's
+      // successor, or the next chunk's first windows)
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (w + SS_GB_NBUF < nwin) {
+          const int nlo = lo + (w + SS_GB_NBUF) * SS_GB_WIN, nn = min(SS_GB_WIN, hi - nlo);
+          bulk_load(ring + (size_t)b * SS_GB_WIN * 4, tC + 4 * (size_t)nlo, 32u * nn,
+                    &gbar[warp][b]);
+        }
+      }
+    }
+    if (!act) continue;
+    for (int k = has_run ? tr.y : k1; k < k1; ++k) {
+      if (!inc_particle<1>(c, k, c.T.inc[k], mode, xs, xc, env, a0, a1, a2)) continue;
+      w0 += a0;
+      w1 += a1;
+      w2 += a2;
+    }
+    const double im = c.T.inv_mass[it];
+    const double u0 = im * w0, u1 = im * w1, u2 = im * w2;
+    if (mode == 0) {
+      c.K.u[IX(3 * it)] = u0;
+      c.K.u[IX(3 * it + 1)] = u1;
+      c.K.u[IX(3 * it + 2)] = u2;
+    } else {
+      c.K.v[IX(3 * it)] += u0;
+      c.K.v[IX(3 * it + 1)] += u1;
+      c.K.v[IX(3 * it + 2)] += u2;
+    }
+  }
+  // rigid bodies: k_gather's body walk
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < c.D.nb; b += gridDim.x * blockDim.x) {
+    const int k0 = c.T.inc_ptr[P + b], k1 = c.T.inc_ptr[P + b + 1];
+    double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = k0; k < k1; ++k) {
+      double acc[6];
+      if (!inc_body(c, c.T.inc[k], mode, xs, xc, env, acc)) continue;
+#pragma unroll
+      for (int kk = 0; kk < 6; ++kk) w[kk] += acc[kk];
+    }
+    gather_body_out(c, b, mode, w, env);
+  }
+}
+
 // ------------------------------------ persistent tile-pipelined J^T z gather
 // k_tet_jt + k_gather<1> (mode 0) of one PCR iteration as ONE persistent
 // launch over a queue of work items, per 32-env tile: P1(T) pieces compute
@@ -2590,7 +2769,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       }
       const double* qp = c.S.quat + tb;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) q[k] = qp[k * ntE];
+      for (int k = 0; k < 4; ++k) q[k] = ld_stream(qp + k * ntE);
       tet_rinv(c, tc, Ri);
       // tet_forward_uv, first half: du, L, G
       double du[9];
@@ -2616,10 +2795,10 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       double sv[6], zz[6];
       const double* sp = c.K.tS + tb;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) sv[k] = sp[k * ntE];
+      for (int k = 0; k < 6; ++k) sv[k] = ld_stream(sp + k * ntE);
       const double* zp = z + ((unsigned)c.D.ot * uE + tb);
 #pragma unroll
-      for (int i = 0; i < 6; ++i) zz[i] = zp[i * ntE];
+      for (int i = 0; i < 6; ++i) zz[i] = ld_stream(zp + i * ntE);
       const double ed = c.T.t_e3[tc], eo = c.T.t_e3[nt + tc], es = c.T.t_e3[2 * nt + tc];
       double S[9], Ki[9];
       S[0] = sv[0]; S[4] = sv[1]; S[8] = sv[2];

@@ -38,7 +38,7 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
     # round-2 kernels that move the same operands as their round-1 twins
     kernel = {"k_apply_rows2": "k_apply_rows", "k_apply_rows_async": "k_apply_rows",
               "k_pcr_dir_rows": "k_pcr_dir", "k_newton_rhs2": "k_newton_rhs",
-              "k_newton_final2": "k_newton_final"}.get(kernel, kernel)
+              "k_newton_final2": "k_newton_final", "k_gather_bulk": "k_gather"}.get(kernel, kernel)
     rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches
     jc = F8 * 10 * d["nt"]                       # compact tet J: quat(4) S(6); R, K^-1 rebuilt
     tc = F8 * 12 * d["nt"]                       # tet column sums J^T x

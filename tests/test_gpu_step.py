@@ -582,3 +582,31 @@ def test_tc_inbox_bitwise(exact):
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("exact", [False, True], ids=["structuredJ", "exactJ"])
+def test_gather_bulk_bitwise(exact):
+    """One env, serial J^T x walk (SS_GATHER_SPLIT=1): the bulk-copy gather
+    (k_gather_bulk, each warp's tet-run range of the incidence-order column
+    sums streamed into shared memory with cp.async.bulk) gives bitwise the
+    state of the per-lane walk (k_gather<17>)."""
+    import os
+    out = {}
+    for mode in ("0", "1"):
+        parts, cfg = scene_parts("S")
+        cfg.solver = "streaming"
+        cfg.exact_jacobian = exact
+        os.environ["SS_GATHER_BULK"] = mode
+        os.environ["SS_GATHER_SPLIT"] = "1"
+        try:
+            sim = M.Simulator(config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_GATHER_BULK", None)
+            os.environ.pop("SS_GATHER_SPLIT", None)
+        for i in range(3):
+            sim.step(M.gait_commands(M.GaitParams(), i * cfg.dt, 4, 4), latency=True)
+        out[mode] = sim.get_state_arrays(0, 1)
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
