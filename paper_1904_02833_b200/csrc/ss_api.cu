@@ -907,7 +907,7 @@ static void plan_partition(PlanBuild& B, const Dims& D, const std::vector<int>& 
   P.oDyn = take(P.MS); P.oBdn = take(P.MS); P.oBdf = take(2 * P.MS);
   P.oResD = take(P.MD); P.oResA = take(3 * P.MA); P.oResH = take(5 * P.MH);
   P.oU = take(P.MDOFX); P.oV = take(P.MDOFX); P.oAng = take(9 * P.MB);
-  P.oRed = take(16 * Cg);
+  P.oRed = take(32 * Cg);  // [16 slots][C][value, tag]
   P.smem_doubles = off;
   B.smem_bytes = 8 * (size_t)off;
 }

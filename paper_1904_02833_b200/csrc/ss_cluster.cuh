@@ -86,12 +86,18 @@ DI double cl_tree16(const double* src, int n) {
 // CTA): per-warp shuffle trees (N independent chains), the CL_THREADS/32 warp
 // partials combined by N*C threads at once — thread (q, dst) evaluates value
 // q's warp tree and pushes the CTA partial to slot (slot + q) mod 16 of CTA
-// dst (DSMEM store) — one cluster barrier, then the C partials combined by
-// the same tree. The sums are bitwise those of the former shuffle-tree
-// implementation (warp 0 reducing, then broadcasting), with one
-// __syncthreads and two shuffle trees fewer on the critical path
-// (tools/micro/cluster_sync.cu). Slots rotate over 16, so a slot is
-// rewritten only 15 barriers later.
+// dst — then the C partials combined by the same tree. The sums are bitwise
+// those of the former shuffle-tree implementation (warp 0 reducing, then
+// broadcasting).
+// Exchange: each partial travels as ONE 16-byte DSMEM store {value, tag}
+// (tag = this launch's reduction count, from 1; every CTA zeroes its box at
+// kernel start, before the first cluster barrier) and the consumer threads
+// poll their own box until every source's tag is present — no cluster
+// barrier (tools/micro/cluster_sync.cu: sum3 with the barrier 3.5k cycles,
+// tagged polling 1.9k). Slot reuse is safe: a CTA writes reduction r + 2
+// only after finishing r + 1, which needs every CTA's r + 1 partial, which
+// each CTA sends only after reading its r values. SS_CL_BARRIER_SUM keeps the
+// barrier exchange (single doubles, [16][C] box).
 template <int N>
 DI void cl_cluster_sumN(const ClPlan& L, const ClSmem& S, const double* v, int slot,
                         double* scratch, double* out) {
@@ -112,6 +118,7 @@ DI void cl_cluster_sumN(const ClPlan& L, const ClSmem& S, const double* v, int s
   __syncthreads();
   const int rank = (int)cg::this_cluster().block_rank();
   static_assert(NW == 16, "warp tree over 16 warp partials");
+#ifdef SS_CL_BARRIER_SUM
   if ((int)threadIdx.x < N * L.C) {
     const int q = threadIdx.x / L.C, dst = threadIdx.x - q * L.C;
     S.peer[dst][L.oRed + ((slot + q) & 15) * L.C + rank] = cl_tree16(scratch + q * NW, NW);
@@ -122,6 +129,32 @@ DI void cl_cluster_sumN(const ClPlan& L, const ClSmem& S, const double* v, int s
     scratch[48 + q] = cl_tree16(S.b + L.oRed + ((slot + q) & 15) * L.C, L.C);
   }
   __syncthreads();
+#else
+  const double tag = scratch[60] + 1.0;  // reductions of this launch so far + 1
+  if ((int)threadIdx.x < N * L.C) {
+    const int q = threadIdx.x / L.C, dst = threadIdx.x - q * L.C;
+    const double t = cl_tree16(scratch + q * NW, NW);
+    double* bx = S.peer[dst] + L.oRed + 2 * (((slot + q) & 15) * L.C + rank);
+    *reinterpret_cast<double2*>(bx) = make_double2(t, tag);
+  }
+  if ((int)threadIdx.x < N * L.C) {
+    const int q = threadIdx.x / L.C, src = threadIdx.x - q * L.C;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(S.b + L.oRed +
+                                                         2 * (((slot + q) & 15) * L.C + src));
+    double val, g;
+    do {
+      asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(val), "=d"(g) : "r"(a) : "memory");
+    } while (g != tag);
+    scratch[64 + 16 * q + src] = val;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < N) {
+    const int q = threadIdx.x;
+    scratch[48 + q] = cl_tree16(scratch + 64 + 16 * q, L.C);
+  }
+  if (threadIdx.x == 0) scratch[60] = tag;
+  __syncthreads();
+#endif
 #pragma unroll
   for (int q = 0; q < N; ++q) out[q] = scratch[48 + q];
 }
@@ -675,6 +708,10 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_newton_cluster(const Ctx c, c
     mn.hp1 = hptr[n + 1];
   }
 
+  // ---- reduction box and counter (cl_cluster_sumN): zeroed before the first
+  // cluster barrier, so no tag of an earlier launch is ever read
+  for (int r = tid; r < 32 * L.C; r += CL_THREADS) sb[L.oRed + r] = 0.0;
+  if (tid == 0) scratch[60] = 0.0;
   // ---- dead rows = 0 (d = 1): init every row, elements overwrite theirs
   for (int r = tid; r < L.NR; r += CL_THREADS) {
     sb[L.oZ + r] = 0.0;

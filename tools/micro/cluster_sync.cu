@@ -81,6 +81,44 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(T, 1) k(long long* 
       asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     } else if (mode == 8) {
       __syncthreads();
+    } else if (mode == 9) {
+      // sum3 with tagged 16-byte DSMEM words polled by the consumers instead
+      // of a cluster barrier (two parity buffers of [3][16] {value, tag})
+      double w[3] = {acc, acc + 1, acc + 2};
+      for (int q = 0; q < 3; ++q)
+        for (int o = 16; o > 0; o >>= 1) w[q] += __shfl_down_sync(0xffffffffu, w[q], o);
+      const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
+      if (l == 0)
+        for (int q = 0; q < 3; ++q) scratch[q * 16 + wi] = w[q];
+      __syncthreads();
+      const double tag = (double)(it + 1);
+      double* box = sm + 8192 + 256 + (it & 1) * 96;  // [3][16][2]
+      if (threadIdx.x < 48) {
+        const int q = threadIdx.x >> 4, dst = threadIdx.x & 15;
+        double t = 0.0;
+        for (int i = 0; i < 16; ++i) t += scratch[q * 16 + i];
+        double* rb = peers[dst] + 8192 + 256 + (it & 1) * 96 + (q * 16 + rank) * 2;
+        unsigned long long ra;
+        asm volatile("cvta.to.shared.u64 %0, %1;" : "=l"(ra) : "l"(rb));
+        asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"l"(ra), "d"(t), "d"(tag) : "memory");
+      }
+      if (threadIdx.x < 48) {
+        const int q = threadIdx.x >> 4, src = threadIdx.x & 15;
+        const double* mine = box + (q * 16 + src) * 2;
+        double v, g;
+        do {
+          asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(g) : "r"((unsigned)__cvta_generic_to_shared(mine)) : "memory");
+        } while (g != tag);
+        scratch[48 + threadIdx.x] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int i = 0; i < 16; ++i) t += scratch[48 + threadIdx.x * 16 + i];
+        scratch[96 + threadIdx.x] = t;
+      }
+      __syncthreads();
+      acc += scratch[96] * 1e-30;
     }
   }
   const long long t1 = clock64();
@@ -92,14 +130,15 @@ int main() {
   long long* d;
   cudaMalloc(&d, 128 * sizeof(long long));
   const size_t smem = (8192 + 512) * 8;
+  cudaMemset(d, 0, 128 * sizeof(long long));
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const char* names[] = {"cl.sync only", "remote st + sync", "own-window st + sync", "local st + sync",
                          "sum3 pattern", "arrive.rel/wait.acq", "arrive.relaxed/wait",
-                         "remote st + rel/acq", "__syncthreads"};
-  for (int mode = 0; mode < 9; ++mode) {
+                         "remote st + rel/acq", "__syncthreads", "sum3 tagged polling"};
+  for (int mode = 0; mode < 10; ++mode) {
     for (int nst : {0, 2, 7}) {
-      if ((mode == 0 || mode == 4 || mode == 5 || mode == 6 || mode == 8) && nst) continue;
+      if ((mode == 0 || mode == 4 || mode == 5 || mode == 6 || mode == 8 || mode == 9) && nst) continue;
       k<<<16, T, smem>>>(d, mode, nst);
       long long h[16];
       cudaError_t e = cudaMemcpy(h, d, 16 * sizeof(long long), cudaMemcpyDeviceToHost);
