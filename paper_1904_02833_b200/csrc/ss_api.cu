@@ -4,6 +4,7 @@
 // reference accumulation order, compliance pattern), device memory, the
 // per-frame launch sequence captured once into a CUDA graph, state I/O.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -144,6 +145,8 @@ struct ss_handle {
   int stepjt = 0;            // k_step_jt (step + tet J^T z in one pass; SS_STEPJT)
   int newton2 = 0;           // k_newton_rhs2 / k_newton_final2 (SS_NEWTON2)
   int gy_dir2 = 1;
+  int apply3 = 0;            // k_apply_rows3 (TMA-staged tet operands; SS_APPLY3)
+  std::vector<TmApply> tm_apply;  // its tensor maps, per wave
   int gather_bulk = 0;       // k_gather_bulk (one large mesh: TMA bulk-copied tC; SS_GATHER_BULK)
   int gbulk_grid = 0;
   JtgPlan jplan{};           // k_jtg plan (fixed at ss_create)
@@ -198,8 +201,8 @@ const char* const kKernelNames[] = {"k_frame_begin", "k_pre",        "k_slots", 
                                     "k_tet_jt",      "k_newton_cluster", "k_gather_fused",
                                     "k_apply_rows_async", "k_jtg", "k_apply_rows2",
                                     "k_pcr_dir_rows", "k_eval_polar", "k_step_jt",
-                                    "k_newton_rhs2", "k_newton_final2", "k_gather_bulk"};
-constexpr int kNumKernels = 24;
+                                    "k_newton_rhs2", "k_newton_final2", "k_gather_bulk", "k_apply_rows3"};
+constexpr int kNumKernels = 25;
 struct Prof {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
 };
@@ -242,11 +245,39 @@ int kid(const char* name) {
     ++n;                                                                 \
   } while (0)
 
+// 3-D tensor map of a [K][nt][E] double field (env innermost) with
+// {32 envs, 4 tets, K rows} boxes (k_apply_rows3)
+static int make_tmap3(CUtensorMap* m, const double* base, int E, int nt, int K) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        !fn)
+      return -1;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)E, (cuuint64_t)nt, (cuuint64_t)K};
+  cuuint64_t strides[2] = {(cuuint64_t)E * 8, (cuuint64_t)nt * E * 8};
+  cuuint32_t box[3] = {32, 4, (cuuint32_t)K};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
 // grid rows of k_apply_rows2 / k_newton_final2 and k_pcr_dir_rows: one
 // resident wave at their occupancy (the partial buffer is sized for them)
 static void set_gy2(ss_handle* H, const Dims& D) {
   int occ_a = 3, occ_d = 4, sms = 148;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_apply_rows2, SS_THREADS, 0);
+  if (env_long("SS_APPLY3", 0)) {  // k_apply_rows3 shares the grid: its residency bounds it
+    int occ_a3 = occ_a;
+    cudaFuncSetAttribute(k_apply_rows3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kA3Smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a3, k_apply_rows3, SS_THREADS, kA3Smem);
+    occ_a = std::min(occ_a, std::max(1, occ_a3));
+  }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_pcr_dir_rows, SS_THREADS, 0);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
   const long rows_el = ((long)D.nd + D.nt + D.na + D.nh + D.ns + 3) / 4;  // tet pairs bound
@@ -285,7 +316,7 @@ static JtgPlan jtg_plan(const Dims& D) {
 // structured application (default).
 template <bool EX>
 int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd, int latency,
-                    int* nl, Prof* prof) {
+                    int* nl, Prof* prof, const TmApply* tma) {
   const Dims& D = c.D;
   cudaStream_t st = H->stream;
   const dim3 blk(SS_THREADS);
@@ -406,7 +437,9 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   } while (0)
 #define APPLY(setup_)                                                        \
   do {                                                                       \
-    if (!EX && H->apply2)                                                    \
+    if (!EX && tma)                                                          \
+      LAUNCH_SM(k_apply_rows3, g_red2, kA3Smem, c, setup_, *tma);            \
+    else if (!EX && H->apply2)                                               \
       LAUNCH(k_apply_rows2, g_red2, c, setup_);                              \
     else if (!EX && H->apply_async)                                          \
       LAUNCH_SM(k_apply_rows_async, g_red, H->apply_async_smem, c, setup_);  \
@@ -471,8 +504,9 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
 int enqueue_frame(ss_handle* H, int w, int has_cmd, int latency, int* nl, Prof* prof = nullptr) {
   const Ctx& c = H->wave[w];
   const double* d_cmd = H->d_cmd + (size_t)w * H->c.D.E * std::max(1, H->c.D.links);
-  return H->c.p.exact_j ? enqueue_frame_t<true>(H, c, d_cmd, has_cmd, latency, nl, prof)
-                        : enqueue_frame_t<false>(H, c, d_cmd, has_cmd, latency, nl, prof);
+  const TmApply* tma = H->apply3 ? &H->tm_apply[w] : nullptr;
+  return H->c.p.exact_j ? enqueue_frame_t<true>(H, c, d_cmd, has_cmd, latency, nl, prof, tma)
+                        : enqueue_frame_t<false>(H, c, d_cmd, has_cmd, latency, nl, prof, tma);
 }
 
 int get_graph(ss_handle* H, int w, int has_cmd, int latency, cudaGraphExec_t* out) {
@@ -1812,6 +1846,23 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   // opt-in: no gain measured (coupled 2-snake frame 6.16 ms either way; 1024 envs and
   // the 1M-tet scene within noise, profiles/r2_summary.md)
   H->pdl = (int)env_long("SS_PDL", 0);
+  // k_apply_rows3: the q / compact J / tet-row z tensor maps of every wave.
+  // Opt-in (SS_APPLY3=1): bitwise k_apply_rows2, 32.5 vs 32.65 ms/frame on its
+  // own at 1024 envs, but the whole two-lane step 7,058-7,070 vs 7,088-7,106
+  // snake-steps/s (its 50 KB of shared memory per CTA); a 3-stage ring took
+  // the u gather's L1 (6,315). The apply waits on the gathered u, not on q/S/z.
+  if (H->apply2 && D.W == 32 && D.E % 32 == 0 && env_long("SS_APPLY3", 0)) {
+    H->tm_apply.resize(H->n_waves);
+    int bad = 0;
+    for (int w = 0; w < H->n_waves; ++w) {
+      const Ctx& cw = H->wave[w];
+      bad |= make_tmap3(&H->tm_apply[w].q, cw.S.quat, D.E, D.nt, 4);
+      bad |= make_tmap3(&H->tm_apply[w].s, cw.K.tS, D.E, D.nt, 6);
+      bad |= make_tmap3(&H->tm_apply[w].z, cw.K.z + (size_t)D.ot * D.E, D.E, D.nt, 6);
+    }
+    H->apply3 = bad ? 0 : 1;
+    if (bad) H->tm_apply.clear();
+  }
   // one large mesh: the J^T x gather streams each warp's tet-run range of the
   // incidence-order column sums with bulk copies (bitwise the serial walk)
   if (D.tc_inbox && env_long("SS_GATHER_BULK", 1)) {

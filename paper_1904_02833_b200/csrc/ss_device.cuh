@@ -17,6 +17,7 @@
 // sums are bitwise the numba block_transpose sums. PCR scalars are per
 // environment, reduced deterministically (fixed tree + fixed block order).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -2833,6 +2834,272 @@ __global__ void __launch_bounds__(SS_THREADS, SS_APPLY2_MINB) k_apply_rows2(cons
       y[5] = 0.5 * ((G[1] + G[3]) - (ws01 + ws10));
       ereg6(ed, eo, es, zz, ez);
       double* ap = c.K.az + ((unsigned)c.D.ot * uE + tb);
+      if (tw_act) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double az = y[i] + ez[i];
+          ap[i * ntE] = az;
+          part += zz[i] * az;
+        }
+      }
+    }
+    buf ^= 1;
+  }
+  // ---- every other item (distance, attachment, hinge, contact slot rows)
+  const int n_other = nd + na + nh + ns;
+  for (int q2 = blockIdx.y * IL + il; q2 < n_other; q2 += gridDim.y * IL) {
+    int it = q2 < nd ? q2 : q2 + nt;
+    if (it < nd) {
+      const int row = c.D.od + it;
+      const double zr = z[IX(row)];
+      const double az = row_dist(c, it, u, env) + c.T.d_dyn[it] * zr;
+      c.K.az[IX(row)] = az;
+      part += zr * az;
+    } else if (it < nd + nt + na) {
+      const int a = it - nd - nt;
+      double y[3];
+      rows_att(c, a, u, env, y);
+      const double dyn = c.T.a_dyn[a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int row = c.D.oa + i * na + a;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else if (it < nd + nt + na + nh) {
+      const int hh = it - nd - nt - na;
+      double y[5];
+      rows_hinge(c, hh, u, env, y);
+      const double dyn = c.T.h_dyn[hh];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int row = c.D.oh + i * nh + hh;
+        const double zr = z[IX(row)];
+        const double az = y[i] + dyn * zr;
+        c.K.az[IX(row)] = az;
+        part += zr * az;
+      }
+    } else {
+      const int s = it - nd - nt - na - nh;
+      if (!c.K.present[IX(s)]) continue;
+      const int rn = c.D.on + s, rf0 = c.D.of + s, rf1 = c.D.of + ns + s;
+      const double zn = z[IX(rn)], z0 = z[IX(rf0)], z1 = z[IX(rf1)];
+      double y[3];
+      rows_slot(c, s, u, env, y);
+      const double an = y[0] + c.K.dynn[IX(s)] * zn;
+      double a0 = z0, a1 = z1;
+      if (c.K.actf[IX(s)] != 0.0) {
+        a0 = y[1] + c.p.fdyn * z0;
+        a1 = y[2] + c.p.fdyn * z1;
+      }
+      c.K.az[IX(rn)] = an;
+      c.K.az[IX(rf0)] = a0;
+      c.K.az[IX(rf1)] = a1;
+      part += zn * an;
+      part += z0 * a0;
+      part += z1 * a1;
+    }
+  }
+  double tot;
+  if (reduce_env(c, part, &tot)) {
+    if (setup) {
+      c.K.rho[env] = tot;
+    } else if (!c.K.broken[env]) {
+      const double rho = c.K.rho[env];
+      c.K.beta[env] = rho > 1e-300 ? tot / rho : 0.0;
+      c.K.rho[env] = tot;
+    }
+  }
+}
+
+// k_apply_rows2 with the streaming tet operands moved by the Tensor Memory
+// Accelerator. A CTA's four warp pairs take four consecutive tets of the
+// same 32 env lanes per iteration, so the quaternion rows [4][nt][E], the
+// compact J [6][nt][E] and the tet rows of z [6][nt][E] of one iteration are
+// three 3-D boxes {32 envs, 4 tets, 4/6 rows} (16 KB): thread 0 issues them
+// with cp.async.bulk.tensor (one CUtensorMap per field and wave, created at
+// ss_create) SS_APPLY3_NST iterations ahead into a shared-memory ring; a
+// stage's arrival completes its `full` mbarrier (transaction bytes), and
+// every warp arrives on its `empty` mbarrier once its operands are in
+// registers, which lets thread 0 refill it. The warps no longer wait a
+// global round trip for q, S, z; only the gathered u (L1/L2) stays on the
+// load path. Arithmetic, order and stores are k_apply_rows2's (az bitwise,
+// rho bitwise the two-warp kernel's: same thread assignment).
+#ifndef SS_APPLY3_NST
+#define SS_APPLY3_NST 2
+#endif
+#ifndef SS_APPLY3_MINB
+#define SS_APPLY3_MINB 3
+#endif
+struct TmApply {
+  CUtensorMap q, s, z;
+};
+constexpr int kA3Box = 16 * 4 * 32;  // doubles per stage: q(4) S(6) z(6) rows x 4 tets x 32 lanes
+constexpr size_t kA3Smem = (size_t)SS_APPLY3_NST * kA3Box * 8;
+DI void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
+      : "memory");
+}
+DI void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+DI void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+               "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(SS_THREADS, SS_APPLY3_MINB) k_apply_rows3(
+    const Ctx c, int setup, const __grid_constant__ TmApply tm) {
+  SETUP
+  __shared__ double gsh[4][2][9][32];  // [pair][buffer][G entry][env lane]
+  __shared__ uint64_t full[SS_APPLY3_NST], empty[SS_APPLY3_NST];
+  extern __shared__ __align__(128) double a3[];
+  const int nd = c.D.nd, nt = c.D.nt, na = c.D.na, nh = c.D.nh, ns = c.D.ns;
+  const double* u = c.K.u;
+  const double* z = c.K.z;
+  TW_SETUP
+  const unsigned uE = (unsigned)E;
+  double part = 0.0;
+  int buf = 0;
+  const int tstride = tw_stride;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SS_APPLY3_NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], SS_THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // CTA-uniform trip count (every warp arrives on every stage's empty barrier)
+  const int t_cta = blockIdx.y * 4;
+  const int niter = nt > t_cta ? (nt - t_cta + tstride - 1) / tstride : 0;
+  const int env0 = blockIdx.x * 32;
+  auto issue = [&](int j) {
+    const int s = j % SS_APPLY3_NST;
+    double* st = a3 + (size_t)s * kA3Box;
+    const int t0 = t_cta + j * tstride;
+    mbar_expect_tx(&full[s], kA3Box * 8);
+    tma_load_3d(st, &tm.q, env0, t0, 0, &full[s]);
+    tma_load_3d(st + 512, &tm.s, env0, t0, 0, &full[s]);
+    tma_load_3d(st + 1280, &tm.z, env0, t0, 0, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < SS_APPLY3_NST && j < niter; ++j) issue(j);
+  }
+  // warp A: the next item's node ids one item ahead
+  int nid_n[4] = {0, 0, 0, 0};
+  {
+    const int t0 = tw_base + tw_off;
+    if (role == 0 && t0 < nt) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) nid_n[v] = c.T.t_idx[v * nt + t0];
+    }
+  }
+  for (int j = 0; j < niter; ++j) {
+    if (threadIdx.x == 0 && j >= 1 && j - 1 + SS_APPLY3_NST < niter) {
+      // refill the stage every warp released in iteration j - 1
+      const int sp = (j - 1) % SS_APPLY3_NST;
+      while (!mbar_try_wait(&empty[sp], (uint32_t)(((j - 1) / SS_APPLY3_NST) & 1))) {
+      }
+      issue(j - 1 + SS_APPLY3_NST);
+    }
+    const int t = t_cta + pair + j * tstride;
+    const bool tw_act = t < nt;
+    const int tc = tw_act ? t : nt - 1;
+    const int s = j % SS_APPLY3_NST;
+    const double* st = a3 + (size_t)s * kA3Box;
+    while (!mbar_try_wait(&full[s], (uint32_t)((j / SS_APPLY3_NST) & 1))) {
+    }
+    double* g = &gsh[pair][buf][0][tw_slot];
+    if (role == 0) {
+      double uv[12], q[4], Ri[9];
+      int nid[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) nid[v] = nid_n[v];
+      if (t + tstride < nt) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) nid_n[v] = c.T.t_idx[v * nt + t + tstride];
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const double* up = u + ((unsigned)(3 * nid[v]) * uE + (unsigned)env);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) uv[3 * v + a] = up[a * uE];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = st[(k * 4 + pair) * 32 + tw_slot];
+      __syncwarp();
+      if (tw_slot == 0) mbar_arrive(&empty[s]);
+      tet_rinv(c, tc, Ri);
+      double du[9];
+#pragma unroll
+      for (int v = 1; v < 4; ++v)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) du[3 * (v - 1) + a] = uv[3 * v + a] - uv[a];
+      double L[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj)
+          L[3 * a + jj] = dot3(du[a], Ri[jj], du[3 + a], Ri[3 + jj], du[6 + a], Ri[6 + jj]);
+      double R[9];
+      quat_to_mat(q[0], q[1], q[2], q[3], R);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj)
+          g[(3 * i + jj) * 32] = dot3(R[i], L[jj], R[3 + i], L[3 + jj], R[6 + i], L[6 + jj]);
+      named_bar(1 + pair, 64);
+    } else {
+      double sv[6], zz[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sv[k] = st[512 + (k * 4 + pair) * 32 + tw_slot];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) zz[i] = st[1280 + (i * 4 + pair) * 32 + tw_slot];
+      __syncwarp();
+      if (tw_slot == 0) mbar_arrive(&empty[s]);
+      const double ed = c.T.t_e3[tc], eo = c.T.t_e3[nt + tc], es = c.T.t_e3[2 * nt + tc];
+      double S[9], Ki[9];
+      S[0] = sv[0]; S[4] = sv[1]; S[8] = sv[2];
+      S[5] = sv[3]; S[7] = sv[3];
+      S[2] = sv[4]; S[6] = sv[4];
+      S[1] = sv[5]; S[3] = sv[5];
+      tet_kinv(S, Ki);
+      named_bar(1 + pair, 64);
+      double G[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) G[k] = g[k * 32];
+      const double g0 = G[7] - G[5], g1 = G[2] - G[6], g2 = G[3] - G[1];
+      const double w0 = dot3(Ki[0], g0, Ki[1], g1, Ki[2], g2);
+      const double w1 = dot3(Ki[3], g0, Ki[4], g1, Ki[5], g2);
+      const double w2 = dot3(Ki[6], g0, Ki[7], g1, Ki[8], g2);
+      const double ws00 = __fma_rn(w1, S[6], -w2 * S[3]);
+      const double ws01 = __fma_rn(w1, S[7], -w2 * S[4]);
+      const double ws02 = __fma_rn(w1, S[8], -w2 * S[5]);
+      const double ws10 = __fma_rn(w2, S[0], -w0 * S[6]);
+      const double ws11 = __fma_rn(w2, S[1], -w0 * S[7]);
+      const double ws12 = __fma_rn(w2, S[2], -w0 * S[8]);
+      const double ws20 = __fma_rn(w0, S[3], -w1 * S[0]);
+      const double ws21 = __fma_rn(w0, S[4], -w1 * S[1]);
+      const double ws22 = __fma_rn(w0, S[5], -w1 * S[2]);
+      double y[6], ez[6];
+      y[0] = G[0] - ws00;
+      y[1] = G[4] - ws11;
+      y[2] = G[8] - ws22;
+      y[3] = 0.5 * ((G[5] + G[7]) - (ws12 + ws21));
+      y[4] = 0.5 * ((G[2] + G[6]) - (ws02 + ws20));
+      y[5] = 0.5 * ((G[1] + G[3]) - (ws01 + ws10));
+      ereg6(ed, eo, es, zz, ez);
+      const unsigned tb = (unsigned)tc * uE + (unsigned)env;
+      double* ap = c.K.az + ((unsigned)c.D.ot * uE + tb);
+      const unsigned ntE = (unsigned)nt * uE;
       if (tw_act) {
 #pragma unroll
         for (int i = 0; i < 6; ++i) {

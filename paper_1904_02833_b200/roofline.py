@@ -36,7 +36,8 @@ def bytes_per_launch_per_env(kernel: str, d: dict, nc: float, structured: bool =
     PCR budget, for the per-launch average over one solve (pcr k_pcr_dir
     launches, pcr - 1 k_pcr_step launches)."""
     # round-2 kernels that move the same operands as their round-1 twins
-    kernel = {"k_apply_rows2": "k_apply_rows", "k_apply_rows_async": "k_apply_rows",
+    kernel = {"k_apply_rows2": "k_apply_rows", "k_apply_rows3": "k_apply_rows",
+              "k_apply_rows_async": "k_apply_rows",
               "k_pcr_dir_rows": "k_pcr_dir", "k_newton_rhs2": "k_newton_rhs",
               "k_newton_final2": "k_newton_final", "k_gather_bulk": "k_gather"}.get(kernel, kernel)
     rows = d["ms"] + 3 * nc                      # rows a PCR kernel touches

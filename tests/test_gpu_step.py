@@ -610,3 +610,35 @@ def test_gather_bulk_bitwise(exact):
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("n", [64, 96, 1024])
+def test_apply3_bitwise(n):
+    """k_apply_rows3 (opt-in SS_APPLY3=1: tet operands staged by TMA
+    tensor-tile loads into a shared-memory ring) against k_apply_rows2: the
+    same expressions on the same thread assignment, so the whole state is
+    bitwise equal."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(23)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_APPLY3"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_APPLY3", None)
+        prof = sim.profile_frames(cmds[0], True, 1)
+        assert (prof["k_apply_rows3"][1] > 0) == (mode == "1")
+        assert (prof["k_apply_rows2"][1] > 0) == (mode == "0")
+        for c in cmds[1:]:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
