@@ -146,17 +146,30 @@ def cpu_oracle_rate(frames_per_core: int, cores: int | None = None):
 
 
 def numba_calibration(port_rate: float) -> dict:
-    """The reference's own numba path cannot run on the GPU box (it is not
-    installed there); profiles/cpu_calibration.json holds both measured on
-    one host (tools/cpu_calibration.py). Scale the port's rate by it."""
-    path = os.path.join(ROOT, "profiles", "cpu_calibration.json")
-    if not os.path.exists(path):
-        return {}
-    cal = json.load(open(path))
-    r = float(cal["port_over_numba_aggregate"])
-    return {"numba_equivalent_value": port_rate / r, "port_over_numba": r,
-            "calibration": "profiles/cpu_calibration.json (numba reference vs this port, "
-                           f"{cal['host_cores']} pinned processes on one host)"}
+    """The reference's own numba path beside the port: measured on a B200
+    box's host cores (profiles/cpu_host_numba.json: the unmodified reference
+    package from baseline/_ref, one pinned process per core,
+    tools/cpu_calibration.py --box), and the port/numba ratio of that run
+    applied to this run's port rate (numba_equivalent_value). Falls back to
+    the build-container calibration (profiles/cpu_calibration.json)."""
+    out = {}
+    for name in ("cpu_host_numba.json", "cpu_calibration.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        if not os.path.exists(path):
+            continue
+        cal = json.load(open(path))
+        r = float(cal["port_over_numba_aggregate"])
+        out = {"numba_equivalent_value": port_rate / r, "port_over_numba": r,
+               "calibration": f"profiles/{name} (numba reference vs this port, "
+                              f"{cal['host_cores']} pinned processes, {cal.get('host', 'one host')})"}
+        if name == "cpu_host_numba.json":
+            out["numba_reference_on_gpu_box_host"] = {
+                "value": round(float(cal["numba"]["aggregate_all_cores"]), 2),
+                "unit": "snake-steps/s", "cores": int(cal["host_cores"]),
+                "per_core_1proc": round(float(cal["numba"]["per_core_1proc"]), 3),
+                "measured": cal.get("when"), "cpu": cal.get("cpu_model")}
+        break
+    return out
 
 
 def run_reference(args):
