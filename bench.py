@@ -374,12 +374,13 @@ def main():
     # the reference-layout byte model beside this build's own
     survey = roofline.survey_model(d, nc_mean, sim.config.substeps, sim.config.newton_iters, pcr)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp) and not hires:  # traffic.json holds the S-scene capture
+    # traffic.json: the batched S-scene capture (scaled to the envs of one
+    # launch); traffic_H.json: the 1M-tet scene (one env)
+    tp = os.path.join(ROOT, "profiles", "traffic_H.json" if hires else "traffic.json")
+    if os.path.exists(tp):
         tj = json.load(open(tp))
         if tj.get(top) is not None:
-            # scaled to the envs of one launch
-            traffic = float(tj[top]) * (n / waves) / float(tj.get("_envs", 1024))
+            traffic = float(tj[top]) * (1.0 if hires else (n / waves) / float(tj.get("_envs", 1024)))
 
     if rank != 0:
         if dist:

@@ -31,12 +31,24 @@ def _run(case, debug):
     if case in ("streaming", "fused", "bench"):
         env["SS_FUSED"] = "1" if case == "fused" else ("0" if case == "streaming" else "")
         env = {k: v for k, v in env.items() if v != ""}
+    if case == "single":  # one env: incidence-order tC, TMA bulk-copy gather
+        env["SS_GATHER_SPLIT"] = "1"
+    if case == "apply3":  # opt-in TMA tensor-tile apply
+        env["SS_APPLY3"] = "1"
     os.environ.update(env)
     try:
         sc = M.SceneConfig()
         if case == "cluster":
             m = M.build_bend_fixture(sc)
             m.sim.config.solver = "cluster"
+            n = 1
+        elif case == "multicluster":  # coupled 2-snake scene: one cluster per snake
+            m = M.build_snake(sc, n_snakes=2)
+            m.sim.config.solver = "cluster"
+            n = 1
+        elif case == "single":
+            m = M.build_snake(sc)
+            m.sim.config.solver = "streaming"
             n = 1
         else:
             n = 1024 if case == "bench" else 64
@@ -60,7 +72,8 @@ def _run(case, debug):
     return out, bad.value, info
 
 
-@pytest.mark.parametrize("case", ["streaming", "fused", "cluster", "bench"])
+@pytest.mark.parametrize("case", ["streaming", "fused", "cluster", "bench", "multicluster",
+                                  "single", "apply3"])
 def test_guards_intact_and_poison_invisible(case):
     ref, bad0, info0 = _run(case, False)
     got, bad, info = _run(case, True)
@@ -68,8 +81,10 @@ def test_guards_intact_and_poison_invisible(case):
     assert info == info0
     if case == "fused":
         assert info["fused_gather"]
-    if case == "cluster":
+    if case in ("cluster", "multicluster"):
         assert info["cluster"]
+    if case == "multicluster":
+        assert info["clusters_per_env"] == 2
     for k in ref:
         assert np.array_equal(ref[k], got[k], equal_nan=True), k
     assert np.isfinite(got["positions"]).all()

@@ -1,6 +1,6 @@
 """profiles/traffic.json from an ncu --set full report: mean DRAM bytes
 (dram__bytes_read.sum + dram__bytes_write.sum) per launch of each kernel.
-Usage: python tools/traffic_from_ncu.py gpurun_out/s_full.ncu-rep [envs]"""
+Usage: python tools/traffic_from_ncu.py gpurun_out/s_full.ncu-rep [envs] [out name]"""
 import csv
 import io
 import json
@@ -25,7 +25,7 @@ for r in rows[2:]:
 out = {k: sum(v) / len(v) for k, v in acc.items()}
 out["_envs"] = envs
 out["_source"] = os.path.basename(rep)
-path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
-                    "traffic.json")
+name = sys.argv[3] if len(sys.argv) > 3 else "traffic.json"  # traffic_H.json: the 1M-tet scene
+path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", name)
 json.dump(out, open(path, "w"), indent=1)
 print(json.dumps(out, indent=1))
