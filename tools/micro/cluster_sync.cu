@@ -11,8 +11,14 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(T, 1) k(long long* 
   cg::cluster_group cl = cg::this_cluster();
   const int rank = cl.block_rank();
   __shared__ double* peers[16];
-  __shared__ double scratch[64];
+  __shared__ double scratch[128];
+  __shared__ uint64_t mbar2[2];
   if (threadIdx.x < 16) peers[threadIdx.x] = cl.map_shared_rank(sm, threadIdx.x);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&mbar2[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   cl.sync();
   double acc = threadIdx.x;
   long long t0 = 0;
@@ -81,6 +87,36 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(T, 1) k(long long* 
       asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     } else if (mode == 8) {
       __syncthreads();
+    } else if (mode == 10) {
+      // remote stores, fence by the writers, relaxed arrive, acquire wait
+      for (int j = 0; j < nst; ++j) {
+        const int dst = (threadIdx.x + j * 7 + rank) & 15;
+        peers[dst][(threadIdx.x * nst + j) & 8191] = acc + j;
+      }
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else if (mode == 11) {
+      // st.async remote stores completing on the destination's mbarrier; each
+      // CTA waits on its own mbarrier for the bytes it receives (no barrier)
+      // two barriers alternating by iteration: a producer can run at most one
+      // iteration ahead of any consumer (it waits for everyone's bytes)
+      const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar2[it & 1]);
+      if (threadIdx.x == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(T * nst * 8) : "memory");
+      for (int j = 0; j < nst; ++j) {
+        const int dst = (threadIdx.x + j * 7 + rank) & 15;
+        const unsigned la = (unsigned)__cvta_generic_to_shared(sm + (((it & 1) * T * nst + threadIdx.x * nst + j) & 8191));
+        unsigned ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(dst));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(mb), "r"(dst));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(acc + j), "r"(rb) : "memory");
+      }
+      unsigned ok = 0;
+      for (long spin = 0; !ok && spin < (1L << 24); ++spin) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(mb), "r"((unsigned)((it >> 1) & 1)) : "memory");
+      }
+      if (!ok) out[100] = 1;  // timed out
     } else if (mode == 9) {
       // sum3 with tagged 16-byte DSMEM words polled by the consumers instead
       // of a cluster barrier (two parity buffers of [3][16] {value, tag})
@@ -129,14 +165,15 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(T, 1) k(long long* 
 int main() {
   long long* d;
   cudaMalloc(&d, 128 * sizeof(long long));
+  if (getenv("MODE_MIN")) { }
   const size_t smem = (8192 + 512) * 8;
   cudaMemset(d, 0, 128 * sizeof(long long));
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const char* names[] = {"cl.sync only", "remote st + sync", "own-window st + sync", "local st + sync",
                          "sum3 pattern", "arrive.rel/wait.acq", "arrive.relaxed/wait",
-                         "remote st + rel/acq", "__syncthreads", "sum3 tagged polling"};
-  for (int mode = 0; mode < 10; ++mode) {
+                         "remote st + rel/acq", "__syncthreads", "sum3 tagged polling", "remote st + fence + relaxed", "st.async + mbarrier"};
+  for (int mode = 0; mode < 12; ++mode) {
     for (int nst : {0, 2, 7}) {
       if ((mode == 0 || mode == 4 || mode == 5 || mode == 6 || mode == 8 || mode == 9) && nst) continue;
       k<<<16, T, smem>>>(d, mode, nst);
@@ -146,6 +183,7 @@ int main() {
       long long mx = 0, mn = 1LL << 60;
       for (int i = 0; i < 16; ++i) { mx = h[i] > mx ? h[i] : mx; mn = h[i] < mn ? h[i] : mn; }
       printf("%-24s stores/thread %d: %lld..%lld cycles/iter\n", names[mode], nst, mn, mx);
+      fflush(stdout);
     }
   }
   return 0;
