@@ -142,6 +142,7 @@ struct ss_handle {
   int gy_red2 = 1;           // its grid rows (one resident wave)
   int dir2 = 0;              // k_pcr_dir_rows (row-wise, SS_DIR2)
   int polar_split = 0;       // k_eval_polar before k_eval_tet (SS_POLAR_SPLIT)
+  int polar_narrow = 0;      // one env, small mesh: 32-thread CTAs for k_eval_polar (SS_POLAR_NARROW)
   int stepjt = 0;            // k_step_jt (step + tet J^T z in one pass; SS_STEPJT)
   int newton2 = 0;           // k_newton_rhs2 / k_newton_final2 (SS_NEWTON2)
   int gy_dir2 = 1;
@@ -377,7 +378,16 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
     NvtxRange* nv_asm = new NvtxRange("assembly: pre, contacts, eval", prof != nullptr);
     LAUNCH(k_pre, g_pre, c, gait && sub == 0 ? 1 : 0);
     if (D.ns) LAUNCH(k_slots, g_slots, c);
-    if (D.nt && H->polar_split) LAUNCH(k_eval_polar, g_polar, c);
+    if (D.nt && H->polar_split) {
+      if (H->polar_narrow) {
+        // one env: one warp per CTA, so the data-dependent polar loops of a
+        // small mesh spread over every SM instead of ~17 full CTAs
+        const dim3 blk(32);
+        LAUNCH(k_eval_polar, dim3(D.tiles, (D.nt + 31) / 32), c);
+      } else {
+        LAUNCH(k_eval_polar, g_polar, c);
+      }
+    }
     if (D.nt) LAUNCH(k_eval_tet<EX>, g_eval, c, H->polar_split);  // + tet J^T lam
     if (D.nd + D.na + D.nh) LAUNCH(k_eval_misc, g_misc, c);
     if (H->use_cluster) {
@@ -1833,6 +1843,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
       env_long("SS_APPLY2", 1))
     H->apply2 = 1;
   H->polar_split = (int)env_long("SS_POLAR_SPLIT", 1);
+  H->polar_narrow = (D.W == 1 && D.nt <= 32 * 4096 && env_long("SS_POLAR_NARROW", 1)) ? 1 : 0;
   H->newton2 = (H->apply2 && env_long("SS_NEWTON2", 1)) ? 1 : 0;  // needs g_red2 (apply2 plan)
   // opt-in: bitwise equal but 60-68 ms/frame against 58.5 for k_pcr_step +
   // k_tet_jt (the separate kernels run at 0.95 / 0.91 of HBM; the fused one
