@@ -642,3 +642,26 @@ def test_apply3_bitwise(n):
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+def test_polar_narrow_bitwise():
+    """One env: k_eval_polar in 32-thread CTAs (SS_POLAR_NARROW, default)
+    gives bitwise the state of the 256-thread launch (each tet's polar loop
+    is independent of the launch shape)."""
+    import os
+    out = {}
+    for mode in ("0", "1"):
+        parts, cfg = scene_parts("S")
+        cfg.solver = "cluster"
+        os.environ["SS_POLAR_NARROW"] = mode
+        try:
+            sim = M.Simulator(config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_POLAR_NARROW", None)
+        for i in range(3):
+            sim.step(M.gait_commands(M.GaitParams(), i * cfg.dt, 4, 4), latency=True)
+        out[mode] = sim.get_state_arrays(0, 1)
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
