@@ -1233,6 +1233,11 @@ static int plan_cluster(ss_handle* H, const Dims& D, const std::vector<int>& d_i
       H->plan.xbuf = (double*)H->xmem;
       H->plan.xcnt = (int*)((char*)H->xmem + xb);
       H->plan.xn = xn;
+    } else {
+      // the sticky fault flag alone (a bounded reduction wait that expired)
+      CK(cudaMalloc(&H->xmem, 16));
+      CK(cudaMemset(H->xmem, 0, 16));
+      H->plan.xcnt = (int*)H->xmem;
     }
     H->use_cluster = 1;
     return SS_OK;
@@ -2421,7 +2426,7 @@ int ss_solver_info(ss_handle* H, int* info) {
   info[7] = H->fused ? H->fused_chunks : 0;
   info[8] = H->use_cluster ? H->plan.G : 0;
   info[9] = 0;
-  if (H->use_cluster && H->plan.G > 1) {
+  if (H->use_cluster && H->plan.xcnt) {
     CK(cudaStreamSynchronize(H->stream));
     CK(cudaMemcpy(&info[9], H->plan.xcnt, sizeof(int), cudaMemcpyDeviceToHost));
   }

@@ -142,9 +142,15 @@ DI void cl_cluster_sumN(const ClPlan& L, const ClSmem& S, const double* v, int s
     const unsigned a = (unsigned)__cvta_generic_to_shared(S.b + L.oRed +
                                                          2 * (((slot + q) & 15) * L.C + src));
     double val, g;
-    do {
+    const long long t0 = clock64();
+    while (true) {
       asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(val), "=d"(g) : "r"(a) : "memory");
-    } while (g != tag);
+      if (g == tag) break;
+      if (clock64() - t0 > (1LL << 32)) {  // never when every CTA runs: flag, do not hang
+        if (L.xcnt) L.xcnt[0] = 3;
+        break;
+      }
+    }
     scratch[64 + 16 * q + src] = val;
   }
   __syncthreads();
