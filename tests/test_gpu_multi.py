@@ -108,3 +108,35 @@ def test_multi_cluster_matches_single_cluster(monkeypatch):
     b1 = _one(runs["0"][0].get_state_arrays(0, 1))
     assert_state_close(a, b1, what="multi vs single cluster")
     assert runs["1"][0].solver_info["cross_cluster_fault"] == 0
+
+
+@pytest.mark.parametrize("n", [4, 10])
+def test_n_coupled_snakes_vs_oracle(oracle_mod, n):
+    """Table II scenes beyond two snakes, two frames of the default gait
+    from rest against the oracle: 4 snakes run one 16-CTA cluster per snake
+    (cross-cluster sums through global memory), 10 snakes do not fit the
+    148 SMs as clusters and run the streaming kernels at one env lane."""
+    from paper_1904_02833_b200.model import build_scene_parts
+    sc = M.SceneConfig()
+    parts, ns, links, fids = build_scene_parts(sc, n)
+    cfg = sc.solver_config()
+    sim = M.Simulator(config=cfg, **parts)
+    info = sim.solver_info
+    if n == 4:
+        assert info["cluster"] and info["clusters_per_env"] == 4
+    else:
+        assert not info["cluster"]
+    parts_o, *_ = build_scene_parts(sc, n)
+    o = oracle_mod.OracleSim(config=cfg, **parts_o)
+    o.set_state(_one(sim.get_state_arrays(0, 1)))
+    gait = M.GaitParams.from_scene(sc)
+    for f in range(2):
+        cmds = M.gait_commands(gait, f * cfg.dt, 4 * n, 4)
+        st = sim.step(cmds, latency=True)
+        o.step(cmds, True)
+        assert_state_close(_one(sim.get_state_arrays(0, 1)), o.get_state(),
+                           what=f"{n} snakes frame {f}")
+        ref = o.stats()
+        assert (st.newton_iterations, st.pcr_iterations, st.contact_count) == \
+            (ref.newton_iterations, ref.pcr_iterations, ref.contact_count)
+    assert sim.solver_info["cross_cluster_fault"] == 0
