@@ -352,11 +352,14 @@ def main():
     waves = sim.solver_info["waves"]
     structured = not sim.config.exact_jacobian
     pcr = sim.config.pcr_iters
-    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean, structured, pcr) * n / waves
+    epl = max(1, round(n / waves))  # envs per launch
+    topo = lambda k: roofline.topology_bytes_per_launch(k, d, epl)  # noqa: E731
+    per_launch = roofline.bytes_per_launch_per_env(top, d, nc_mean, structured, pcr) * n / waves \
+        + topo(top)
     avg_ms = prof[top][0] / prof[top][1]
     # algorithmic bytes of one frame of every env of this rank (all modelled kernels)
-    step_bytes = sum(roofline.bytes_per_launch_per_env(k, d, nc_mean, structured, pcr)
-                     * (v[1] / args.profile_frames) * n / waves for k, v in prof.items())
+    step_bytes = sum((roofline.bytes_per_launch_per_env(k, d, nc_mean, structured, pcr) * n / waves
+                      + topo(k)) * (v[1] / args.profile_frames) for k, v in prof.items())
     achieved = per_launch / (avg_ms * 1e-3) / 1e9
     # per-kernel table (live CUDA events): algorithmic bytes per launch, mean
     # launch time, achieved GB/s and the fraction of the HBM peak
@@ -364,7 +367,7 @@ def main():
     for k, (kms, kl) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         if kl == 0:
             continue
-        kb = roofline.bytes_per_launch_per_env(k, d, nc_mean, structured, pcr) * n / waves
+        kb = roofline.bytes_per_launch_per_env(k, d, nc_mean, structured, pcr) * n / waves + topo(k)
         kus = 1e3 * kms / kl
         per_kernel[k] = {"ms_per_frame": round(kms / args.profile_frames, 4),
                          "launches_per_frame": kl // args.profile_frames,

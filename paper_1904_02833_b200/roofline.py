@@ -2,9 +2,11 @@
 
 Bytes are the env-private traffic one launch must move per environment if
 every operand is read once and every result written once (fp64 values,
-int32 flags). Scene topology shared by every environment of a batch
-(index arrays, rest-shape inverses, incidence lists, compliance) is
-excluded: it is read by all envs and stays L2-resident. Contact rows count
+int32 flags), plus (topology_bytes_per_launch) the scene topology the
+launch reads once for all its envs — index arrays, rest-shape inverses,
+E_tet, incidence lists: ~0.5 MB for the snake (L2-resident across the
+envs of a batch, negligible), ~100-120 MB per tet kernel for the 1M-tet
+mesh, where one env's launch streams it from HBM. Contact rows count
 only for present contacts (absent slots are skipped by every kernel); `nc`
 is the mean number of present contacts per substep. DESIGN.md §4 derives
 each line; bench.py divides by the live CUDA-event duration.
@@ -113,3 +115,29 @@ def survey_model(d: dict, nc: float, substeps: int = 2, newton: int = 4, pcr: in
     sh_apply = 2 * 4 * idx + F8 * 36 * nt
     shared = substeps * (newton * (applies * sh_apply + 2 * 4 * idx) + 3 * 4 * idx)
     return {"total": float(total), "shared": float(shared), "env_private": float(total - shared)}
+
+
+def topology_bytes_per_launch(kernel: str, d: dict, envs_per_launch: int = 1) -> float:
+    """Scene topology one launch must read once (shared by all its envs):
+    int32 tet indices (16 B/tet), the packed rest inverse (80 B/tet), E_tet
+    (24 B/tet), family index / compliance arrays, incidence lists (4 B per
+    incidence + 20 B per particle). One env of a large mesh also reads the
+    incidence destination of each tet vertex in k_tet_jt (16 B/tet)."""
+    kernel = {"k_apply_rows2": "k_apply_rows", "k_apply_rows3": "k_apply_rows",
+              "k_apply_rows_async": "k_apply_rows", "k_newton_rhs2": "k_newton_rhs",
+              "k_newton_final2": "k_newton_final", "k_gather_bulk": "k_gather",
+              "k_pcr_dir_rows": "k_pcr_dir"}.get(kernel, kernel)
+    nt, nd, na, nh, P, ns = d["nt"], d["nd"], d["na"], d["nh"], d["P"], d["ns"]
+    small = 16 * nd + 16 * na + 16 * nh
+    if kernel in ("k_apply_rows", "k_newton_rhs", "k_eval_tet"):
+        return float((16 + 80 + 24) * nt + small)
+    if kernel == "k_newton_final":
+        return float((80 + 24) * nt + small)
+    if kernel == "k_tet_jt":
+        return float((80 + (16 if envs_per_launch == 1 else 0)) * nt)
+    if kernel == "k_eval_polar":
+        return float((16 + 80) * nt)
+    if kernel == "k_gather":
+        n_inc = 4 * nt + 2 * nd + 2 * na + 2 * nh + 2 * ns
+        return float(4 * n_inc + 20 * P)
+    return 0.0
