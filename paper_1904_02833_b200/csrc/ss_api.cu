@@ -174,6 +174,19 @@ long env_long(const char* name, long dflt) {
   const char* v = getenv(name);
   return v && *v ? atol(v) : dflt;
 }
+// layout of the tet column sums tC: 0 tet-major ([nt][12][E] batched, [12][nt]
+// few lanes), 1 one large mesh in incidence order (a 32-byte sector per
+// incidence), 2 batched incidence order ([n_inc][3][E]: a DOF's tet run is
+// consecutive env lines, gathered without code lookups). The opt-in
+// experimental J^T kernels assume layout 0.
+int tc_mode(const Dims& D) {
+  if (D.E == 1 && env_long("SS_TC_INBOX", 1)) return 1;
+  if (D.W == 32 && env_long("SS_TC_INBOX2", 1) && !env_long("SS_FUSED", 0) &&
+      !env_long("SS_JTG", 0) && !env_long("SS_STEPJT", 0))
+    return 2;
+  return 0;
+}
+
 // Measured on the 1024-env snake (tools/grid_sweep.sh): the PCR row/element
 // kernels gain from 16 CTAs per SM-slot of grid (more independent blocks in
 // flight: k_pcr_step 49.3 -> 45.1 ms/frame), the reducing kernels from
@@ -352,7 +365,8 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
   const double* xc_dl = c.K.az + (size_t)D.ms * D.E;
   // tet column sums in incidence order (one large mesh): separate
   // instantiations of the kernels that write or read them
-  const bool ib = D.tc_inbox != 0;
+  const bool ib = D.tc_inbox == 1;
+  const bool ib2 = D.tc_inbox == 2;
 #define GATHER(mode, xs, xc)                                           \
   do {                                                                 \
     if (ib) {                                                          \
@@ -362,6 +376,8 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       else if (gsp == 4) LAUNCH(k_gather<20>, g_gather, c, mode, xs, xc); \
       else if (gsp == 2) LAUNCH(k_gather<18>, g_gather, c, mode, xs, xc); \
       else LAUNCH(k_gather<17>, g_gather, c, mode, xs, xc);               \
+    } else if (ib2) {                                                  \
+      LAUNCH(k_gather<33>, g_gather, c, mode, xs, xc);                   \
     } else {                                                           \
       if (gsp == 8) LAUNCH(k_gather<8>, g_gather, c, mode, xs, xc);       \
       else if (gsp == 4) LAUNCH(k_gather<4>, g_gather, c, mode, xs, xc);  \
@@ -429,6 +445,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       NvtxRange nv_newton("newton", prof != nullptr);
       if (!EX && H->newton2) {
         if (ib) LAUNCH(k_newton_rhs2<1>, g_el, c);
+        else if (ib2) LAUNCH(k_newton_rhs2<2>, g_el, c);
         else LAUNCH(k_newton_rhs2<0>, g_el, c);
       }
       else LAUNCH(k_newton_rhs<EX>, g_el, c);  // + tet J^T z0
@@ -481,6 +498,7 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
             LAUNCH(k_jtg, dim3(H->jtg_grid), c, jp);
           } else {
             if (D.nt && ib) LAUNCH(k_tet_jt<EX ? 3 : 2>, g_tet, c);
+            else if (D.nt && ib2) LAUNCH(k_tet_jt<EX ? 5 : 4>, g_tet, c);
             else if (D.nt) LAUNCH(k_tet_jt<EX ? 1 : 0>, g_tet, c);
             GATHER(0, xs_z, xc_z);
           }
@@ -491,6 +509,9 @@ int enqueue_frame_t(ss_handle* H, const Ctx& c, const double* d_cmd, int has_cmd
       }
       if (!EX && H->newton2 && ib)
         LAUNCH(k_newton_final2<1>, g_red2, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
+               c.p.pcr == 1 ? 1 : 0);
+      else if (!EX && H->newton2 && ib2)
+        LAUNCH(k_newton_final2<2>, g_red2, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
                c.p.pcr == 1 ? 1 : 0);
       else if (!EX && H->newton2)
         LAUNCH(k_newton_final2<0>, g_red2, c, c.p.pcr > 0 ? 1 : 0, it == c.p.newton - 1 ? 1 : 0,
@@ -1512,7 +1533,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
   D.n_inc = (int)inc.size();
   // one large mesh: tet column sums in incidence order (ss_device.cuh tc_put;
   // SS_TC_INBOX=0 keeps the component-major [12][nt] layout)
-  D.tc_inbox = (D.E == 1 && env_long("SS_TC_INBOX", 1)) ? 1 : 0;
+  D.tc_inbox = tc_mode(D);
 
   // ---- allocations
   ss_handle* H = new ss_handle();
@@ -1694,8 +1715,9 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
     K.ang_inv = A.take<double>(9 * (size_t)D.nb * Es);
     K.res = A.take<double>((size_t)D.ms * Es);
     K.tS = A.take<double>(6 * (size_t)D.nt * Es);
-    K.tC = D.tc_inbox ? A.take<double>(4 * (size_t)D.n_inc)
-                      : A.take<double>(12 * (size_t)D.nt * Es);
+    K.tC = D.tc_inbox == 1 ? A.take<double>(4 * (size_t)D.n_inc)
+         : D.tc_inbox == 2 ? A.take<double>(3 * (size_t)D.n_inc * Es)
+                           : A.take<double>(12 * (size_t)D.nt * Es);
     K.rw = A.take<double>(3 * (size_t)D.na * Es);
     K.hJ = A.take<double>(60 * (size_t)D.nh * Es);
     K.wJ = A.take<double>(18 * (size_t)D.nw * Es);
@@ -1756,6 +1778,7 @@ int ss_create(const ss_topology* t, const ss_params* p, int n_envs, int device,
       D.lgW = 0;
       while ((1 << D.lgW) < D.W) ++D.lgW;
       D.tiles = D.E / D.W;
+      D.tc_inbox = tc_mode(D);
       H->c.D = D;
       H->gy_red = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, H->caps.reduce).y;
       H->gy_dir = (int)grid_items(D, (long)D.nd + D.nt + D.na + D.nh + D.ns, H->caps.dir).y;

@@ -189,8 +189,15 @@ DI void tc_ld4(const double* p, double& a0, double& a1, double& a2) {
 template <int IB = -1>
 DI void tc_put(const Ctx& c, int t, int v, int env, double a0, double a1, double a2) {
   const int E = c.D.E, nt = c.D.nt;
-  if (IB < 0 ? c.D.tc_inbox != 0 : IB == 1) {
+  const int mode = IB < 0 ? c.D.tc_inbox : IB;
+  if (mode == 1) {
     tc_st4(c.K.tC + 4 * (size_t)__ldg(&c.T.tdst[4 * (size_t)t + v]), a0, a1, a2);
+  } else if (mode == 2) {
+    // batched incidence order: [n_inc][3][E], three 256-byte env lines per incidence
+    double* p = c.K.tC + (size_t)__ldg(&c.T.tdst[4 * (size_t)t + v]) * 3 * E + env;
+    p[0] = a0;
+    p[E] = a1;
+    p[2 * (size_t)E] = a2;
   } else {
     c.K.tC[TCX(3 * v, t)] = a0;
     c.K.tC[TCX(3 * v + 1, t)] = a1;
@@ -212,8 +219,14 @@ DI void tc_put12(const Ctx& c, int t, int env, const double* col12) {
 template <int IB = -1>
 DI void tc_get(const Ctx& c, int k, int v, int e, int env, double& a0, double& a1, double& a2) {
   const int E = c.D.E, nt = c.D.nt;
-  if (IB < 0 ? c.D.tc_inbox != 0 : IB == 1) {
+  const int mode = IB < 0 ? c.D.tc_inbox : IB;
+  if (mode == 1) {
     tc_ld4(c.K.tC + 4 * (size_t)k, a0, a1, a2);
+  } else if (mode == 2) {
+    const double* p = c.K.tC + (size_t)k * 3 * E + env;
+    a0 = p[0];
+    a1 = p[E];
+    a2 = p[2 * (size_t)E];
   } else {
     a0 = c.K.tC[TCX(3 * v, e)];
     a1 = c.K.tC[TCX(3 * v + 1, e)];
@@ -1467,9 +1480,14 @@ __global__ void __launch_bounds__(SS_THREADS, SS_GATHER_MINB) k_gather(const Ctx
           constexpr int GU = SS_GATHER_UNROLL;
           for (; k + GU - 1 < tr.y; k += GU) {
             double a[3 * GU];
-            if (IB) {
+            if (IB == 1) {
 #pragma unroll
               for (int j = 0; j < GU; ++j) tc_ld4(tC + 4 * (size_t)(k + j), a[3 * j], a[3 * j + 1], a[3 * j + 2]);
+            } else if (IB == 2) {
+              // incidence order: the run's addresses follow from k, no code lookup
+              const double* p = tC + (size_t)k * 3 * E + env;
+#pragma unroll
+              for (int j = 0; j < 3 * GU; ++j) a[j] = p[(size_t)j * E];
             } else {
 #pragma unroll
               for (int j = 0; j < GU; ++j) {
@@ -3501,7 +3519,7 @@ __global__ void __launch_bounds__(SS_THREADS, SS_STEPJT_MINB) k_step_jt(const Ct
 template <int M>
 __global__ void __launch_bounds__(SS_THREADS, (M & 1) ? 2 : SS_TETJT_MINB) k_tet_jt(const Ctx c) {
   constexpr bool EXACT = (M & 1) != 0;
-  constexpr int IB = (M >> 1) & 1;
+  constexpr int IB = (M >> 1) & 3;
   SETUP
   if (c.K.broken[env]) return;  // z unchanged: tC from the previous pass is still valid
   const int nt = c.D.nt;

@@ -665,3 +665,33 @@ def test_polar_narrow_bitwise():
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("exact", [False, True], ids=["structuredJ", "exactJ"])
+@pytest.mark.parametrize("n", [64, 1024])
+def test_tc_inbox2_bitwise(n, exact):
+    """Batched layouts: tet column sums in incidence order ([n_inc][3][E],
+    SS_TC_INBOX2, default) give bitwise the state of the tet-major layout
+    (the gather adds the same values in the same order)."""
+    import os
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    cfg.exact_jacobian = exact
+    rng = np.random.default_rng(29)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_TC_INBOX2"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_TC_INBOX2", None)
+        for c in cmds:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
