@@ -695,3 +695,31 @@ def test_tc_inbox2_bitwise(n, exact):
         sim.close()
     for k in out["0"]:
         assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
+
+
+def test_pdl_bitwise():
+    """Programmatic dependent launch of the frame kernels (SS_PDL=1, opt-in):
+    every kernel waits for its predecessor's memory before its first read,
+    so the state is bitwise the plain stream order's."""
+    import os
+    n = 64
+    parts, cfg = scene_parts("S")
+    cfg.solver = "streaming"
+    rng = np.random.default_rng(37)
+    bias = rng.uniform(-0.5, 0.5, n)
+    cmds = [np.stack([M.gait_commands(M.GaitParams(turn_bias=b), i * cfg.dt, 4, 4) for b in bias])
+            for i in range(3)]
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["SS_PDL"] = mode
+        try:
+            sim = M.BatchedSimulator(n, config=cfg, **parts)
+            sim._ensure()
+        finally:
+            os.environ.pop("SS_PDL", None)
+        for c in cmds:
+            sim.step(c, latency=True)
+        out[mode] = sim.get_state_arrays()
+        sim.close()
+    for k in out["0"]:
+        assert np.array_equal(out["0"][k], out["1"][k], equal_nan=True), k
