@@ -144,3 +144,45 @@ def test_bench_layout_65536_vs_oracle(oracle_mod):
         assert_state_close(got[e], o.get_state(), tol=STEP_TOL, what=f"env {e}")
         assert sim.get_stats(e, 1)[0].contact_count == o.stats().contact_count, f"env {e}"
     sim.close()
+
+
+def test_bench_layout_1024_exact_jacobian_vs_oracle(oracle_mod):
+    """The bench layout (1024 envs, two 512-lane waves) in exact tet-Jacobian
+    mode (the reference expressions per 6x12 column; the one-thread apply /
+    direction / step kernels at 32-env tiles) against the oracle, one frame,
+    4 envs over both waves."""
+    import dataclasses
+    import torch
+    from bench import env_commands
+    n = 1024
+    spots = (0, 511, 512, 1023)
+    model = M.build_snake(M.SceneConfig(), n_envs=n)
+    sim = model.sim
+    sim.config.exact_jacobian = True  # before the handle exists (_ensure reads it)
+    g = load_golden("step_S.npz")
+    f0 = int(g["frames_captured"][-1])
+    before = golden_frame(g, f0, "before")
+    sim.set_state_arrays(before, 0, 1)
+    sim.capture_initial(0)
+    sim.reset_envs(np.arange(n))
+    info = sim.solver_info
+    assert not info["cluster"] and info["env_lanes"] == 512 and info["waves"] == 2, info
+    cmds = env_commands(n, 1, f0)
+    d_cmds = torch.from_numpy(cmds).to("cuda:0")
+    from paper_1904_02833_b200.model import build_scene_parts
+    sc = M.SceneConfig()
+    parts, *_ = build_scene_parts(sc)
+    cfg = dataclasses.replace(sc.solver_config(), exact_jacobian=True)
+    sim.step_device(d_cmds.data_ptr(), True, 1)
+    sim.synchronize()
+    got = _spot(sim, spots)
+    stats = sim.get_stats()
+    for e in spots:
+        o = oracle_mod.OracleSim(config=cfg, **parts)
+        o.set_state(before)
+        o.step(cmds[0, e], True)
+        assert_state_close(got[e], o.get_state(), what=f"exact env {e} frame 1")
+        assert stats[e].contact_count == o.stats().contact_count
+    # the exact-mode kernels ran (one thread per tet, reference column expressions)
+    prof = sim.profile_frames(cmds[0], True, 1)
+    assert prof["k_apply_rows"][1] > 0 and prof["k_apply_rows2"][1] == 0
